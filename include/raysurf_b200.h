@@ -1,0 +1,160 @@
+/*
+ * raysurf_b200.h -- C ABI of the B200 segment/triangle intersection engine.
+ *
+ * This is the drop-in boundary for the reference's kernel-backend plugin
+ * (raysurf/_backend/__init__.py:15-51, module protocol build_tree /
+ * batch_query / batch_baseline, and the native _core it wraps).  Plain
+ * pointers and sizes only; no torch types.  Every entry point returns an
+ * RS_* status; rs_last_error() gives the message for the calling thread.
+ *
+ * Pointer conventions: `d_` = device (CUDA global memory), `h_` = host
+ * (pinned or pageable).  Arrays are C-contiguous little-endian:
+ *   vertices (n_v,3) f32, triangles (n_t,3) i32, segment starts/ends
+ *   (n_r,3) f32 -- the reference's Mesh / SegmentBatch layouts
+ *   (mesh.py:20-32, engine.py:35-48).
+ * `stream` is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Mapping to the reference (paths under raysurf/):
+ *   rs_build_from_sorted  <- _backend/_compiled.py:27-69 build_tree(mesh, sorted_codes, sorted_ids)
+ *                            and _core.pyx:117-184 construct_range/_climb
+ *   rs_build              <- engine.py:250-268 (centroids, support, quantise,
+ *                            encode, sort) + build_tree, all on device
+ *   rs_query              <- _backend/_compiled.py:72-112 batch_query /
+ *                            _core.pyx:195-352 (dense per-segment rows)
+ *   rs_query_compact      <- batch_query + engine.py:206-215 _assemble
+ *                            (barycentric rows, ascending ray index)
+ *   rs_baseline           <- _backend/_compiled.py:115-140 batch_baseline /
+ *                            _core.pyx:355-433
+ *   rs_tree_download      <- the 12 BvhTree fields (lbvh.py:39-55)
+ *   rs_run_batch_host     <- engine.py:222-290 run_batch on host arrays
+ *                            (copies, build, query, compaction, copies back)
+ */
+#ifndef RAYSURF_B200_H
+#define RAYSURF_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RS_API __attribute__((visibility("default")))
+#else
+#define RS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define RS_OK 0
+#define RS_STACK_OVERFLOW 1 /* -> TraversalStackOverflow(segment_index) (exceptions.py:21-26) */
+#define RS_CUDA_ERROR 2     /* CUDA error or out of device memory (-> MemoryError / RuntimeError) */
+#define RS_INVALID_ARG 3    /* -> ValidationError (exceptions.py:15-18) */
+#define RS_INTERNAL 4       /* internal capacity exceeded (never expected) */
+
+/* modes (_backend/_compiled.py:17-21) */
+#define RS_MODE_BOOLEAN 0
+#define RS_MODE_BARYCENTRIC 1
+#define RS_MODE_COUNT 2
+
+/* tree kinds */
+#define RS_TREE_REFERENCE 0 /* per-axis 63-bit Morton: bit-identical to the reference tree */
+#define RS_TREE_FAST 1      /* isotropic 30-bit Morton: same results, fewer node visits */
+
+typedef struct rs_tree rs_tree;
+
+RS_API int rs_abi_version(void);
+RS_API const char *rs_last_error(void);
+
+/* Build a BVH over a device-resident mesh (all keys computed on device). */
+RS_API int rs_build(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
+             int tree_kind, void *stream, rs_tree **out);
+
+/* Build from caller-sorted Morton keys (device arrays of length n_t):
+ * reproduces _compiled.build_tree field for field. */
+RS_API int rs_build_from_sorted(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
+                         const uint64_t *d_sorted_codes, const int32_t *d_sorted_ids,
+                         void *stream, rs_tree **out);
+
+/* Synchronises `stream`; returns triangle count, root ref, height, kind. */
+RS_API int rs_tree_info(const rs_tree *tree, int64_t *n_tri, int32_t *root, int32_t *height,
+                 int32_t *kind, void *stream);
+
+/* Copy the 12 BvhTree fields into host arrays (sizes per lbvh.py:39-55:
+ * bounds (n,6) f32, the rest (n,) i32).  Any pointer may be NULL. */
+RS_API int rs_tree_download(const rs_tree *tree, float *h_internal_bounds, int32_t *h_child_left,
+                     int32_t *h_child_right, int32_t *h_range_left, int32_t *h_range_right,
+                     int32_t *h_internal_triangle_id, int32_t *h_internal_visit,
+                     float *h_leaf_bounds, int32_t *h_leaf_triangle_id,
+                     int32_t *h_leaf_range_left, int32_t *h_leaf_range_right,
+                     int32_t *h_sorted_triangle_ids, void *stream);
+
+/* Release a tree (stream-ordered). */
+RS_API int rs_free(rs_tree *tree, void *stream);
+
+/* Dense per-segment query, device arrays of n_r rows (row i of each output
+ * is written; unused outputs may be NULL: boolean writes d_detected, count
+ * writes d_counts, barycentric writes d_detected/d_tri/d_dist/d_points).
+ * ref_semantics=1 reproduces the reference's max_collisions flush points
+ * and max_stack overflow exactly (use with a RS_TREE_REFERENCE tree).
+ * Synchronises `stream`.  On RS_STACK_OVERFLOW *bad_segment is the lowest
+ * overflowing row. */
+RS_API int rs_query(const rs_tree *tree, const float *d_starts, const float *d_ends, int64_t n_r,
+             int mode, int max_collisions, int max_stack, int ref_semantics,
+             int32_t *d_detected, int32_t *d_counts, int32_t *d_tri, float *d_dist,
+             float *d_points, int64_t *bad_segment, void *stream);
+
+/* Barycentric query with fused ordered compaction: rows for intersecting
+ * segments only, ray indices ascending (engine.py:206-215).  Output arrays
+ * must hold n_r rows; *n_hits receives the row count.  Synchronises. */
+RS_API int rs_query_compact(const rs_tree *tree, const float *d_starts, const float *d_ends,
+                     int64_t n_r, int max_collisions, int max_stack, int ref_semantics,
+                     int32_t *d_ray_index, float *d_distance, int32_t *d_triangle_id,
+                     float *d_point, int64_t *n_hits, int64_t *bad_segment, void *stream);
+
+/* Traversal statistics (internal-node visits and exact tests, summed over
+ * segments) for the roofline's W32/W64 units.  Synchronises. */
+RS_API int rs_query_stats(const rs_tree *tree, const float *d_starts, const float *d_ends, int64_t n_r,
+                   int mode, int max_collisions, int max_stack, int ref_semantics,
+                   int64_t *internal_visits, int64_t *exact_tests, void *stream);
+
+/* All-pairs baseline (no BVH), device arrays, dense outputs as rs_query. */
+RS_API int rs_baseline(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
+                const float *d_starts, const float *d_ends, int64_t n_r, int mode,
+                int32_t *d_detected, int32_t *d_counts, int32_t *d_tri, float *d_dist,
+                float *d_points, void *stream);
+
+/* Whole run_batch on device arrays: build (tree_kind) + query (+ compaction
+ * for barycentric).  boolean -> d_flags = crossing, count -> d_flags = counts;
+ * barycentric -> d_ray_index/d_distance/d_triangle_id/d_point (n_r rows
+ * capacity), *n_hits.  Synchronises. */
+RS_API int rs_run_batch_device(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
+                        const float *d_starts, const float *d_ends, int64_t n_r, int mode,
+                        int tree_kind, int max_collisions, int max_stack, int32_t *d_flags,
+                        int32_t *d_ray_index, float *d_distance, int32_t *d_triangle_id,
+                        float *d_point, int64_t *n_hits, int64_t *bad_segment, void *stream);
+
+/* Whole run_batch on HOST arrays: mesh H2D, device build, rays streamed in
+ * chunks (H2D / query / D2H overlapped on two streams), results D2H.
+ * Outputs as rs_run_batch_device but host arrays (barycentric rows capacity
+ * n_r).  chunk_rays <= 0 picks the default. */
+RS_API int rs_run_batch_host(const float *h_verts, int64_t n_v, const int32_t *h_tris, int64_t n_t,
+                      const float *h_starts, const float *h_ends, int64_t n_r, int mode,
+                      int tree_kind, int max_collisions, int max_stack, int64_t chunk_rays,
+                      int32_t *h_flags, int32_t *h_ray_index, float *h_distance,
+                      int32_t *h_triangle_id, float *h_point, int64_t *n_hits,
+                      int64_t *bad_segment, void *stream);
+
+/* Device phase timing for rs_run_batch_device (the reference's
+ * ResultSet.timings "construct"/"query", engine.py:238-288): when enabled,
+ * CUDA events on the caller's stream bracket the build and the query kernel;
+ * rs_last_timings returns the last call's milliseconds. */
+RS_API int rs_set_timing(int enable);
+RS_API int rs_last_timings(float *build_ms, float *query_ms);
+
+/* Cumulative number of kernels this library has launched. */
+RS_API long long rs_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAYSURF_B200_H */

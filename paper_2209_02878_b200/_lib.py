@@ -1,0 +1,87 @@
+"""ctypes binding of the engine's C ABI (include/raysurf_b200.h).
+
+The shared library is built in-tree by `make -C paper_2209_02878_b200/csrc`
+(or `__graft_entry__.build()`).  There is no fallback: if the library is
+missing or no CUDA device is present, every compute call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import re
+from pathlib import Path
+
+from .exceptions import TraversalStackOverflow, ValidationError
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libraysurf_b200.so"
+HEADER = PKG.parent / "include" / "raysurf_b200.h"
+
+RS_OK, RS_STACK_OVERFLOW, RS_CUDA_ERROR, RS_INVALID_ARG, RS_INTERNAL = range(5)
+MODE_TAGS = {"boolean": 0, "barycentric": 1, "count": 2}
+TREE_KINDS = {"reference": 0, "fast": 1}
+
+p, i32, i64 = C.c_void_p, C.c_int, C.c_int64
+_SIGS = {
+    "rs_abi_version": (i32, []),
+    "rs_last_error": (C.c_char_p, []),
+    "rs_build": (i32, [p, i64, p, i64, i32, p, p]),
+    "rs_build_from_sorted": (i32, [p, i64, p, i64, p, p, p, p]),
+    "rs_tree_info": (i32, [p, p, p, p, p, p]),
+    "rs_tree_download": (i32, [p] + [p] * 12 + [p]),
+    "rs_free": (i32, [p, p]),
+    "rs_query": (i32, [p, p, p, i64, i32, i32, i32, i32, p, p, p, p, p, p, p]),
+    "rs_query_compact": (i32, [p, p, p, i64, i32, i32, i32, p, p, p, p, p, p, p]),
+    "rs_query_stats": (i32, [p, p, p, i64, i32, i32, i32, i32, p, p, p]),
+    "rs_baseline": (i32, [p, i64, p, i64, p, p, i64, i32, p, p, p, p, p, p]),
+    "rs_run_batch_device": (i32, [p, i64, p, i64, p, p, i64, i32, i32, i32, i32,
+                                  p, p, p, p, p, p, p, p]),
+    "rs_run_batch_host": (i32, [p, i64, p, i64, p, p, i64, i32, i32, i32, i32, i64,
+                                p, p, p, p, p, p, p, p]),
+    "rs_set_timing": (i32, [i32]),
+    "rs_last_timings": (i32, [p, p]),
+    "rs_kernel_launches": (C.c_longlong, []),
+}
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Every entry point include/raysurf_b200.h declares."""
+    return re.findall(r"RS_API\s+[^()]*?\b(rs_\w+)\s*\(", HEADER.read_text())
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C {PKG / 'csrc'}` "
+                "(the engine has no CPU fallback)")
+        dll = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(dll, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = dll
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().rs_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, bad_segment: int | None = None, max_stack: int | None = None) -> None:
+    """Map an RS_* status onto the reference's exception contract
+    (exceptions.py:4-26, _compiled.py:108-112)."""
+    if status == RS_OK:
+        return
+    if status == RS_STACK_OVERFLOW:
+        raise TraversalStackOverflow(
+            f"traversal stack overflow (capacity {max_stack})", segment_index=bad_segment)
+    if status == RS_INVALID_ARG:
+        raise ValidationError(last_error())
+    if status == RS_CUDA_ERROR and "memory" in last_error():
+        raise MemoryError(last_error())
+    raise RuntimeError(f"raysurf_b200 status {status}: {last_error()}")

@@ -1,0 +1,410 @@
+// rs_build.cu -- device BVH construction for sm_100a.
+//
+//   k_prep      per triangle: f64 centroid (morton.py:34-37), grid-wide
+//               support min/max (morton.py:40-45) via ordered-u64 atomics after
+//               a block reduction, and the reference's _reset_tree of internal
+//               slot j (lbvh.py:175-195).
+//   k_keys      per triangle: quantise (morton.py:48-63 or the isotropic fast
+//               grid) and interleave (morton.py:117-128) -> (code, index).
+//   onesweep    stable LSD radix sort, 8-bit digits, one kernel per pass with
+//               decoupled look-back (== np.lexsort((idx, code)), morton.py:131-146).
+//   k_climb     Apetrei single-pass climb (lbvh.py:198-233, _core.pyx:148-184):
+//               write child/range, release fence, acq_rel visit counter; the
+//               second arriver unions the children and also emits the packed
+//               64-B RsNode the traversal reads.
+#include <cuda/atomic>
+
+#include "rs_common.cuh"
+#include "rs_internal.h"
+
+namespace rs {
+
+// ------------------------------------------------------------------ prep ---
+
+__device__ __forceinline__ double warp_min(double v) {
+    for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
+                                              const int* __restrict__ T, int n, double* cent,
+                                              RsHeader* hdr, TreeArrays ta, int do_centroids) {
+    __shared__ double red[8][6];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        // _reset_tree (lbvh.py:181-189) for internal slot j
+        reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[0] = make_float2(0.f, 0.f);
+        reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[1] = make_float2(0.f, 0.f);
+        reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[2] = make_float2(0.f, 0.f);
+        ta.child_l[j] = kEmpty;
+        ta.child_r[j] = kEmpty;
+        ta.range_l[j] = -1;
+        ta.range_r[j] = -1;
+        ta.int_tri[j] = -1;
+        ta.visit[j] = 0;
+        if (do_centroids) {
+            const int ia = T[3ll * j], ib = T[3ll * j + 1], ic = T[3ll * j + 2];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double a = V[3ll * ia + k], b = V[3ll * ib + k], c = V[3ll * ic + k];
+                const double m = __ddiv_rn(__dadd_rn(__dadd_rn(a, b), c), 3.0);
+                cent[3ll * j + k] = m;
+                lo[k] = fmin(lo[k], m);
+                hi[k] = fmax(hi[k], m);
+            }
+        }
+    }
+    if (!do_centroids) return;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = warp_min(lo[k]);
+        hi[k] = warp_max(hi[k]);
+    }
+    if (l == 0)
+        for (int k = 0; k < 3; ++k) {
+            red[w][k] = lo[k];
+            red[w][3 + k] = hi[k];
+        }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x;
+        double v = red[0][k];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+            v = k < 3 ? fmin(v, red[i][k]) : fmax(v, red[i][k]);
+        if (isfinite(v)) {
+            if (k < 3)
+                atomicMax(&hdr->smin[k], ~ord_of(v));
+            else
+                atomicMax(&hdr->smax[k - 3], ord_of(v));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ keys ---
+
+__device__ __forceinline__ unsigned long long split21(unsigned long long v) {
+    v &= 0x1FFFFFull;
+    v = (v | v << 32) & 0x1F00000000FFFFull;
+    v = (v | v << 16) & 0x1F0000FF0000FFull;
+    v = (v | v << 8) & 0x100F00F00F00F00Full;
+    v = (v | v << 4) & 0x10C30C30C30C30C3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+
+__device__ __forceinline__ unsigned quant1(double p, double lo, double ext, double gmax) {
+    double s = floor(__dmul_rn(__ddiv_rn(__dsub_rn(p, lo), ext), gmax));
+    s = s < 0.0 ? 0.0 : (s > gmax ? gmax : s);  // np.clip (morton.py:62)
+    return (unsigned)s;
+}
+
+__global__ void __launch_bounds__(256) k_keys(const double* __restrict__ cent, int n,
+                                              const RsHeader* __restrict__ hdr, int kind,
+                                              unsigned long long* keys, int* vals) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double lo[3], ext[3], gmax;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = from_ord(~hdr->smin[k]);
+        ext[k] = __dsub_rn(from_ord(hdr->smax[k]), lo[k]);
+    }
+    if (kind == kTreeFast) {  // isotropic grid: one extent for every axis
+        const double e = fmax(fmax(ext[0], ext[1]), ext[2]);
+        ext[0] = ext[1] = ext[2] = e;
+        gmax = (double)((1u << kIsoBits) - 1u);
+    } else {
+        gmax = kGridMax21;
+    }
+    unsigned long long code = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const unsigned q = ext[k] > 0.0 ? quant1(cent[3ll * j + k], lo[k], ext[k], gmax) : 0u;
+        code |= split21(q) << k;
+    }
+    keys[j] = code;
+    vals[j] = j;
+}
+
+// ------------------------------------------------------------ radix sort ---
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys per tile
+constexpr int kSortWarps = kSortThreads / 32;
+
+__global__ void __launch_bounds__(256) k_sort_hist(const unsigned long long* __restrict__ keys,
+                                                   int n, int passes, unsigned* ghist) {
+    __shared__ unsigned h[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[j];
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+        const unsigned v = (&h[0][0])[i];
+        if (v) atomicAdd(&ghist[i], v);
+    }
+}
+
+// Onesweep pass: status words are (flag << 62 | count), flag 1 = tile
+// aggregate, 2 = inclusive prefix over tiles <= this one.
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+    const unsigned long long* __restrict__ kin, const int* __restrict__ vin,
+    unsigned long long* __restrict__ kout, int* __restrict__ vout, int n, int shift,
+    const unsigned* __restrict__ ghist, unsigned long long* status, unsigned* tile_counter) {
+    __shared__ unsigned warp_cnt[kSortWarps][256];
+    __shared__ unsigned long long gbase[256];
+    __shared__ int s_tile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&warp_cnt[0][0])[i] = 0;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    const long long base = (long long)tile * kSortTile + (long long)w * 32 * kSortItems;
+
+    unsigned long long key[kSortItems];
+    int val[kSortItems];
+    unsigned rank[kSortItems];
+    int dig[kSortItems];
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+        const long long idx = base + k * 32 + l;
+        const bool ok = idx < n;
+        key[k] = ok ? kin[idx] : 0ull;
+        val[k] = ok ? vin[idx] : 0;
+        dig[k] = ok ? (int)((key[k] >> shift) & 255u) : -1;
+    }
+    const unsigned lt = (1u << l) - 1u;
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+        const int d = dig[k];
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned r = 0;
+        if (d >= 0) r = warp_cnt[w][d] + __popc(peers & lt);
+        __syncwarp();
+        if (d >= 0 && (peers & lt) == 0) warp_cnt[w][d] += __popc(peers);
+        __syncwarp();
+        rank[k] = r;
+    }
+    __syncthreads();
+    // per digit: scan across warps, publish tile count, look back.
+    const int d = threadIdx.x;  // kSortThreads == 256 == radix
+    unsigned tot = 0;
+#pragma unroll
+    for (int i = 0; i < kSortWarps; ++i) {
+        const unsigned c = warp_cnt[i][d];
+        warp_cnt[i][d] = tot;
+        tot += c;
+    }
+    {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(
+            status[(long long)tile * 256 + d]);
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            me.store((2ull << 62) | tot, cuda::memory_order_release);
+        } else {
+            me.store((1ull << 62) | tot, cuda::memory_order_release);
+            for (int j = tile - 1; j >= 0;) {
+                cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> prev(
+                    status[(long long)j * 256 + d]);
+                const unsigned long long v = prev.load(cuda::memory_order_acquire);
+                const unsigned flag = (unsigned)(v >> 62);
+                if (flag == 0) continue;
+                excl += v & ((1ull << 62) - 1);
+                if (flag == 2) break;
+                --j;
+            }
+            me.store((2ull << 62) | (excl + tot), cuda::memory_order_release);
+        }
+        // exclusive global digit base: sum of ghist[< d] + tiles before us
+        unsigned long long gb = 0;
+        for (int i = 0; i < d; ++i) gb += ghist[i];
+        gbase[d] = gb + excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+        const int dd = dig[k];
+        if (dd < 0) continue;
+        const unsigned long long pos = gbase[dd] + warp_cnt[w][dd] + rank[k];
+        kout[pos] = key[k];
+        vout[pos] = val[k];
+    }
+}
+
+// ----------------------------------------------------------------- climb ---
+
+// lbvh.py:130-145 / _core.pyx:52-64: strict order on split positions a, b.
+__device__ __forceinline__ bool delta_less(const unsigned long long* __restrict__ c,
+                                           const int* __restrict__ id, int a, int b) {
+    const unsigned long long xa = c[a] ^ c[a + 1], xb = c[b] ^ c[b + 1];
+    if (xa != xb) return xa < xb;
+    const int ia = id[a] ^ id[a + 1], ib = id[b] ^ id[b + 1];
+    if (ia != ib) return ia < ib;
+    return a < b;
+}
+
+__device__ __forceinline__ void load_box_cg(const float* p, float b[6]) {
+    const float2 x = __ldcg(reinterpret_cast<const float2*>(p));
+    const float2 y = __ldcg(reinterpret_cast<const float2*>(p) + 1);
+    const float2 z = __ldcg(reinterpret_cast<const float2*>(p) + 2);
+    b[0] = x.x; b[1] = x.y; b[2] = y.x; b[3] = y.y; b[4] = z.x; b[5] = z.y;
+}
+
+__global__ void __launch_bounds__(256) k_climb(const float* __restrict__ V,
+                                               const int* __restrict__ T, int n,
+                                               const unsigned long long* __restrict__ codes,
+                                               const int* __restrict__ ids, TreeArrays ta,
+                                               RsNode* nodes, RsLeaf* leaves, RsHeader* hdr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int n_int = n - 1;
+    // leaf init (lbvh.py:190-194) + the packed leaf record for the exact test
+    const int tid = ids[i];
+    const int ia = T[3ll * tid], ib = T[3ll * tid + 1], ic = T[3ll * tid + 2];
+    float a[3], b[3], c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a[k] = V[3ll * ia + k];
+        b[k] = V[3ll * ib + k];
+        c[k] = V[3ll * ic + k];
+    }
+    float box[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // mesh.py:74-75
+        box[2 * k] = fminf(fminf(a[k], b[k]), c[k]);
+        box[2 * k + 1] = fmaxf(fmaxf(a[k], b[k]), c[k]);
+    }
+    float* lb_out = ta.leaf_bounds + 6ll * i;
+    reinterpret_cast<float2*>(lb_out)[0] = make_float2(box[0], box[1]);
+    reinterpret_cast<float2*>(lb_out)[1] = make_float2(box[2], box[3]);
+    reinterpret_cast<float2*>(lb_out)[2] = make_float2(box[4], box[5]);
+    ta.leaf_tri[i] = tid;
+    ta.leaf_range_l[i] = i;
+    ta.leaf_range_r[i] = i;
+    ta.sorted_ids[i] = tid;
+    RsLeaf lf;
+    lf.p0 = make_float4(a[0], a[1], a[2], b[0]);
+    lf.p1 = make_float4(b[1], b[2], c[0], c[1]);
+    lf.p2 = make_float4(c[2], __int_as_float(tid), 0.f, 0.f);
+    leaves[i] = lf;
+    if (n == 1) {  // lbvh.py:163-166: the single leaf is the root
+        ta.child_l[0] = n_int;
+        hdr->root = n_int;
+        hdr->height = 0;
+        return;
+    }
+    int left = i, right = i, node = n_int + i, height = 0;
+    for (;;) {
+        if (left == 0 && right == n - 1) {  // root reached (lbvh.py:210-214)
+            ta.child_l[n - 1] = node;
+            if (node < n_int) ta.int_tri[node] = -2;
+            hdr->root = node;
+            hdr->height = height;
+            return;
+        }
+        int parent;
+        if (left == 0 || (right != n - 1 && delta_less(codes, ids, right, left - 1))) {
+            parent = right;
+            ta.child_l[parent] = node;
+            ta.range_l[parent] = left;
+        } else {
+            parent = left - 1;
+            ta.child_r[parent] = node;
+            ta.range_r[parent] = right;
+        }
+        ta.height[node] = height;  // ref-indexed: internal 0..n-2, leaves n-1..2n-2
+        cuda::atomic_ref<int, cuda::thread_scope_device> vis(ta.visit[parent]);
+        if (vis.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // first arriver stops
+        left = __ldcg(ta.range_l + parent);
+        right = __ldcg(ta.range_r + parent);
+        const int cl = __ldcg(ta.child_l + parent), cr = __ldcg(ta.child_r + parent);
+        float l6[6], r6[6];
+        load_box_cg(cl < n_int ? ta.int_bounds + 6ll * cl : ta.leaf_bounds + 6ll * (cl - n_int), l6);
+        load_box_cg(cr < n_int ? ta.int_bounds + 6ll * cr : ta.leaf_bounds + 6ll * (cr - n_int), r6);
+        const int hl = __ldcg(ta.height + cl), hr = __ldcg(ta.height + cr);
+        height = 1 + (hl > hr ? hl : hr);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {  // _core.pyx:181-183 (_fmin/_fmax)
+            box[2 * k] = l6[2 * k] < r6[2 * k] ? l6[2 * k] : r6[2 * k];
+            box[2 * k + 1] = l6[2 * k + 1] > r6[2 * k + 1] ? l6[2 * k + 1] : r6[2 * k + 1];
+        }
+        float* pb = ta.int_bounds + 6ll * parent;
+        reinterpret_cast<float2*>(pb)[0] = make_float2(box[0], box[1]);
+        reinterpret_cast<float2*>(pb)[1] = make_float2(box[2], box[3]);
+        reinterpret_cast<float2*>(pb)[2] = make_float2(box[4], box[5]);
+        RsNode nd;
+        nd.a = make_float4(l6[0], l6[1], l6[2], l6[3]);
+        nd.b = make_float4(l6[4], l6[5], r6[0], r6[1]);
+        nd.c = make_float4(r6[2], r6[3], r6[4], r6[5]);
+        nd.d = make_int4(cl, cr, 0, 0);
+        nodes[parent] = nd;
+        node = parent;
+    }
+}
+
+// ------------------------------------------------------------ host glue ---
+
+static int grid_for(long long n, int block, int cap) {
+    long long g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    return (int)(g < cap ? g : cap);
+}
+
+void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hdr,
+                 const TreeArrays& ta, bool centroids, cudaStream_t s) {
+    count_launches(1);
+    k_prep<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(V, T, n, cent, hdr, ta, centroids ? 1 : 0);
+}
+
+void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
+                 unsigned long long* keys, int* vals, cudaStream_t s) {
+    count_launches(1);
+    k_keys<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(cent, n, hdr, kind, keys, vals);
+}
+
+size_t sort_scratch_bytes(int n, int passes) {
+    const long long tiles = (n + kSortTile - 1) / kSortTile;
+    return (size_t)passes * 256 * 4 + 64 + (size_t)passes * tiles * 256 * 8;
+}
+
+// Sorts (keys, vals) by the low 8*passes bits of the key; returns via
+// (keys, vals) when passes is even, else (keys_alt, vals_alt).  scratch must
+// hold sort_scratch_bytes(n, passes) bytes.
+void launch_sort(unsigned long long* keys, int* vals, unsigned long long* keys_alt,
+                 int* vals_alt, int n, int passes, void* scratch, cudaStream_t s) {
+    const long long tiles = (n + kSortTile - 1) / kSortTile;
+    unsigned* ghist = reinterpret_cast<unsigned*>(scratch);
+    unsigned* counters = ghist + passes * 256;
+    unsigned long long* status =
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(scratch) + passes * 256 * 4 + 64);
+    cudaMemsetAsync(scratch, 0, sort_scratch_bytes(n, passes), s);
+    count_launches(1 + passes);
+    k_sort_hist<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(keys, n, passes, ghist);
+    unsigned long long *ki = keys, *ko = keys_alt;
+    int *vi = vals, *vo = vals_alt;
+    for (int p = 0; p < passes; ++p) {
+        k_onesweep<<<(unsigned)tiles, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, 8 * p,
+                                                            ghist + 256 * p, status + p * tiles * 256,
+                                                            counters + p);
+        unsigned long long* tk = ki; ki = ko; ko = tk;
+        int* tv = vi; vi = vo; vo = tv;
+    }
+}
+
+void launch_climb(const float* V, const int* T, int n, const unsigned long long* codes,
+                  const int* ids, const TreeArrays& ta, RsNode* nodes, RsLeaf* leaves,
+                  RsHeader* hdr, cudaStream_t s) {
+    count_launches(1);
+    k_climb<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(V, T, n, codes, ids, ta, nodes, leaves, hdr);
+}
+
+}  // namespace rs

@@ -1,0 +1,605 @@
+// rs_capi.cu -- the extern "C" boundary (include/raysurf_b200.h) and the
+// native host runtime behind it: stream-ordered device memory (cudaMallocAsync
+// pool), tree lifetime, status read-back, and the chunked H2D / query / D2H
+// pipeline of rs_run_batch_host.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/raysurf_b200.h"
+#include "rs_common.cuh"
+#include "rs_internal.h"
+
+using namespace rs;
+
+namespace rs {
+static std::atomic<long long> g_launches{0};
+void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace rs
+
+struct rs_tree {
+    int64_t n;
+    int kind;
+    char* block;
+    RsHeader* hdr;
+    RsNode* nodes;
+    RsLeaf* leaves;
+    TreeArrays ta;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+// Phase timing (engine.py's timings dict, measured on device): when enabled,
+// events bracket the build and the query kernel on the caller's stream.
+thread_local bool g_timing = false;
+thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+thread_local float g_build_ms = 0.f, g_query_ms = 0.f;
+thread_local bool g_ev_valid = false;
+
+void ev_record(int k, cudaStream_t s) {
+    if (!g_timing) return;
+    if (!g_ev[k]) cudaEventCreate(&g_ev[k]);
+    cudaEventRecord(g_ev[k], s);
+}
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(RS_CUDA_ERROR, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                              \
+    } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Carves consecutive 256-B aligned sub-buffers out of one allocation.
+struct Carver {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        T* p = reinterpret_cast<T*>(base + off);
+        off += align256(count * sizeof(T));
+        return p;
+    }
+};
+
+size_t tree_bytes(int64_t n) {
+    size_t b = align256(sizeof(RsHeader));
+    b += align256(sizeof(RsNode) * (size_t)(n > 1 ? n - 1 : 1));
+    b += align256(sizeof(RsLeaf) * (size_t)n);
+    b += 2 * align256(sizeof(float) * 6 * (size_t)n);
+    b += 10 * align256(sizeof(int) * (size_t)n);
+    b += align256(sizeof(int) * 2 * (size_t)n);
+    return b;
+}
+
+void carve_tree(rs_tree* t) {
+    Carver c{t->block};
+    const size_t n = (size_t)t->n;
+    t->hdr = c.take<RsHeader>(1);
+    t->nodes = c.take<RsNode>(n > 1 ? n - 1 : 1);
+    t->leaves = c.take<RsLeaf>(n);
+    t->ta.int_bounds = c.take<float>(6 * n);
+    t->ta.leaf_bounds = c.take<float>(6 * n);
+    t->ta.child_l = c.take<int>(n);
+    t->ta.child_r = c.take<int>(n);
+    t->ta.range_l = c.take<int>(n);
+    t->ta.range_r = c.take<int>(n);
+    t->ta.int_tri = c.take<int>(n);
+    t->ta.visit = c.take<int>(n);
+    t->ta.leaf_tri = c.take<int>(n);
+    t->ta.leaf_range_l = c.take<int>(n);
+    t->ta.leaf_range_r = c.take<int>(n);
+    t->ta.sorted_ids = c.take<int>(n);
+    t->ta.height = c.take<int>(2 * n);
+}
+
+bool g_pool_configured = false;
+
+int configure_pool() {
+    if (g_pool_configured) return RS_OK;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    unsigned long long thr = ~0ull;  // keep freed blocks cached in the pool
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_pool_configured = true;
+    return RS_OK;
+}
+
+int check_mesh(int64_t n_v, int64_t n_t) {
+    if (n_t < 1) return fail(RS_INVALID_ARG, "cannot build a BVH over an empty mesh");
+    if (n_t > 2147483647ll)
+        return fail(RS_INVALID_ARG, "triangle count %lld exceeds capacity 2147483647", (long long)n_t);
+    if (n_v < 3 || n_v > 2147483647ll)
+        return fail(RS_INVALID_ARG, "vertex count %lld out of range", (long long)n_v);
+    return RS_OK;
+}
+
+int alloc_tree(int64_t n, int kind, cudaStream_t s, rs_tree** out) {
+    int rc = configure_pool();
+    if (rc) return rc;
+    rs_tree* t = new rs_tree();
+    t->n = n;
+    t->kind = kind;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&t->block), tree_bytes(n), s);
+    if (e != cudaSuccess) {
+        delete t;
+        return fail(RS_CUDA_ERROR, "device allocation of %zu bytes failed: %s", tree_bytes(n),
+                    cudaGetErrorString(e));
+    }
+    carve_tree(t);
+    *out = t;
+    return RS_OK;
+}
+
+int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
+               const uint64_t* sorted_codes, const int* sorted_ids, cudaStream_t s,
+               rs_tree** out) {
+    int rc = check_mesh(n_v, n_t);
+    if (rc) return rc;
+    if (kind != kTreeReference && kind != kTreeFast)
+        return fail(RS_INVALID_ARG, "unknown tree kind %d", kind);
+    rs_tree* t = nullptr;
+    rc = alloc_tree(n_t, kind, s, &t);
+    if (rc) return rc;
+    const int n = (int)n_t;
+    CK(cudaMemsetAsync(t->hdr, 0, sizeof(RsHeader), s));
+    if (sorted_codes) {
+        launch_prep(V, T, n, nullptr, t->hdr, t->ta, false, s);
+        launch_climb(V, T, n, reinterpret_cast<const unsigned long long*>(sorted_codes),
+                     sorted_ids, t->ta, t->nodes, t->leaves, t->hdr, s);
+    } else {
+        const int passes = kind == kTreeFast ? 4 : 8;  // 30-bit vs 63-bit keys
+        const size_t sb = sort_scratch_bytes(n, passes);
+        const size_t bytes = align256(24ull * n) + 2 * align256(8ull * n) + 2 * align256(4ull * n) +
+                             align256(sb);
+        char* scratch = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s));
+        Carver c{scratch};
+        double* cent = c.take<double>(3ull * n);
+        unsigned long long* keys = c.take<unsigned long long>(n);
+        unsigned long long* keys2 = c.take<unsigned long long>(n);
+        int* vals = c.take<int>(n);
+        int* vals2 = c.take<int>(n);
+        void* sort_scratch = c.take<char>(sb);
+        launch_prep(V, T, n, cent, t->hdr, t->ta, true, s);
+        launch_keys(cent, n, t->hdr, kind, keys, vals, s);
+        launch_sort(keys, vals, keys2, vals2, n, passes, sort_scratch, s);
+        launch_climb(V, T, n, keys, vals, t->ta, t->nodes, t->leaves, t->hdr, s);
+        CK(cudaFreeAsync(scratch, s));
+    }
+    CK(cudaGetLastError());
+    *out = t;
+    return RS_OK;
+}
+
+int check_query(int mode, int max_coll, int max_stack) {
+    if (mode < 0 || mode > 2) return fail(RS_INVALID_ARG, "unknown mode %d", mode);
+    if (max_coll < 2) return fail(RS_INVALID_ARG, "collision buffer needs capacity >= 2");
+    if (max_stack < 1) return fail(RS_INVALID_ARG, "traversal stack needs capacity >= 1");
+    return RS_OK;
+}
+
+int kstack_for(bool ref, int max_stack) {
+    if (!ref) return 64;  // fast tree height <= 61 (30 code bits + 31 id bits)
+    return max_stack < 128 ? max_stack : 128;  // reference tree height <= 94
+}
+
+QueryArgs make_args(const rs_tree* t, const float* s, const float* e, int64_t n_r, int max_coll,
+                    int max_stack, RsStatus* st) {
+    QueryArgs a{};
+    a.nodes = t->nodes;
+    a.leaves = t->leaves;
+    a.hdr = t->hdr;
+    a.n_int = (int)(t->n - 1);
+    a.starts = s;
+    a.ends = e;
+    a.n_r = n_r;
+    a.max_coll = max_coll;
+    a.max_stack = max_stack;
+    a.status = st;
+    return a;
+}
+
+int read_status(RsStatus* d_st, cudaStream_t s, RsStatus* h) {
+    CK(cudaMemcpyAsync(h, d_st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return RS_OK;
+}
+
+int status_code(const RsStatus& h, int64_t* bad_segment) {
+    if (bad_segment) *bad_segment = h.bad ? (int64_t)~h.bad : -1;
+    if (h.bad) return fail(RS_STACK_OVERFLOW, "traversal stack overflow");
+    if (h.internal) return fail(RS_INTERNAL, "internal traversal capacity exceeded");
+    return RS_OK;
+}
+
+// Per-thread cached pipeline resources for rs_run_batch_host.
+struct Pipe {
+    int device = -1;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_in[2], ev_q[2], ev_out[2];
+};
+thread_local Pipe g_pipe;
+
+int pipe_init() {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    if (g_pipe.device == dev) return RS_OK;
+    CK(cudaStreamCreateWithFlags(&g_pipe.copy, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&g_pipe.ev_in[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g_pipe.ev_q[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g_pipe.ev_out[k], cudaEventDisableTiming));
+    }
+    g_pipe.device = dev;
+    return RS_OK;
+}
+
+}  // namespace
+
+// ===================================================================== ABI ==
+
+extern "C" {
+
+int rs_abi_version(void) { return 1; }
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+int rs_build(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
+             int tree_kind, void* stream, rs_tree** out) {
+    if (!out) return fail(RS_INVALID_ARG, "null output handle");
+    return build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, S(stream), out);
+}
+
+int rs_build_from_sorted(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
+                         const uint64_t* d_sorted_codes, const int32_t* d_sorted_ids,
+                         void* stream, rs_tree** out) {
+    if (!out || !d_sorted_codes || !d_sorted_ids) return fail(RS_INVALID_ARG, "null argument");
+    return build_impl(d_verts, n_v, d_tris, n_t, kTreeReference, d_sorted_codes, d_sorted_ids,
+                      S(stream), out);
+}
+
+int rs_tree_info(const rs_tree* t, int64_t* n_tri, int32_t* root, int32_t* height,
+                 int32_t* kind, void* stream) {
+    if (!t) return fail(RS_INVALID_ARG, "null tree");
+    RsHeader h;
+    CK(cudaMemcpyAsync(&h, t->hdr, sizeof h, cudaMemcpyDeviceToHost, S(stream)));
+    CK(cudaStreamSynchronize(S(stream)));
+    if (n_tri) *n_tri = t->n;
+    if (root) *root = h.root;
+    if (height) *height = h.height;
+    if (kind) *kind = t->kind;
+    return RS_OK;
+}
+
+int rs_tree_download(const rs_tree* t, float* ib, int32_t* cl, int32_t* cr, int32_t* rl,
+                     int32_t* rr, int32_t* it, int32_t* vi, float* lb, int32_t* lt, int32_t* lrl,
+                     int32_t* lrr, int32_t* si, void* stream) {
+    if (!t) return fail(RS_INVALID_ARG, "null tree");
+    const size_t n = (size_t)t->n;
+    cudaStream_t s = S(stream);
+    struct { void* h; const void* d; size_t b; } cp[] = {
+        {ib, t->ta.int_bounds, 24 * n}, {cl, t->ta.child_l, 4 * n}, {cr, t->ta.child_r, 4 * n},
+        {rl, t->ta.range_l, 4 * n}, {rr, t->ta.range_r, 4 * n}, {it, t->ta.int_tri, 4 * n},
+        {vi, t->ta.visit, 4 * n}, {lb, t->ta.leaf_bounds, 24 * n}, {lt, t->ta.leaf_tri, 4 * n},
+        {lrl, t->ta.leaf_range_l, 4 * n}, {lrr, t->ta.leaf_range_r, 4 * n},
+        {si, t->ta.sorted_ids, 4 * n}};
+    for (auto& c : cp)
+        if (c.h) CK(cudaMemcpyAsync(c.h, c.d, c.b, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return RS_OK;
+}
+
+int rs_free(rs_tree* t, void* stream) {
+    if (!t) return RS_OK;
+    cudaError_t e = cudaFreeAsync(t->block, S(stream));
+    delete t;
+    if (e != cudaSuccess) return fail(RS_CUDA_ERROR, "cudaFreeAsync: %s", cudaGetErrorString(e));
+    return RS_OK;
+}
+
+static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
+                      int max_coll, int max_stack, int ref, int32_t* det, int32_t* cnt,
+                      int32_t* tri, float* dist, float* pts, int32_t* c_ray, float* c_dist,
+                      int32_t* c_tri, float* c_pt, int64_t* n_hits, int64_t* bad, bool stats,
+                      int64_t* visits, int64_t* mts, cudaStream_t s) {
+    if (!t) return fail(RS_INVALID_ARG, "null tree");
+    int rc = check_query(mode, max_coll, max_stack);
+    if (rc) return rc;
+    if (n_r < 0) return fail(RS_INVALID_ARG, "negative segment count");
+    if (n_r > 2147483647ll) return fail(RS_INVALID_ARG, "segment count exceeds int32 indexing");
+    const bool compact = c_ray != nullptr;
+    const size_t cs = compact ? compact_scratch_bytes(n_r) : 0;
+    char* blk = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
+    RsStatus* st = reinterpret_cast<RsStatus*>(blk);
+    CK(cudaMemsetAsync(blk, 0, align256(sizeof(RsStatus)) + cs, s));
+    QueryArgs a = make_args(t, d_s, d_e, n_r, max_coll, max_stack, st);
+    a.detected = det; a.counts = cnt; a.tri = tri; a.dist = dist; a.points = pts;
+    a.c_ray = c_ray; a.c_dist = c_dist; a.c_tri = c_tri; a.c_point = c_pt;
+    a.tile_status = reinterpret_cast<unsigned long long*>(blk + align256(sizeof(RsStatus)));
+    ev_record(1, s);
+    if (launch_query(a, mode, ref != 0, compact, kstack_for(ref != 0, max_stack), stats, s))
+        return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
+    CK(cudaGetLastError());
+    ev_record(2, s);
+    RsStatus h;
+    rc = read_status(st, s, &h);
+    CK(cudaFreeAsync(blk, s));
+    if (rc) return rc;
+    if (n_hits) *n_hits = (int64_t)h.hits;
+    if (visits) *visits = (int64_t)h.visits;
+    if (mts) *mts = (int64_t)h.mts;
+    return status_code(h, bad);
+}
+
+int rs_query(const rs_tree* t, const float* d_starts, const float* d_ends, int64_t n_r, int mode,
+             int max_coll, int max_stack, int ref, int32_t* d_detected, int32_t* d_counts,
+             int32_t* d_tri, float* d_dist, float* d_points, int64_t* bad, void* stream) {
+    if (mode == kBoolean && !d_detected) return fail(RS_INVALID_ARG, "boolean needs d_detected");
+    if (mode == kCount && !d_counts) return fail(RS_INVALID_ARG, "count needs d_counts");
+    if (mode == kBarycentric && !(d_detected && d_tri && d_dist && d_points))
+        return fail(RS_INVALID_ARG, "barycentric needs detected/tri/dist/points");
+    return query_impl(t, d_starts, d_ends, n_r, mode, max_coll, max_stack, ref, d_detected,
+                      d_counts, d_tri, d_dist, d_points, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, bad, false, nullptr, nullptr, S(stream));
+}
+
+int rs_query_compact(const rs_tree* t, const float* d_starts, const float* d_ends, int64_t n_r,
+                     int max_coll, int max_stack, int ref, int32_t* d_ray, float* d_dist,
+                     int32_t* d_tri, float* d_pt, int64_t* n_hits, int64_t* bad, void* stream) {
+    if (!(d_ray && d_dist && d_tri && d_pt)) return fail(RS_INVALID_ARG, "null output");
+    if (n_hits) *n_hits = 0;
+    return query_impl(t, d_starts, d_ends, n_r, kBarycentric, max_coll, max_stack, ref, nullptr,
+                      nullptr, nullptr, nullptr, nullptr, d_ray, d_dist, d_tri, d_pt, n_hits, bad,
+                      false, nullptr, nullptr, S(stream));
+}
+
+int rs_query_stats(const rs_tree* t, const float* d_starts, const float* d_ends, int64_t n_r,
+                   int mode, int max_coll, int max_stack, int ref, int64_t* visits, int64_t* mts,
+                   void* stream) {
+    cudaStream_t s = S(stream);
+    // outputs go to a scratch block: stats runs are diagnostics
+    char* blk = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(28ull * (n_r > 0 ? n_r : 1)), s));
+    int32_t* i0 = reinterpret_cast<int32_t*>(blk);
+    float* f1 = reinterpret_cast<float*>(blk + 8ull * n_r);
+    float* f3 = reinterpret_cast<float*>(blk + 16ull * n_r);
+    int32_t* i2 = reinterpret_cast<int32_t*>(blk + 12ull * n_r);
+    int64_t bad;
+    int rc = query_impl(t, d_starts, d_ends, n_r, mode, max_coll, max_stack, ref, i0, i0, i2, f1,
+                        f3, nullptr, nullptr, nullptr, nullptr, nullptr, &bad, true, visits, mts, s);
+    cudaFreeAsync(blk, s);
+    return rc;
+}
+
+int rs_baseline(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
+                const float* d_starts, const float* d_ends, int64_t n_r, int mode,
+                int32_t* d_detected, int32_t* d_counts, int32_t* d_tri, float* d_dist,
+                float* d_points, void* stream) {
+    if (mode < 0 || mode > 2) return fail(RS_INVALID_ARG, "unknown mode %d", mode);
+    if (n_t < 0 || n_r < 0 || n_t > 2147483647ll || n_r > 2147483647ll)
+        return fail(RS_INVALID_ARG, "bad sizes");
+    (void)n_v;
+    BaselineArgs a{d_verts, d_tris, (int)n_t, d_starts, d_ends, n_r, d_detected, d_counts,
+                   d_tri, d_dist, d_points};
+    cudaStream_t s = S(stream);
+    if (n_t > 0) launch_baseline(a, mode, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return RS_OK;
+}
+
+int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
+                        const float* d_starts, const float* d_ends, int64_t n_r, int mode,
+                        int tree_kind, int max_coll, int max_stack, int32_t* d_flags,
+                        int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
+                        int64_t* n_hits, int64_t* bad, void* stream) {
+    int rc = check_query(mode, max_coll, max_stack);
+    if (rc) return rc;
+    if (bad) *bad = -1;
+    if (n_hits) *n_hits = 0;
+    if (n_r == 0 || n_t == 0) return RS_OK;  // engine.py:233-234 (caller pre-zeroes d_flags)
+    cudaStream_t s = S(stream);
+    rs_tree* t = nullptr;
+    ev_record(0, s);
+    rc = rs_build(d_verts, n_v, d_tris, n_t, tree_kind, stream, &t);
+    if (rc) return rc;
+    const int ref = tree_kind == kTreeReference;
+    if (mode == kBarycentric)
+        rc = query_impl(t, d_starts, d_ends, n_r, mode, max_coll, max_stack, ref, nullptr, nullptr,
+                        nullptr, nullptr, nullptr, d_ray, d_dist, d_tri, d_pt, n_hits, bad, false,
+                        nullptr, nullptr, s);
+    else
+        rc = query_impl(t, d_starts, d_ends, n_r, mode, max_coll, max_stack, ref, d_flags, d_flags,
+                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, bad,
+                        false, nullptr, nullptr, s);
+    const int rc2 = rs_free(t, stream);
+    if (g_timing && !rc) {
+        cudaEventElapsedTime(&g_build_ms, g_ev[0], g_ev[1]);
+        cudaEventElapsedTime(&g_query_ms, g_ev[1], g_ev[2]);
+        g_ev_valid = true;
+    }
+    return rc ? rc : rc2;
+}
+
+RS_API int rs_set_timing(int enable) {
+    g_timing = enable != 0;
+    g_ev_valid = false;
+    return RS_OK;
+}
+
+RS_API int rs_last_timings(float* build_ms, float* query_ms) {
+    if (!g_ev_valid) return fail(RS_INVALID_ARG, "no timed rs_run_batch_device call yet");
+    if (build_ms) *build_ms = g_build_ms;
+    if (query_ms) *query_ms = g_query_ms;
+    return RS_OK;
+}
+
+RS_API long long rs_kernel_launches(void) { return g_launches.load(); }
+
+int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, int64_t n_t,
+                      const float* h_starts, const float* h_ends, int64_t n_r, int mode,
+                      int tree_kind, int max_coll, int max_stack, int64_t chunk_rays,
+                      int32_t* h_flags, int32_t* h_ray, float* h_dist, int32_t* h_tri,
+                      float* h_pt, int64_t* n_hits, int64_t* bad, void* stream) {
+    int rc = check_query(mode, max_coll, max_stack);
+    if (rc) return rc;
+    if (bad) *bad = -1;
+    if (n_hits) *n_hits = 0;
+    if (n_r == 0 || n_t == 0) {
+        if (h_flags && n_r > 0) memset(h_flags, 0, sizeof(int32_t) * (size_t)n_r);
+        return RS_OK;
+    }
+    if (n_r > 2147483647ll) return fail(RS_INVALID_ARG, "segment count exceeds int32 indexing");
+    rc = check_mesh(n_v, n_t);
+    if (rc) return rc;
+    rc = configure_pool();
+    if (rc) return rc;
+    rc = pipe_init();
+    if (rc) return rc;
+    cudaStream_t s = S(stream);
+    cudaStream_t cp = g_pipe.copy;
+    if (chunk_rays <= 0) chunk_rays = n_r > (8ll << 20) ? (n_r + 7) / 8 : (n_r > (1 << 20) ? (n_r + 3) / 4 : n_r);
+    chunk_rays = ((chunk_rays + 127) / 128) * 128;
+    const int64_t nchunks = (n_r + chunk_rays - 1) / chunk_rays;
+    const bool bary = mode == kBarycentric;
+
+    // one device block: mesh, 2x chunk inputs, outputs, status, tile status
+    const size_t mesh_b = align256(12ull * n_v) + align256(12ull * n_t);
+    const size_t in_b = 2 * 2 * align256(12ull * chunk_rays);
+    const size_t out_b = bary ? 4 * align256(12ull * n_r) : 2 * align256(4ull * chunk_rays);
+    const size_t tiles_b = align256(compact_scratch_bytes(chunk_rays)) * (size_t)nchunks;
+    const size_t st_b = align256(sizeof(RsStatus) * (size_t)nchunks);
+    char* blk = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), mesh_b + in_b + out_b + tiles_b + st_b, s));
+    Carver c{blk};
+    float* dV = c.take<float>(3ull * n_v);
+    int* dT = c.take<int>(3ull * n_t);
+    float* din[2][2];
+    for (int k = 0; k < 2; ++k) {
+        din[k][0] = c.take<float>(3ull * chunk_rays);
+        din[k][1] = c.take<float>(3ull * chunk_rays);
+    }
+    int32_t* dflag[2] = {nullptr, nullptr};
+    int32_t *dray = nullptr, *dtri = nullptr;
+    float *ddist = nullptr, *dpt = nullptr;
+    if (bary) {
+        dray = c.take<int32_t>(n_r);
+        ddist = c.take<float>(n_r);
+        dtri = c.take<int32_t>(n_r);
+        dpt = c.take<float>(3ull * n_r);
+    } else {
+        dflag[0] = c.take<int32_t>(chunk_rays);
+        dflag[1] = c.take<int32_t>(chunk_rays);
+    }
+    char* tiles = reinterpret_cast<char*>(c.take<char>(align256(compact_scratch_bytes(chunk_rays)) * nchunks));
+    RsStatus* st = c.take<RsStatus>(nchunks);
+    CK(cudaMemsetAsync(tiles, 0, tiles_b + st_b, s));
+    CK(cudaMemcpyAsync(dV, h_verts, 12ull * n_v, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dT, h_tris, 12ull * n_t, cudaMemcpyHostToDevice, s));
+    rs_tree* t = nullptr;
+    rc = build_impl(dV, n_v, dT, n_t, tree_kind, nullptr, nullptr, s, &t);
+    if (rc) {
+        cudaFreeAsync(blk, s);
+        return rc;
+    }
+    const int ref = tree_kind == kTreeReference;
+    // The copy stream must see the memset/mesh copies ordered before chunk 0.
+    CK(cudaEventRecord(g_pipe.ev_q[1], s));
+    CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[1], 0));
+    unsigned long long running = 0;  // barycentric rows already placed
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int b = (int)(k & 1);
+        const int64_t lo = k * chunk_rays;
+        const int64_t cnt = (lo + chunk_rays <= n_r) ? chunk_rays : n_r - lo;
+        if (k >= 2) CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));  // buffer b free again
+        CK(cudaMemcpyAsync(din[b][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, cp));
+        CK(cudaMemcpyAsync(din[b][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, cp));
+        CK(cudaEventRecord(g_pipe.ev_in[b], cp));
+        CK(cudaStreamWaitEvent(s, g_pipe.ev_in[b], 0));
+        if (k >= 2 && !bary) CK(cudaStreamWaitEvent(s, g_pipe.ev_out[b], 0));
+        QueryArgs a = make_args(t, din[b][0], din[b][1], cnt, max_coll, max_stack, st + k);
+        a.ray_offset = lo;
+        if (bary) {
+            // each chunk compacts into its own region; rows are concatenated on the host
+            a.c_ray = dray + lo;
+            a.c_dist = ddist + lo;
+            a.c_tri = dtri + lo;
+            a.c_point = dpt + 3 * lo;
+            a.tile_status = reinterpret_cast<unsigned long long*>(
+                tiles + align256(compact_scratch_bytes(chunk_rays)) * k);
+        } else {
+            a.detected = dflag[b];
+            a.counts = dflag[b];
+        }
+        if (launch_query(a, mode, ref != 0, bary, kstack_for(ref != 0, max_stack), false, s)) {
+            rs_free(t, stream);
+            cudaFreeAsync(blk, s);
+            return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
+        }
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(g_pipe.ev_q[b], s));
+        if (!bary) {
+            CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));
+            CK(cudaMemcpyAsync(h_flags + lo, dflag[b], 4ull * cnt, cudaMemcpyDeviceToHost, cp));
+            CK(cudaEventRecord(g_pipe.ev_out[b], cp));
+        }
+    }
+    // statuses of every chunk; barycentric row counts come back with them
+    RsStatus* hst = new RsStatus[nchunks];
+    CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[(nchunks - 1) & 1], 0));
+    CK(cudaMemcpyAsync(hst, st, sizeof(RsStatus) * nchunks, cudaMemcpyDeviceToHost, cp));
+    CK(cudaStreamSynchronize(cp));
+    unsigned long long badv = 0, internal = 0;
+    for (int64_t k = 0; k < nchunks; ++k) {
+        if (hst[k].bad && (!badv || ~hst[k].bad < ~badv)) badv = hst[k].bad;
+        internal |= hst[k].internal;
+    }
+    if (bary && !badv && !internal) {
+        for (int64_t k = 0; k < nchunks; ++k) {
+            const int64_t lo = k * chunk_rays;
+            const size_t m = (size_t)hst[k].hits;
+            if (m) {
+                CK(cudaMemcpyAsync(h_ray + running, dray + lo, 4 * m, cudaMemcpyDeviceToHost, cp));
+                CK(cudaMemcpyAsync(h_dist + running, ddist + lo, 4 * m, cudaMemcpyDeviceToHost, cp));
+                CK(cudaMemcpyAsync(h_tri + running, dtri + lo, 4 * m, cudaMemcpyDeviceToHost, cp));
+                CK(cudaMemcpyAsync(h_pt + 3 * running, dpt + 3 * lo, 12 * m, cudaMemcpyDeviceToHost, cp));
+            }
+            running += m;
+        }
+        CK(cudaStreamSynchronize(cp));
+    }
+    delete[] hst;
+    rs_free(t, stream);
+    CK(cudaFreeAsync(blk, s));
+    CK(cudaStreamSynchronize(s));
+    if (n_hits) *n_hits = (int64_t)running;
+    RsStatus agg{};
+    agg.bad = badv;
+    agg.internal = internal;
+    return status_code(agg, bad);
+}
+
+}  // extern "C"

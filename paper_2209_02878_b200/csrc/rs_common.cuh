@@ -1,0 +1,136 @@
+// rs_common.cuh -- shared device types and helpers for the raysurf B200 engine.
+//
+// HBM layout (one BVH per device):
+//   RsNode  nodes[N_t - 1]  64 B  internal node = both children's f32 AABBs
+//                                  + both child refs; one 64-B line per visit
+//   RsLeaf  leaves[N_t]     48 B  Morton-ordered triangle: 9 vertex floats +
+//                                  original triangle id (for the exact test)
+//   the reference's SoA BvhTree fields (lbvh.py:39-55) are kept beside them
+//   so a built tree can be downloaded field-for-field (rs_tree_download).
+//
+// Node references use the reference's tagging (lbvh.py:1-17): ref < N_t - 1
+// is an internal node, otherwise leaf ref - (N_t - 1); -1 is empty.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rs {
+
+constexpr int kEmpty = -1;
+constexpr double kDetEps = 1e-9;   // geometry.py:14-15
+constexpr double kBaryEps = 1e-7;  // geometry.py:16-17
+constexpr double kGridMax21 = 2097151.0;  // morton.py:15-16
+constexpr int kIsoBits = 10;       // fast tree: 30-bit isotropic Morton
+
+enum Mode { kBoolean = 0, kBarycentric = 1, kCount = 2 };  // _compiled.py:17-21
+enum TreeKind { kTreeReference = 0, kTreeFast = 1 };
+
+struct __align__(16) RsNode {
+    float4 a;  // l.xmin l.xmax l.ymin l.ymax
+    float4 b;  // l.zmin l.zmax r.xmin r.xmax
+    float4 c;  // r.ymin r.ymax r.zmin r.zmax
+    int4 d;    // lref rref - -
+};
+
+struct __align__(16) RsLeaf {
+    float4 p0;  // a.x a.y a.z b.x
+    float4 p1;  // b.y b.z c.x c.y
+    float4 p2;  // c.z tid(bits) - -
+};
+
+// Per-tree device header (zeroed with one memset before a build).
+struct RsHeader {
+    unsigned long long smin[3];  // ~ordered(min centroid)  (atomicMax of complement)
+    unsigned long long smax[3];  //  ordered(max centroid)
+    int root;
+    int height;
+    int pad[2];
+};
+
+// Per-query device status (zeroed before a query).
+struct RsStatus {
+    unsigned long long bad;       // ~lowest overflowing segment (0 = none)
+    unsigned long long internal;  // internal-capacity overflow (should stay 0)
+    unsigned long long hits;      // barycentric: number of compacted rows
+    unsigned long long tile_counter;
+    unsigned long long visits;    // optional stats
+    unsigned long long mts;
+};
+
+// ---- ordered encodings so atomics on u64 give min/max of doubles ----------
+__device__ __forceinline__ unsigned long long ord_of(double d) {
+    unsigned long long u = __double_as_longlong(d);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double from_ord(unsigned long long o) {
+    unsigned long long u = (o & 0x8000000000000000ull) ? (o & ~0x8000000000000000ull) : ~o;
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(u);
+#else
+    double d;
+    __builtin_memcpy(&d, &u, 8);
+    return d;
+#endif
+}
+
+// ---- f32 box test: touching counts (geometry.py:69-79, _core.pyx:44-49) ---
+__device__ __forceinline__ bool overlap6(const float q[6], float x0, float x1, float y0, float y1,
+                                         float z0, float z1) {
+    return q[0] <= x1 && q[1] >= x0 && q[2] <= y1 && q[3] >= y0 && q[4] <= z1 && q[5] >= z0;
+}
+
+// ---- f64 Moller-Trumbore in the reference op order (geometry.py:82-137,
+// _core.pyx:67-114).  Explicit _rn intrinsics: no FMA contraction, so the
+// result is bit-identical to the -ffp-contract=off CPU reference. ----------
+__device__ __forceinline__ bool mt_hit(float ax_, float ay_, float az_, float bx, float by,
+                                       float bz, float cx, float cy, float cz, double sx,
+                                       double sy, double sz, double dx, double dy, double dz,
+                                       double* t_out) {
+    const double ax = ax_, ay = ay_, az = az_;
+    const double e1x = __dsub_rn((double)bx, ax), e1y = __dsub_rn((double)by, ay),
+                 e1z = __dsub_rn((double)bz, az);
+    const double e2x = __dsub_rn((double)cx, ax), e2y = __dsub_rn((double)cy, ay),
+                 e2z = __dsub_rn((double)cz, az);
+    const double px = __dsub_rn(__dmul_rn(dy, e2z), __dmul_rn(dz, e2y));
+    const double py = __dsub_rn(__dmul_rn(dz, e2x), __dmul_rn(dx, e2z));
+    const double pz = __dsub_rn(__dmul_rn(dx, e2y), __dmul_rn(dy, e2x));
+    const double det =
+        __dadd_rn(__dadd_rn(__dmul_rn(e1x, px), __dmul_rn(e1y, py)), __dmul_rn(e1z, pz));
+    if (fabs(det) < kDetEps) return false;
+    const double inv_det = __ddiv_rn(1.0, det);
+    const double tx = __dsub_rn(sx, ax), ty = __dsub_rn(sy, ay), tz = __dsub_rn(sz, az);
+    const double u = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(tx, px), __dmul_rn(ty, py)), __dmul_rn(tz, pz)), inv_det);
+    if (u < -kBaryEps || u > 1.0 + kBaryEps) return false;
+    const double qx = __dsub_rn(__dmul_rn(ty, e1z), __dmul_rn(tz, e1y));
+    const double qy = __dsub_rn(__dmul_rn(tz, e1x), __dmul_rn(tx, e1z));
+    const double qz = __dsub_rn(__dmul_rn(tx, e1y), __dmul_rn(ty, e1x));
+    const double v = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(dx, qx), __dmul_rn(dy, qy)), __dmul_rn(dz, qz)), inv_det);
+    if (v < -kBaryEps || __dadd_rn(u, v) > 1.0 + kBaryEps) return false;
+    const double t = __dmul_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz)),
+        inv_det);
+    if (t < 0.0 || t > 1.0) return false;
+    *t_out = t;
+    return true;
+}
+
+// _core.pyx:330-348: point = s + t*d (f64), distance = f32(sqrt(|p - s|^2)).
+__device__ __forceinline__ void hit_point(double sx, double sy, double sz, double dx, double dy,
+                                          double dz, double t, float* px_, float* py_,
+                                          float* pz_, float* dist) {
+    const double px = __dadd_rn(sx, __dmul_rn(t, dx));
+    const double py = __dadd_rn(sy, __dmul_rn(t, dy));
+    const double pz = __dadd_rn(sz, __dmul_rn(t, dz));
+    const double ddx = __dsub_rn(px, sx), ddy = __dsub_rn(py, sy), ddz = __dsub_rn(pz, sz);
+    const double s2 =
+        __dadd_rn(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)), __dmul_rn(ddz, ddz));
+    *dist = __double2float_rn(__dsqrt_rn(s2));
+    *px_ = __double2float_rn(px);
+    *py_ = __double2float_rn(py);
+    *pz_ = __double2float_rn(pz);
+}
+
+}  // namespace rs

@@ -1,0 +1,92 @@
+// rs_internal.h -- host-side declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "rs_common.cuh"
+
+namespace rs {
+
+// Number of kernels this library has launched (bench.py's gpu_launches).
+void count_launches(long long k);
+
+// The reference BvhTree SoA fields (lbvh.py:39-55) plus climb scratch.
+struct TreeArrays {
+    float* int_bounds;   // (n,6)
+    int* child_l;        // (n,)  slot n-1: root ref
+    int* child_r;
+    int* range_l;
+    int* range_r;
+    int* int_tri;        // -1 internal, -2 root
+    int* visit;
+    float* leaf_bounds;  // (n,6)
+    int* leaf_tri;
+    int* leaf_range_l;
+    int* leaf_range_r;
+    int* sorted_ids;
+    int* height;         // (2n,) subtree height by node ref
+};
+
+void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hdr,
+                 const TreeArrays& ta, bool centroids, cudaStream_t s);
+void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
+                 unsigned long long* keys, int* vals, cudaStream_t s);
+size_t sort_scratch_bytes(int n, int passes);
+void launch_sort(unsigned long long* keys, int* vals, unsigned long long* keys_alt,
+                 int* vals_alt, int n, int passes, void* scratch, cudaStream_t s);
+void launch_climb(const float* V, const int* T, int n, const unsigned long long* codes,
+                  const int* ids, const TreeArrays& ta, RsNode* nodes, RsLeaf* leaves,
+                  RsHeader* hdr, cudaStream_t s);
+
+// Query-side launch parameters.
+struct QueryArgs {
+    const RsNode* nodes;
+    const RsLeaf* leaves;
+    const RsHeader* hdr;  // root ref is read on device (no host sync after a build)
+    int n_int;
+    const float* starts;  // (n_r,3) f32 AoS
+    const float* ends;
+    long long n_r;
+    int max_coll;
+    int max_stack;
+    // dense outputs (rows [0, n_r) of the caller's arrays), any may be null
+    int* detected;
+    int* counts;
+    int* tri;
+    float* dist;
+    float* points;
+    // compact barycentric outputs
+    int* c_ray;
+    float* c_dist;
+    int* c_tri;
+    float* c_point;
+    unsigned long long* tile_status;
+    long long ray_offset;  // added to compacted ray indices
+    RsStatus* status;
+};
+
+// kstack: traversal stack capacity.  Fast trees (30-bit codes + 31-bit ids)
+// have height <= 61, so 64 always suffices; reference trees use
+// min(max_stack, 128) (height <= 94).
+// ref_semantics: emulate the reference's collision-buffer flush points and
+// max_stack overflow exactly (reference tree); compact: barycentric rows.
+int launch_query(const QueryArgs& a, int mode, bool ref_semantics, bool compact, int kstack,
+                 bool stats, cudaStream_t s);
+size_t compact_scratch_bytes(long long n_r);
+
+struct BaselineArgs {
+    const float* V;
+    const int* T;
+    int n_t;
+    const float* starts;
+    const float* ends;
+    long long n_r;
+    int* detected;
+    int* counts;
+    int* tri;
+    float* dist;
+    float* points;
+};
+void launch_baseline(const BaselineArgs& a, int mode, cudaStream_t s);
+
+}  // namespace rs

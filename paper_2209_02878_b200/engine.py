@@ -1,0 +1,397 @@
+"""Batch orchestration: the reference's public engine API on the B200 path.
+
+`run_batch` / `run_baseline_allpairs` keep the reference signatures and
+ResultSet semantics (raysurf/engine.py:35-335).  Where the reference fans
+segment chunks out to CPU threads (engine.py:160-180), this engine makes one
+native call: for host (numpy) inputs `rs_run_batch_host` streams the rays
+through the GPU (H2D / build / query / D2H overlapped in C++), for torch CUDA
+inputs `rs_run_batch_device` runs build + query + compaction on device.
+Nothing here computes intersections on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .exceptions import ValidationError
+from .mesh import Mesh, is_device_array
+
+MAX_COLLISIONS = 32  # lbvh.py:30-31
+MAX_STACK = 64
+MODE_BOOLEAN = "boolean"
+MODE_BARYCENTRIC = "barycentric"
+MODE_COUNT = "count"
+MODES = (MODE_BOOLEAN, MODE_BARYCENTRIC, MODE_COUNT)
+TREES = ("auto", "fast", "reference")
+BACKEND_NAME = "b200"
+
+
+@dataclass
+class SegmentBatch:
+    """Paired segment endpoints, (N_r,3) f32 each (engine.py:35-61); numpy
+    arrays or torch CUDA tensors."""
+
+    starts: object
+    ends: object
+
+    @classmethod
+    def from_arrays(cls, starts, ends) -> "SegmentBatch":
+        if is_device_array(starts):
+            import torch
+
+            s = starts.to(torch.float32).reshape(-1, 3).contiguous()
+            e = ends.to(device=s.device, dtype=torch.float32).reshape(-1, 3).contiguous()
+        else:
+            s = np.ascontiguousarray(starts, dtype=np.float32).reshape(-1, 3)
+            e = np.ascontiguousarray(ends, dtype=np.float32).reshape(-1, 3)
+        batch = cls(starts=s, ends=e)
+        batch.validate()
+        return batch
+
+    @property
+    def count(self) -> int:
+        return int(self.starts.shape[0])
+
+    @property
+    def on_device(self) -> bool:
+        return is_device_array(self.starts)
+
+    def validate(self) -> None:
+        if tuple(self.starts.shape) != tuple(self.ends.shape):
+            raise ValidationError(
+                f"segment start/end arrays differ in shape: "
+                f"{tuple(self.starts.shape)} vs {tuple(self.ends.shape)}")
+        if self.on_device:
+            import torch
+
+            ok = bool(torch.isfinite(self.starts).all()) and bool(torch.isfinite(self.ends).all())
+        else:
+            ok = bool(np.isfinite(self.starts).all() and np.isfinite(self.ends).all())
+        if not ok:
+            raise ValidationError("segment endpoints contain non-finite values")
+
+
+@dataclass(eq=False)
+class ResultSet:
+    """Per-mode output (engine.py:64-90).  boolean: `crossing` (N_r,) i32;
+    count: `counts` (N_r,) i32; barycentric: `ray_index` ascending with
+    `distance`, `triangle_id`, `point` rows.  Arrays are numpy for host
+    inputs and torch CUDA tensors for device inputs."""
+
+    mode: str
+    num_rays: int
+    crossing: object = None
+    counts: object = None
+    ray_index: object = None
+    distance: object = None
+    triangle_id: object = None
+    point: object = None
+    timings: dict = field(default_factory=dict)
+
+    def num_crossing(self) -> int:
+        if self.mode == MODE_BOOLEAN:
+            return int((self.crossing != 0).sum())
+        if self.mode == MODE_COUNT:
+            return int((self.counts != 0).sum())
+        return int(self.ray_index.shape[0])
+
+
+@dataclass
+class EngineConfig:
+    """engine.py:93-112 plus the tree choice.
+
+    tree="auto" builds the isotropic 30-bit "fast" tree (identical results,
+    ~3.7x fewer node visits on terrain) unless max_stack is lowered below the
+    default, in which case the reference tree is built so the
+    TraversalStackOverflow segment index matches the reference exactly.
+    `workers` is validated for compatibility; the GPU path ignores it.
+    """
+
+    mode: str = MODE_BOOLEAN
+    sort_rays: bool = False
+    workers: int | None = None
+    max_collisions: int = MAX_COLLISIONS
+    max_stack: int = MAX_STACK
+    backend: str | None = None
+    tree: str = "auto"
+    chunk_rays: int = 0
+
+    def resolved_workers(self) -> int:
+        if self.workers is None:
+            return max(1, os.cpu_count() or 1)
+        if self.workers < 1:
+            raise ValidationError("workerCount must be >= 1")
+        return self.workers
+
+    def resolved_tree(self) -> str:
+        if self.tree != "auto":
+            return self.tree
+        return "reference" if self.max_stack < MAX_STACK else "fast"
+
+    def validate(self) -> None:
+        if self.mode not in MODES:
+            raise ValidationError(f"unknown mode {self.mode!r}")
+        self.resolved_workers()
+        if self.backend not in (None, BACKEND_NAME):
+            raise ValidationError(f"unknown backend {self.backend!r} (have: {BACKEND_NAME})")
+        if self.tree not in TREES:
+            raise ValidationError(f"unknown tree {self.tree!r} (have: {', '.join(TREES)})")
+        if self.max_collisions < 2:  # lbvh.py:92-93
+            raise ValidationError("collision buffer needs capacity >= 2")
+        if self.max_stack < 1:
+            raise ValidationError("traversal stack needs capacity >= 1")
+
+
+def compute_segment_boxes(segments: SegmentBatch) -> np.ndarray:
+    """(N_r,6) f32 segment AABBs (engine.py:115-122).  Host helper kept for
+    API parity; the query kernel computes the same boxes in registers."""
+    s = np.asarray(segments.starts.cpu() if segments.on_device else segments.starts)
+    e = np.asarray(segments.ends.cpu() if segments.on_device else segments.ends)
+    boxes = np.empty((s.shape[0], 6), dtype=np.float32)
+    boxes[:, 0::2] = np.minimum(s, e)
+    boxes[:, 1::2] = np.maximum(s, e)
+    return boxes
+
+
+def sort_segments_by_morton(segments: SegmentBatch):
+    """Z-order of segment midpoints (engine.py:125-147): returns the permuted
+    batch and perm (perm[k] = original index of sorted slot k)."""
+    from . import morton
+
+    n = segments.count
+    if n == 0:
+        return segments, np.empty(0, dtype=np.int64)
+    host = not segments.on_device
+    s = np.asarray(segments.starts if host else segments.starts.cpu())
+    e = np.asarray(segments.ends if host else segments.ends.cpu())
+    mid = (s.astype(np.float64) + e.astype(np.float64)) / 2.0
+    perm = morton.order_points(mid)
+    if host:
+        return SegmentBatch(np.ascontiguousarray(s[perm]), np.ascontiguousarray(e[perm])), perm
+    import torch
+
+    p = torch.from_numpy(perm).to(segments.starts.device)
+    return SegmentBatch(segments.starts[p].contiguous(), segments.ends[p].contiguous()), perm
+
+
+# --------------------------------------------------------------- internals --
+
+def _ptr(a) -> C.c_void_p:
+    if a is None:
+        return C.c_void_p(0)
+    if isinstance(a, np.ndarray):
+        return C.c_void_p(a.ctypes.data)
+    return C.c_void_p(a.data_ptr())
+
+
+def _stream():
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _host_empty(shape, dtype):
+    """Pinned host array (so D2H runs at full PCIe rate); torch caches the
+    pinned blocks across calls."""
+    import torch
+
+    tdt = {np.int32: torch.int32, np.float32: torch.float32}[dtype]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+
+def _empty_result(mode: str, n: int, like_device=None) -> ResultSet:
+    if like_device is not None:
+        import torch
+
+        dev = like_device
+        z = lambda *s, dt=torch.int32: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
+        if mode == MODE_BOOLEAN:
+            return ResultSet(mode, n, crossing=z(n))
+        if mode == MODE_COUNT:
+            return ResultSet(mode, n, counts=z(n))
+        return ResultSet(mode, n, ray_index=z(0), distance=z(0, dt=torch.float32),
+                         triangle_id=z(0), point=z(0, 3, dt=torch.float32))
+    if mode == MODE_BOOLEAN:
+        return ResultSet(mode, n, crossing=np.zeros(n, np.int32))
+    if mode == MODE_COUNT:
+        return ResultSet(mode, n, counts=np.zeros(n, np.int32))
+    return ResultSet(mode, n, ray_index=np.zeros(0, np.int32), distance=np.zeros(0, np.float32),
+                     triangle_id=np.zeros(0, np.int32), point=np.zeros((0, 3), np.float32))
+
+
+def _unpermute(rs: ResultSet, perm) -> ResultSet:
+    """engine.py:191-198 for permuted inputs, then re-sort compacted rows."""
+    if perm is None:
+        return rs
+    dev = rs.mode != MODE_BARYCENTRIC and is_device_array(rs.crossing if rs.mode == MODE_BOOLEAN else rs.counts)
+    if rs.mode in (MODE_BOOLEAN, MODE_COUNT):
+        key = "crossing" if rs.mode == MODE_BOOLEAN else "counts"
+        vals = getattr(rs, key)
+        if dev:
+            import torch
+
+            out = torch.empty_like(vals)
+            out[torch.from_numpy(perm).to(vals.device)] = vals
+        else:
+            out = np.empty_like(vals)
+            out[perm] = vals
+        setattr(rs, key, out)
+        return rs
+    ri = rs.ray_index
+    if is_device_array(ri):
+        import torch
+
+        pt = torch.from_numpy(perm).to(ri.device)
+        orig = pt[ri.long()]
+        order = torch.argsort(orig)
+        rs.ray_index = orig[order].to(torch.int32)
+        rs.distance, rs.triangle_id, rs.point = rs.distance[order], rs.triangle_id[order], rs.point[order]
+    else:
+        orig = perm[ri]
+        order = np.argsort(orig, kind="stable")
+        rs.ray_index = orig[order].astype(np.int32)
+        rs.distance, rs.triangle_id, rs.point = rs.distance[order], rs.triangle_id[order], rs.point[order]
+    return rs
+
+
+def _run_host(mesh: Mesh, seg: SegmentBatch, config: EngineConfig, kind: str) -> ResultSet:
+    n = seg.count
+    mode = config.mode
+    flags = ray = dist = tri = pt = None
+    if mode == MODE_BARYCENTRIC:
+        ray, dist = _host_empty(n, np.int32), _host_empty(n, np.float32)
+        tri, pt = _host_empty(n, np.int32), _host_empty((n, 3), np.float32)
+    else:
+        flags = _host_empty(n, np.int32)
+    n_hits, bad = C.c_int64(0), C.c_int64(-1)
+    t0 = time.perf_counter()
+    st = _lib.lib().rs_run_batch_host(
+        _ptr(mesh.vertices), mesh.num_vertices, _ptr(mesh.triangles), mesh.num_triangles,
+        _ptr(seg.starts), _ptr(seg.ends), n, _lib.MODE_TAGS[mode], _lib.TREE_KINDS[kind],
+        config.max_collisions, config.max_stack, int(config.chunk_rays),
+        _ptr(flags), _ptr(ray), _ptr(dist), _ptr(tri), _ptr(pt), C.byref(n_hits), C.byref(bad),
+        _stream())
+    elapsed = time.perf_counter() - t0
+    _lib.check(st, bad.value, config.max_stack)
+    timings = {"query": elapsed}
+    if mode == MODE_BOOLEAN:
+        return ResultSet(mode, n, crossing=flags, timings=timings)
+    if mode == MODE_COUNT:
+        return ResultSet(mode, n, counts=flags, timings=timings)
+    k = n_hits.value
+    return ResultSet(mode, n, ray_index=ray[:k], distance=dist[:k], triangle_id=tri[:k],
+                     point=pt[:k], timings=timings)
+
+
+def run_device(mesh: Mesh, seg: SegmentBatch, config: EngineConfig, kind: str,
+               out: dict | None = None) -> ResultSet:
+    """Device-resident run_batch: torch CUDA tensors in, torch CUDA tensors
+    out, one native call (build + query + compaction).  `out` may supply
+    preallocated output tensors (bench.py reuses them across steps)."""
+    import torch
+
+    n = seg.count
+    mode = config.mode
+    dev = seg.starts.device
+    out = out or {}
+    if mode == MODE_BARYCENTRIC:
+        ray = out.get("ray") if out.get("ray") is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        dist = out.get("dist") if out.get("dist") is not None else torch.empty(n, dtype=torch.float32, device=dev)
+        tri = out.get("tri") if out.get("tri") is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        pt = out.get("pt") if out.get("pt") is not None else torch.empty((n, 3), dtype=torch.float32, device=dev)
+        flags = None
+    else:
+        flags = out.get("flags") if out.get("flags") is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        ray = dist = tri = pt = None
+    n_hits, bad = C.c_int64(0), C.c_int64(-1)
+    st = _lib.lib().rs_run_batch_device(
+        _ptr(mesh.vertices), mesh.num_vertices, _ptr(mesh.triangles), mesh.num_triangles,
+        _ptr(seg.starts), _ptr(seg.ends), n, _lib.MODE_TAGS[mode], _lib.TREE_KINDS[kind],
+        config.max_collisions, config.max_stack, _ptr(flags), _ptr(ray), _ptr(dist), _ptr(tri),
+        _ptr(pt), C.byref(n_hits), C.byref(bad), _stream())
+    _lib.check(st, bad.value, config.max_stack)
+    if mode == MODE_BOOLEAN:
+        return ResultSet(mode, n, crossing=flags)
+    if mode == MODE_COUNT:
+        return ResultSet(mode, n, counts=flags)
+    k = n_hits.value
+    return ResultSet(mode, n, ray_index=ray[:k], distance=dist[:k], triangle_id=tri[:k], point=pt[:k])
+
+
+def run_batch(mesh: Mesh, segments: SegmentBatch, config: EngineConfig | None = None) -> ResultSet:
+    """Index the mesh on the GPU and test every segment (engine.py:222-290).
+
+    Results equal the reference's for the same inputs in every mode."""
+    config = config or EngineConfig()
+    config.validate()
+    n = segments.count
+    dev = segments.on_device
+    if dev != mesh.on_device and mesh.num_triangles and n:
+        raise ValidationError("mesh and segments must both be host arrays or both CUDA tensors")
+    if n == 0 or mesh.num_triangles == 0:
+        return _empty_result(config.mode, n, segments.starts.device if dev else None)
+    timings = {}
+    perm = None
+    if config.sort_rays:
+        t0 = time.perf_counter()
+        segments, perm = sort_segments_by_morton(segments)
+        timings["ray sort"] = time.perf_counter() - t0
+    kind = config.resolved_tree()
+    if dev:
+        t0 = time.perf_counter()
+        rs = run_device(mesh, segments, config, kind)
+        rs.timings["query"] = time.perf_counter() - t0
+    else:
+        rs = _run_host(mesh, segments, config, kind)
+    rs.timings.update(timings)
+    return _unpermute(rs, perm)
+
+
+def run_baseline_allpairs(mesh: Mesh, segments: SegmentBatch,
+                          config: EngineConfig | None = None) -> ResultSet:
+    """Every (segment, triangle) pair on the GPU (engine.py:293-335); results
+    identical to run_batch."""
+    from ._backend import b200
+
+    config = config or EngineConfig()
+    config.validate()
+    n = segments.count
+    dev = segments.on_device
+    if n == 0 or mesh.num_triangles == 0:
+        return _empty_result(config.mode, n, segments.starts.device if dev else None)
+    perm = None
+    timings = {}
+    if config.sort_rays:
+        t0 = time.perf_counter()
+        segments, perm = sort_segments_by_morton(segments)
+        timings["ray sort"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    out = b200.baseline_dense(mesh, segments, config.mode)
+    timings["query"] = time.perf_counter() - t0
+    rs = _assemble_dense(config.mode, out, n, dev)
+    rs.timings = timings
+    return _unpermute(rs, perm)
+
+
+def _assemble_dense(mode: str, out: dict, n: int, dev: bool) -> ResultSet:
+    """engine.py:200-215 over dense per-segment rows."""
+    if mode == MODE_BOOLEAN:
+        return ResultSet(mode, n, crossing=out["detected"])
+    if mode == MODE_COUNT:
+        return ResultSet(mode, n, counts=out["counts"])
+    det = out["detected"]
+    if dev:
+        import torch
+
+        idx = torch.nonzero(det).flatten()
+        return ResultSet(mode, n, ray_index=idx.to(torch.int32), distance=out["dist"][idx],
+                         triangle_id=out["tri"][idx], point=out["points"][idx])
+    idx = np.nonzero(det)[0].astype(np.int32)
+    return ResultSet(mode, n, ray_index=idx, distance=out["dist"][idx],
+                     triangle_id=out["tri"][idx], point=out["points"][idx])

@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference's own
+outputs (golden fixtures) and vs the C oracle on fresh inputs.
+
+Bar: integer/index fields bit-exact; distance/point
+bit-exact as well (f64 Moller-Trumbore in the reference op order, no FMA).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2209_02878_b200 as rs  # noqa: E402
+from paper_2209_02878_b200._backend import b200  # noqa: E402
+from golden_io import (MODES, OVERFLOWS, SCENES, SOUPS, TREE_FIELDS, TREE_SIZES,  # noqa: E402
+                       assert_result_fields, expected, load)
+from oracle import oracle as O  # noqa: E402
+
+
+def _np(x):
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+def result_dict(r):
+    return {f: _np(getattr(r, f)) for f in ("crossing", "counts", "ray_index", "distance",
+                                            "triangle_id", "point") if getattr(r, f) is not None}
+
+
+def mesh_batch(fx, device=False):
+    V, T, s, e = fx["vertices"], fx["triangles"], fx["starts"], fx["ends"]
+    if device:
+        V, T, s, e = (torch.from_numpy(a).cuda() for a in (V, T, s, e))
+    return rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e)
+
+
+# ------------------------------------------------------------------ trees --
+
+@pytest.mark.parametrize("n", TREE_SIZES)
+def test_tree_from_sorted_matches_reference(n):
+    fx = load(f"tree_{n}")
+    mesh = rs.Mesh.from_arrays(fx["vertices"], fx["triangles"])
+    tree, _, _ = b200.build_tree(mesh, fx["sorted_codes"], fx["sorted_ids"])
+    for f in TREE_FIELDS:
+        assert np.array_equal(getattr(tree, f), fx[f"tree_{f}"]), f
+
+
+@pytest.mark.parametrize("n", TREE_SIZES)
+def test_device_keys_and_sort_match_reference(n):
+    fx = load(f"tree_{n}")
+    mesh = rs.Mesh.from_arrays(fx["vertices"], fx["triangles"])
+    tree = b200.DeviceTree(mesh, kind="reference").download()
+    for f in TREE_FIELDS:
+        assert np.array_equal(getattr(tree, f), fx[f"tree_{f}"]), f
+
+
+@pytest.mark.parametrize("n", TREE_SIZES)
+def test_fast_tree_matches_oracle(n):
+    fx = load(f"tree_{n}")
+    V, T = fx["vertices"], fx["triangles"]
+    codes, ids = O.sorted_keys(V, T, "fast", 10)
+    want = O.build_tree(V, T, codes, ids)
+    got = b200.DeviceTree(rs.Mesh.from_arrays(V, T), kind="fast").download()
+    for f in TREE_FIELDS:
+        assert np.array_equal(getattr(got, f), want[f]), f
+
+
+def test_large_tree_matches_oracle():
+    sc = rs.generate_scene(200_000, 10, 0.5, seed=5)
+    V, T = sc.mesh.vertices, sc.mesh.triangles
+    for kind in ("reference", "fast"):
+        codes, ids = O.sorted_keys(V, T, kind, 10)
+        want = O.build_tree(V, T, codes, ids)
+        got = b200.DeviceTree(sc.mesh, kind=kind).download()
+        for f in TREE_FIELDS:
+            assert np.array_equal(getattr(got, f), want[f]), (kind, f)
+
+
+# ---------------------------------------------------------------- results --
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+@pytest.mark.parametrize("tree", ["fast", "reference"])
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", SCENES)
+def test_scene_results_bitwise(name, mode, tree, device):
+    fx = load(f"scene_{name}")
+    mesh, batch = mesh_batch(fx, device)
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree=tree))
+    assert_result_fields(result_dict(got), expected(fx, "batch", mode), f"{name} {mode} {tree}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", SCENES + tuple(f"soup:{s}" for s in SOUPS))
+def test_baseline_bitwise(name, mode):
+    fx = load(f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}")
+    mesh, batch = mesh_batch(fx)
+    got = rs.run_baseline_allpairs(mesh, batch, rs.EngineConfig(mode=mode))
+    assert_result_fields(result_dict(got), expected(fx, "base", mode), f"{name} baseline {mode}")
+
+
+@pytest.mark.parametrize("tree", ["fast", "reference"])
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", SOUPS)
+def test_soup_results_with_resume(name, mode, tree):
+    fx = load(f"soup_{name}")
+    mesh, batch = mesh_batch(fx)
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree=tree))
+    assert_result_fields(result_dict(got), expected(fx, "batch", mode), name)
+    for cap in (4, 8):
+        got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree=tree, max_collisions=cap))
+        assert_result_fields(result_dict(got), expected(fx, f"cap{cap}", mode), f"{name} cap{cap}")
+
+
+@pytest.mark.parametrize("via", ["engine", "plugin", "host-chunks"])
+@pytest.mark.parametrize("name", OVERFLOWS)
+def test_overflow_index(name, via):
+    fx = load(f"soup_{name}")
+    mesh, batch = mesh_batch(fx)
+    for mode_i, cap, st, idx in fx["overflow"].tolist():
+        mode = MODES[mode_i]
+        try:
+            if via == "plugin":
+                tree, _, _ = b200.build_tree(mesh, fx["sorted_codes"], fx["sorted_ids"])
+                out = O.empty_outputs(batch.count)
+                b200.batch_query(mesh, tree, batch, None, mode, cap, st, 0, batch.count, out)
+            else:
+                cfg = rs.EngineConfig(mode=mode, max_collisions=cap, max_stack=st,
+                                      chunk_rays=128 if via == "host-chunks" else 0)
+                rs.run_batch(mesh, batch, cfg)
+            got = -1
+        except rs.TraversalStackOverflow as exc:
+            got = exc.segment_index
+        assert got == idx, (mode, cap, st, via)
+
+
+@pytest.mark.parametrize("cap", (32, 8))
+@pytest.mark.parametrize("mode", MODES)
+def test_layered(cap, mode):
+    fx = load("layered")
+    mesh, batch = mesh_batch(fx)
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, max_collisions=cap))
+    assert_result_fields(result_dict(got), expected(fx, f"cap{cap}", mode), f"layered cap{cap}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_plugin_protocol_chunks(mode):
+    """build_tree + batch_query/batch_baseline over uneven [lo, hi) chunks,
+    as the reference engine drives a backend (engine.py:160-180)."""
+    fx = load("soup_17")
+    mesh, batch = mesh_batch(fx)
+    tree, _, _ = b200.build_tree(mesh, fx["sorted_codes"], fx["sorted_ids"])
+    n = batch.count
+    out_q, out_b = O.empty_outputs(n), O.empty_outputs(n)
+    for lo, hi in ((0, 1), (1, 97), (97, 300), (300, n)):
+        b200.batch_query(mesh, tree, batch, None, mode, 32, 64, lo, hi, out_q)
+        b200.batch_baseline(mesh, None, batch, None, mode, lo, hi, out_b)
+    assert_result_fields(O.assemble(mode, out_q), expected(fx, "batch", mode), "plugin query")
+    assert_result_fields(O.assemble(mode, out_b), expected(fx, "base", mode), "plugin baseline")
+
+
+# --------------------------------------------------- fresh inputs vs oracle --
+
+def _random_soup(seed, n_tri, n_seg, span=12.0):
+    rng = np.random.default_rng(seed)
+    nv = max(3, n_tri + 2)
+    V = rng.uniform(-10, 10, size=(nv, 3)).astype(np.float32)
+    T = np.stack([rng.choice(nv, 3, replace=False) for _ in range(n_tri)]).astype(np.int32)
+    s = rng.uniform(-span, span, size=(n_seg, 3)).astype(np.float32)
+    e = rng.uniform(-span, span, size=(n_seg, 3)).astype(np.float32)
+    return V, T, s, e
+
+
+@pytest.mark.parametrize("seed,n_tri,n_seg", [(1, 1, 50), (2, 2, 300), (3, 64, 2000),
+                                              (4, 700, 3000), (5, 3000, 1000)])
+@pytest.mark.parametrize("mode", MODES)
+def test_random_soup_vs_oracle(seed, n_tri, n_seg, mode):
+    V, T, s, e = _random_soup(seed, n_tri, n_seg)
+    want = O.run_batch(V, T, s, e, mode=mode, max_stack=10**6)
+    for tree in ("fast", "reference"):
+        got = rs.run_batch(rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e),
+                           rs.EngineConfig(mode=mode, tree=tree, max_stack=256))
+        assert_result_fields(result_dict(got), want, f"soup {seed} {mode} {tree}")
+
+
+def test_edge_cases():
+    # single triangle (leaf root), zero-length segments, touching boxes, in-plane segments
+    V = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float32)
+    T = np.array([[0, 1, 2]], np.int32)
+    s = np.array([[0.25, 0.25, -1], [0.25, 0.25, 0], [2, 2, -1], [-1, 0.25, 0],
+                  [0, 0, -1], [1, 0, 0], [0.5, 0.5, 1]], np.float32)
+    e = np.array([[0.25, 0.25, 1], [0.25, 0.25, 0], [2, 2, 1], [2, 0.25, 0],
+                  [0, 0, 1], [1, 0, 0], [0.5, 0.5, -1]], np.float32)
+    for mode in MODES:
+        want = O.run_batch(V, T, s, e, mode=mode)
+        got = rs.run_batch(rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e),
+                           rs.EngineConfig(mode=mode))
+        assert_result_fields(result_dict(got), want, f"edge {mode}")
+    # empty batch / empty mesh (engine.py:233-234)
+    empty = rs.SegmentBatch.from_arrays(np.zeros((0, 3)), np.zeros((0, 3)))
+    for mode in MODES:
+        r = rs.run_batch(rs.Mesh.from_arrays(V, T), empty, rs.EngineConfig(mode=mode))
+        assert r.num_rays == 0 and r.num_crossing() == 0
+        r = rs.run_batch(rs.Mesh.from_arrays(np.zeros((0, 3)), np.zeros((0, 3))),
+                         rs.SegmentBatch.from_arrays(s, e), rs.EngineConfig(mode=mode))
+        assert r.num_crossing() == 0
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sort_rays_invariance(mode):
+    fx = load("scene_s19")
+    mesh, batch = mesh_batch(fx)
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, sort_rays=True))
+    assert_result_fields(result_dict(got), expected(fx, "batch", mode), f"sort_rays {mode}")
+
+
+@pytest.mark.parametrize("chunk", [128, 1000, 4096])
+@pytest.mark.parametrize("mode", MODES)
+def test_host_pipeline_chunking(mode, chunk):
+    fx = load("scene_c1")
+    mesh, batch = mesh_batch(fx)
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, chunk_rays=chunk))
+    assert_result_fields(result_dict(got), expected(fx, "batch", mode), f"chunk {chunk}")
+
+
+# ----------------------------------------------- full-size, property-based --
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c2_full_size_ground_truth(mode):
+    """BASELINE configs[1]/[2] at full size (29,284 tris x 10M segments):
+    generated ground truth for every segment, plus a bitwise oracle check
+    on a 200k-segment sample."""
+    sc = rs.generate_scene(29_284, 10_000_000, 0.5, seed=2022)
+    mesh, batch = sc.mesh, sc.segments
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode))
+    truth = sc.expected_crossings.astype(np.int32)
+    if mode == "boolean":
+        assert np.array_equal(got.crossing, truth)
+    elif mode == "count":
+        assert np.array_equal(got.counts, truth)
+    else:
+        assert np.array_equal(got.ray_index, np.nonzero(truth)[0])
+    idx = np.random.default_rng(0).choice(batch.count, 200_000, replace=False)
+    idx.sort()
+    s, e = batch.starts[idx], batch.ends[idx]
+    want = O.run_batch(mesh.vertices, mesh.triangles, s, e, mode=mode)
+    sub = rs.run_batch(mesh, rs.SegmentBatch.from_arrays(s, e), rs.EngineConfig(mode=mode))
+    assert_result_fields(result_dict(sub), want, f"C2 sample {mode}")
+    if mode == "barycentric":
+        # dense full-size rows agree with the sampled rows at the same segments
+        pos = np.searchsorted(got.ray_index, idx[want["ray_index"]])
+        assert np.array_equal(got.triangle_id[pos], want["triangle_id"])
+        assert np.array_equal(got.point[pos], want["point"])
+        assert np.array_equal(got.distance[pos], want["distance"])
+
+
+def test_device_path_matches_host_path_c2():
+    sc = rs.generate_scene(29_284, 2_000_000, 0.5, seed=7)
+    host = rs.run_batch(sc.mesh, sc.segments, rs.EngineConfig(mode="barycentric"))
+    dm = rs.Mesh.from_arrays(torch.from_numpy(sc.mesh.vertices).cuda(),
+                             torch.from_numpy(sc.mesh.triangles).cuda())
+    db = rs.SegmentBatch.from_arrays(torch.from_numpy(sc.segments.starts).cuda(),
+                                     torch.from_numpy(sc.segments.ends).cuda())
+    dev = rs.run_batch(dm, db, rs.EngineConfig(mode="barycentric"))
+    for f in ("ray_index", "distance", "triangle_id", "point"):
+        assert np.array_equal(_np(getattr(dev, f)), getattr(host, f)), f

@@ -1,0 +1,124 @@
+"""CPU-only checks of the host side: the C-ABI library loads and exports
+what the header declares, the scene generator reproduces the reference,
+config validation and the sort_rays permutation logic."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2209_02878_b200 as rs
+from paper_2209_02878_b200 import _lib, morton
+from golden_io import SCENES, load
+from oracle import oracle as O
+
+
+def test_library_exports_every_header_symbol():
+    names = _lib.header_symbols()
+    assert len(names) >= 13
+    dll = C.CDLL(str(_lib.LIB_PATH))
+    for n in names:
+        assert hasattr(dll, n), n
+    assert set(names) == set(_lib._SIGS), "ctypes signatures out of sync with the header"
+    assert _lib.lib().rs_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_generate_scene_reproduces_reference(name):
+    fx = load(f"scene_{name}")
+    n_tri, n_ray, seed = fx["params"].tolist()
+    sc = rs.generate_scene(n_tri, n_ray, float(fx["frac"]), seed)
+    assert np.array_equal(sc.mesh.vertices, fx["vertices"])
+    assert np.array_equal(sc.mesh.triangles, fx["triangles"])
+    assert np.array_equal(sc.segments.starts, fx["starts"])
+    assert np.array_equal(sc.segments.ends, fx["ends"])
+    assert np.array_equal(sc.expected_crossings, fx["expected"])
+
+
+def test_layered_scene_counts_by_construction():
+    base = rs.generate_scene(300, 2000, 0.5, seed=3)
+    lay = rs.layered_scene(base, layers=4)
+    assert lay.mesh.num_triangles == 4 * 300
+    want = O.run_batch(lay.mesh.vertices, lay.mesh.triangles, lay.segments.starts,
+                       lay.segments.ends, mode="count")
+    assert np.array_equal(want["counts"], lay.expected_crossings)
+
+
+def test_config_validation():
+    with pytest.raises(rs.ValidationError):
+        rs.EngineConfig(mode="nope").validate()
+    with pytest.raises(rs.ValidationError):
+        rs.EngineConfig(workers=0).validate()
+    with pytest.raises(rs.ValidationError):
+        rs.EngineConfig(max_collisions=1).validate()  # reference compiled path would overrun
+    with pytest.raises(rs.ValidationError):
+        rs.EngineConfig(max_stack=0).validate()
+    with pytest.raises(rs.ValidationError):
+        rs.EngineConfig(backend="compiled").validate()
+    with pytest.raises(rs.ValidationError):
+        rs.EngineConfig(tree="bvh8").validate()
+    assert rs.EngineConfig().resolved_tree() == "fast"
+    assert rs.EngineConfig(max_stack=3).resolved_tree() == "reference"
+    assert rs.EngineConfig(tree="reference").resolved_tree() == "reference"
+
+
+def test_segment_and_mesh_validation():
+    with pytest.raises(rs.ValidationError):
+        rs.SegmentBatch.from_arrays(np.zeros((2, 3)), np.zeros((3, 3)))
+    with pytest.raises(rs.ValidationError):
+        rs.SegmentBatch.from_arrays([[0, 0, np.nan]], [[1, 1, 1]])
+    with pytest.raises(rs.ValidationError):
+        rs.Mesh.from_arrays(np.zeros((3, 3)), [[0, 1, 3]])
+    with pytest.raises(rs.ValidationError):
+        rs.Mesh.from_arrays(np.zeros((3, 3)), [[0, 1, 1]])
+    with pytest.raises(rs.ValidationError):
+        rs.Mesh.from_arrays([[0, 0, np.inf]] * 3, [[0, 1, 2]])
+
+
+def test_sort_rays_permutation_matches_reference_rule():
+    rng = np.random.default_rng(2)
+    s = rng.uniform(-12, 12, size=(5000, 3)).astype(np.float32)
+    e = rng.uniform(-12, 12, size=(5000, 3)).astype(np.float32)
+    batch = rs.SegmentBatch.from_arrays(s, e)
+    sorted_batch, perm = rs.sort_segments_by_morton(batch)
+    mid = (s.astype(np.float64) + e.astype(np.float64)) / 2.0
+    lo, hi = O.support(mid)
+    codes = O.morton_codes(O.quantize(mid, lo, hi))
+    _, want = O.sort_by_code(codes)
+    assert np.array_equal(perm, want)
+    restored = np.empty_like(sorted_batch.starts)
+    restored[perm] = sorted_batch.starts
+    assert np.array_equal(restored, s)
+    again, perm2 = rs.sort_segments_by_morton(sorted_batch)  # fixed point (test_engine.py:65-71)
+    assert np.array_equal(perm2, np.arange(5000))
+
+
+def test_morton_encode_known_answers():
+    top = morton.GRID_MAX
+    q = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [top, top, top]], np.uint32)
+    assert morton.encode(q).tolist() == [0, 1, 2, 4, 2**63 - 1]
+    fx = load("morton")
+    assert np.array_equal(morton.encode(fx["q"]), fx["codes"])
+    assert np.array_equal(morton.quantize(fx["pts"]), fx["pts_q"])
+
+
+def test_unpermute_barycentric_rows():
+    from paper_2209_02878_b200.engine import ResultSet, _unpermute
+
+    perm = np.array([3, 0, 2, 1])
+    r = ResultSet("barycentric", 4, ray_index=np.array([0, 2, 3], np.int32),
+                  distance=np.array([1, 2, 3], np.float32), triangle_id=np.array([7, 8, 9], np.int32),
+                  point=np.arange(9, dtype=np.float32).reshape(3, 3))
+    r = _unpermute(r, perm)
+    assert r.ray_index.tolist() == [1, 2, 3]
+    assert r.triangle_id.tolist() == [9, 8, 7]
+    b = _unpermute(ResultSet("boolean", 4, crossing=np.array([1, 0, 0, 1], np.int32)), perm)
+    assert b.crossing.tolist() == [0, 1, 0, 1]

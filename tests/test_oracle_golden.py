@@ -82,3 +82,15 @@ def test_layered(cap, mode):
     args = (fx["vertices"], fx["triangles"], fx["starts"], fx["ends"])
     got = O.run_batch(*args, mode=mode, max_coll=cap)
     assert_result_fields(got, expected(fx, f"cap{cap}", mode), f"layered cap{cap}")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_reference_arm_matches_golden(mode):
+    """oracle/ref_engine.py (the reference's compiled kernel, or the C port
+    when it is absent) reproduces the reference results."""
+    from oracle import ref_engine
+
+    fx = load("scene_s19")
+    res, _ = ref_engine.run_batch(fx["vertices"], fx["triangles"], fx["starts"], fx["ends"],
+                                  mode=mode, workers=3)
+    assert_result_fields(res, expected(fx, "batch", mode), f"ref arm {mode}")

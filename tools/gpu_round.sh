@@ -1,0 +1,25 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench, ncu launch list + one full capture.
+# usage: gpurun --timeout 1500 -- bash tools/gpu_round.sh [tag] [what...]
+set -u
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+TAG=${1:-r1}; shift || true
+WHAT=${*:-"tests smoke bench ncu"}
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi -L > "$OUT/gpu.txt" 2>&1
+for w in $WHAT; do
+  case $w in
+    tests) timeout 900 python -m pytest tests -x -q -m gpu -p no:cacheprovider > "$OUT/pytest_gpu.txt" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.txt";;
+    quick) timeout 600 python -m pytest tests -x -q -m gpu -p no:cacheprovider -k "not c2_full and not large_tree" > "$OUT/pytest_gpu.txt" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.txt";;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.txt" 2>&1; echo "smoke rc=$?" >> "$OUT/smoke.txt";;
+    bench) timeout 600 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err";;
+    bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
+    ncu)
+      timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+        --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_bench.log" 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_query -s 2 -c 1 \
+        -o "$OUT/query" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_full.log" 2>&1;;
+  esac
+done
+ls -la "$OUT"
