@@ -39,6 +39,8 @@ def expected(fx: dict, prefix: str, mode: str) -> dict:
 def assert_result_fields(got: dict, want: dict, context: str = "", float_tol: float = 0.0):
     """tests/helpers.py:65-82 semantics: exact, floats optionally to float_tol."""
     for f, w in want.items():
+        if f == "mode":
+            continue
         g = got.get(f)
         assert g is not None, f"{context}: missing {f}"
         g = np.asarray(g)
