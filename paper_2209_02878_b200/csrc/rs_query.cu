@@ -16,12 +16,20 @@
 // identical (tests/test_gpu_parity.py::test_overflow_index).
 #include <cuda/atomic>
 
+#include <cstdlib>
+
 #include "rs_common.cuh"
 #include "rs_internal.h"
 
 namespace rs {
 
 constexpr int kQueryThreads = 128;
+
+// RS_SIMPLE_QUERY=1 selects the one-segment-per-thread kernel (A/B tuning).
+static const bool g_simple_query = [] {
+    const char* e = getenv("RS_SIMPLE_QUERY");
+    return e && e[0] == '1';
+}();
 
 struct Ray {
     float box[6];
@@ -193,6 +201,132 @@ __global__ void __launch_bounds__(kQueryThreads) k_query_dense(QueryArgs a) {
     if (STATS) flush_stats(a, visits, mts);
 }
 
+// ---------------------------------------------------- persistent warps ---
+//
+// One traversal step = one internal-node visit.  Returns 0 (continue),
+// 1 (ray finished), 2 (reference max_stack overflow), 3 (internal capacity).
+struct Trav {
+    int node;
+    int top;
+    int count;
+};
+
+template <int MODE, bool REF, int KSTACK>
+__device__ __forceinline__ int trav_step(const QueryArgs& a, const Ray& r, Hit& h, Trav& t,
+                                         int* stack, int cap, unsigned long long& visits,
+                                         unsigned long long& mts) {
+    const int n_int = a.n_int;
+    const int node = t.node;
+    if (node >= n_int) {  // single-triangle tree: leaf root (_core.pyx:260-267)
+        const float4 p0 = __ldg(&a.leaves[0].p0), p1 = __ldg(&a.leaves[0].p1),
+                     p2 = __ldg(&a.leaves[0].p2);
+        const float x0 = fminf(fminf(p0.x, p0.w), p1.z), x1 = fmaxf(fmaxf(p0.x, p0.w), p1.z);
+        const float y0 = fminf(fminf(p0.y, p1.x), p1.w), y1 = fmaxf(fmaxf(p0.y, p1.x), p1.w);
+        const float z0 = fminf(fminf(p0.z, p1.y), p2.x), z1 = fmaxf(fmaxf(p0.z, p1.y), p2.x);
+        if (overlap6(r.box, x0, x1, y0, y1, z0, z1)) test_leaf<MODE>(a.leaves, 0, r, h, mts);
+        return 1;
+    }
+    ++visits;
+    const float4* np = reinterpret_cast<const float4*>(a.nodes + node);
+    const float4 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
+    const int4 nd = __ldg(reinterpret_cast<const int4*>(np + 3));
+    const bool oa = overlap6(r.box, n0.x, n0.y, n0.z, n0.w, n1.x, n1.y);
+    const bool ob = overlap6(r.box, n1.z, n1.w, n2.x, n2.y, n2.z, n2.w);
+    const int ca = nd.x, cb = nd.y;
+    const bool la = ca >= n_int, lb = cb >= n_int;
+    if (oa && la) {
+        test_leaf<MODE>(a.leaves, ca - n_int, r, h, mts);
+        ++t.count;
+    }
+    if (ob && lb) {
+        test_leaf<MODE>(a.leaves, cb - n_int, r, h, mts);
+        ++t.count;
+    }
+    const bool ta = oa && !la, tb = ob && !lb;
+    if (!ta && !tb) {
+        if (t.top == 0) return 1;
+        t.node = stack[--t.top];
+    } else {
+        t.node = ta ? ca : cb;
+        if (ta && tb) {
+            if (t.top >= cap) return (REF && t.top + 1 >= a.max_stack) ? 2 : 3;
+            stack[t.top++] = cb;
+        }
+    }
+    if (MODE == kBoolean) {
+        if (REF) {
+            if (t.count >= a.max_coll - 1) {
+                if (h.det) return 1;
+                t.count = 0;
+            }
+        } else if (h.det) {
+            return 1;
+        }
+    }
+    return 0;
+}
+
+// Persistent warps with dynamic ray fetch: a lane whose segment is finished
+// goes idle; once kRefill lanes of the warp are idle the warp claims that
+// many new segments with one atomicAdd on a global counter (contiguous ids ->
+// coalesced endpoint loads).  Keeps SIMD lanes busy although half of the
+// segments leave the tree at the root and the rest need 10-40 node visits.
+constexpr int kPersistThreads = 128;
+constexpr int kRefill = 8;
+
+template <int MODE, bool REF, int KSTACK, bool STATS>
+__global__ void __launch_bounds__(kPersistThreads) k_query_persistent(QueryArgs a) {
+    const unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int stack[KSTACK];
+    const int root = __ldg(&a.hdr->root);
+    const int cap = REF ? (a.max_stack - 1 < KSTACK ? a.max_stack - 1 : KSTACK) : KSTACK;
+    long long ray = -1;
+    Ray r;
+    Hit h;
+    Trav t;
+    bool exhausted = false;
+    unsigned long long visits = 0, mts = 0;
+    for (;;) {
+        const unsigned idle = __ballot_sync(kFull, ray < 0);
+        if (!exhausted && __popc(idle) >= kRefill) {
+            const int k = __popc(idle);
+            const int leader = __ffs(idle) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(&a.status->tile_counter, (unsigned long long)k);
+            base = __shfl_sync(kFull, base, leader);
+            if (base + k >= (unsigned long long)a.n_r) exhausted = true;
+            if (ray < 0) {
+                const long long mine = (long long)base + __popc(idle & lt);
+                if (mine < a.n_r) {
+                    ray = mine;
+                    load_ray(a.starts, a.ends, ray, r);
+                    h.det = 0;
+                    h.n_hits = 0;
+                    h.best_tri = -1;
+                    h.best_t = 0.0;
+                    t.node = root;
+                    t.top = 0;
+                    t.count = 0;
+                }
+            }
+        } else if (idle == kFull) {
+            break;
+        }
+        if (ray >= 0) {
+            const int st = trav_step<MODE, REF, KSTACK>(a, r, h, t, stack, cap, visits, mts);
+            if (st != 0) {
+                if (st == 1) write_dense<MODE>(a, ray, r, h);
+                else if (st == 2) atomicMax(&a.status->bad, ~(unsigned long long)(ray + a.ray_offset));
+                else atomicAdd(&a.status->internal, 1ull);
+                ray = -1;
+            }
+        }
+    }
+    if (STATS) flush_stats(a, visits, mts);
+}
+
 // Barycentric with fused ordered compaction (engine.py:206-215): each CTA
 // takes a dynamic tile id, traces its rays, block-scans the hit flags and
 // chains a decoupled look-back over the tile prefixes, then writes its hits at
@@ -281,8 +415,21 @@ static void go(const QueryArgs& a, bool compact, bool stats, cudaStream_t s) {
         }
         return;
     }
-    if (stats) k_query_dense<MODE, REF, KS, true><<<grid, kQueryThreads, 0, s>>>(a);
-    else k_query_dense<MODE, REF, KS, false><<<grid, kQueryThreads, 0, s>>>(a);
+    if (g_simple_query) {
+        if (stats) k_query_dense<MODE, REF, KS, true><<<grid, kQueryThreads, 0, s>>>(a);
+        else k_query_dense<MODE, REF, KS, false><<<grid, kQueryThreads, 0, s>>>(a);
+        return;
+    }
+    auto kern = stats ? k_query_persistent<MODE, REF, KS, true> : k_query_persistent<MODE, REF, KS, false>;
+    static int per_sm[2] = {0, 0};
+    int& occ = per_sm[stats ? 1 : 0];
+    if (!occ) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPersistThreads, 0);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long want = (a.n_r + kPersistThreads - 1) / kPersistThreads;
+    long long pg = (long long)sms * (occ > 0 ? occ : 1);
+    kern<<<(unsigned)(want < pg ? want : pg), kPersistThreads, 0, s>>>(a);
 }
 
 template <int MODE, bool REF>

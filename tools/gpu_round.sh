@@ -14,6 +14,8 @@ for w in $WHAT; do
     quick) timeout 600 python -m pytest tests -x -q -m gpu -p no:cacheprovider -k "not c2_full and not large_tree" > "$OUT/pytest_gpu.txt" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.txt";;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.txt" 2>&1; echo "smoke rc=$?" >> "$OUT/smoke.txt";;
     bench) timeout 600 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err";;
+    bench_simple) RS_SIMPLE_QUERY=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_simple.json" 2>> "$OUT/bench.err";;
+    benchq) timeout 600 python bench.py --no-cpu-baseline > "$OUT/bench.json" 2>> "$OUT/bench.err";;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
