@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(256) k_climb(const float* __restrict__ V,
     int left = i, right = i, node = n_int + i, height = 0;
     for (;;) {
         if (left == 0 && right == n - 1) {  // root reached (lbvh.py:210-214)
+            ta.parent[node] = -1;
             ta.child_l[n - 1] = node;
             if (node < n_int) ta.int_tri[node] = -2;
             hdr->root = node;
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(256) k_climb(const float* __restrict__ V,
             ta.range_r[parent] = right;
         }
         ta.height[node] = height;  // ref-indexed: internal 0..n-2, leaves n-1..2n-2
+        ta.parent[node] = parent;
         cuda::atomic_ref<int, cuda::thread_scope_device> vis(ta.visit[parent]);
         if (vis.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // first arriver stops
         left = __ldcg(ta.range_l + parent);
@@ -351,6 +353,64 @@ __global__ void __launch_bounds__(256) k_climb(const float* __restrict__ V,
     }
 }
 
+// -------------------------------------------------------------- collapse ---
+
+__device__ __forceinline__ RsSlot make_slot(float x0, float x1, float y0, float y1, float z0,
+                                            float z1, int ref) {
+    RsSlot t;
+    t.lo_x = x0; t.hi_x = x1; t.lo_y = y0; t.hi_y = y1; t.lo_z = z0; t.hi_z = z1;
+    t.ref = ref;
+    t.pad = 0;
+    return t;
+}
+
+__device__ __forceinline__ RsSlot empty_slot() {
+    return make_slot(INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY, kEmpty);
+}
+
+__global__ void __launch_bounds__(256) k_collapse(int n, TreeArrays ta, const RsNode* __restrict__ nodes,
+                                                  RsNode4* __restrict__ nodes4,
+                                                  const RsHeader* __restrict__ hdr) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_int = n - 1;
+    if (n == 1) {  // single leaf: a root node holding it
+        if (p == 0) {
+            const float* b = ta.leaf_bounds;
+            RsNode4 q;
+            q.s[0] = make_slot(b[0], b[1], b[2], b[3], b[4], b[5], 0);
+            q.s[1] = q.s[2] = q.s[3] = empty_slot();
+            nodes4[0] = q;
+        }
+        return;
+    }
+    if (p >= n_int) return;
+    int depth = 0;
+    for (int x = __ldg(ta.parent + p); x >= 0; x = __ldg(ta.parent + x)) ++depth;
+    if (depth & 1) return;  // absorbed into its parent's 4-wide node
+    const RsNode nd = nodes[p];
+    RsSlot out[4];
+    int k = 0;
+    const int ca = nd.d.x, cb = nd.d.y;
+    if (ca >= n_int) {
+        out[k++] = make_slot(nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.b.x, nd.b.y, ca);
+    } else {
+        const RsNode c = nodes[ca];
+        out[k++] = make_slot(c.a.x, c.a.y, c.a.z, c.a.w, c.b.x, c.b.y, c.d.x);
+        out[k++] = make_slot(c.b.z, c.b.w, c.c.x, c.c.y, c.c.z, c.c.w, c.d.y);
+    }
+    if (cb >= n_int) {
+        out[k++] = make_slot(nd.b.z, nd.b.w, nd.c.x, nd.c.y, nd.c.z, nd.c.w, cb);
+    } else {
+        const RsNode c = nodes[cb];
+        out[k++] = make_slot(c.a.x, c.a.y, c.a.z, c.a.w, c.b.x, c.b.y, c.d.x);
+        out[k++] = make_slot(c.b.z, c.b.w, c.c.x, c.c.y, c.c.z, c.c.w, c.d.y);
+    }
+    while (k < 4) out[k++] = empty_slot();
+    RsNode4* q = nodes4 + p;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q->s[j] = out[j];
+}
+
 // ------------------------------------------------------------ host glue ---
 
 static int grid_for(long long n, int block, int cap) {
@@ -369,6 +429,12 @@ void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
                  unsigned long long* keys, int* vals, cudaStream_t s) {
     count_launches(1);
     k_keys<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(cent, n, hdr, kind, keys, vals);
+}
+
+void launch_collapse(int n, const TreeArrays& ta, const RsNode* nodes, RsNode4* nodes4,
+                     const RsHeader* hdr, cudaStream_t s) {
+    count_launches(1);
+    k_collapse<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(n, ta, nodes, nodes4, hdr);
 }
 
 size_t sort_scratch_bytes(int n, int passes) {

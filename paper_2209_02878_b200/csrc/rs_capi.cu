@@ -26,6 +26,7 @@ struct rs_tree {
     RsHeader* hdr;
     RsNode* nodes;
     RsLeaf* leaves;
+    RsNode4* nodes4;  // fast trees only
     TreeArrays ta;
 };
 
@@ -87,7 +88,8 @@ size_t tree_bytes(int64_t n) {
     b += align256(sizeof(RsLeaf) * (size_t)n);
     b += 2 * align256(sizeof(float) * 6 * (size_t)n);
     b += 10 * align256(sizeof(int) * (size_t)n);
-    b += align256(sizeof(int) * 2 * (size_t)n);
+    b += 2 * align256(sizeof(int) * 2 * (size_t)n);
+    b += align256(sizeof(RsNode4) * (size_t)(n > 1 ? n - 1 : 1));
     return b;
 }
 
@@ -110,6 +112,8 @@ void carve_tree(rs_tree* t) {
     t->ta.leaf_range_r = c.take<int>(n);
     t->ta.sorted_ids = c.take<int>(n);
     t->ta.height = c.take<int>(2 * n);
+    t->ta.parent = c.take<int>(2 * n);
+    t->nodes4 = c.take<RsNode4>(n > 1 ? n - 1 : 1);
 }
 
 bool g_pool_configured = false;
@@ -186,6 +190,7 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
         launch_keys(cent, n, t->hdr, kind, keys, vals, s);
         launch_sort(keys, vals, keys2, vals2, n, passes, sort_scratch, s);
         launch_climb(V, T, n, keys, vals, t->ta, t->nodes, t->leaves, t->hdr, s);
+        if (kind == kTreeFast) launch_collapse(n, t->ta, t->nodes, t->nodes4, t->hdr, s);
         CK(cudaFreeAsync(scratch, s));
     }
     CK(cudaGetLastError());
@@ -209,6 +214,7 @@ QueryArgs make_args(const rs_tree* t, const float* s, const float* e, int64_t n_
                     int max_stack, RsStatus* st) {
     QueryArgs a{};
     a.nodes = t->nodes;
+    a.nodes4 = t->kind == kTreeFast ? t->nodes4 : nullptr;
     a.leaves = t->leaves;
     a.hdr = t->hdr;
     a.n_int = (int)(t->n - 1);

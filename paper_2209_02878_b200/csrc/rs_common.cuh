@@ -33,6 +33,17 @@ struct __align__(16) RsNode {
     int4 d;    // lref rref - -
 };
 
+// 4-wide node: one 32-B slot per child, read by the 4 lanes of a segment's
+// lane group with one 256-bit load each (one 128-B line per node visit).
+struct __align__(32) RsSlot {
+    float lo_x, hi_x, lo_y, hi_y, lo_z, hi_z;  // exact f32 child AABB
+    int ref;                                   // child ref (-1 = empty slot)
+    int pad;
+};
+struct __align__(128) RsNode4 {
+    RsSlot s[4];
+};
+
 struct __align__(16) RsLeaf {
     float4 p0;  // a.x a.y a.z b.x
     float4 p1;  // b.y b.z c.x c.y

@@ -25,6 +25,7 @@ struct TreeArrays {
     int* leaf_range_r;
     int* sorted_ids;
     int* height;         // (2n,) subtree height by node ref
+    int* parent;         // (2n,) parent internal node by node ref (root: -1)
 };
 
 void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hdr,
@@ -38,9 +39,17 @@ void launch_climb(const float* V, const int* T, int n, const unsigned long long*
                   const int* ids, const TreeArrays& ta, RsNode* nodes, RsLeaf* leaves,
                   RsHeader* hdr, cudaStream_t s);
 
+// Collapse the binary LBVH into the 4-wide BVH the fast traversal reads:
+// internal nodes at even depth are kept, each takes its grandchildren (or a
+// leaf child itself) as its <= 4 children.  Node4 slots are indexed by the
+// binary node id (sparse), so no allocation pass is needed.
+void launch_collapse(int n, const TreeArrays& ta, const RsNode* nodes, RsNode4* nodes4,
+                     const RsHeader* hdr, cudaStream_t s);
+
 // Query-side launch parameters.
 struct QueryArgs {
     const RsNode* nodes;
+    const RsNode4* nodes4;  // fast trees: 4-wide nodes (null for reference trees)
     const RsLeaf* leaves;
     const RsHeader* hdr;  // root ref is read on device (no host sync after a build)
     int n_int;

@@ -25,11 +25,15 @@ namespace rs {
 
 constexpr int kQueryThreads = 128;
 
-// RS_SIMPLE_QUERY=1 selects the one-segment-per-thread kernel (A/B tuning).
-static const bool g_simple_query = [] {
-    const char* e = getenv("RS_SIMPLE_QUERY");
+// A/B tuning switches: RS_BINARY_FAST=1 traverses fast trees with the
+// binary kernels; RS_SIMPLE_QUERY=1 picks one-segment-per-thread over the
+// persistent binary kernel.
+static bool env_flag(const char* k) {
+    const char* e = getenv(k);
     return e && e[0] == '1';
-}();
+}
+static const bool g_simple_query = env_flag("RS_SIMPLE_QUERY");
+static const bool g_binary_fast = env_flag("RS_BINARY_FAST");
 
 struct Ray {
     float box[6];
@@ -327,6 +331,125 @@ __global__ void __launch_bounds__(kPersistThreads) k_query_persistent(QueryArgs 
     if (STATS) flush_stats(a, visits, mts);
 }
 
+// ------------------------------------------------ 4-lane quad traversal ---
+//
+// Fast trees are traversed as a 4-wide BVH by groups of 4 lanes: one segment
+// per group, one child slot per lane.  A node visit is one 256-bit load per
+// lane, i.e. the group reads exactly one 128-B line, so the 8 groups of a warp
+// touch 8 lines per step instead of the 32+ scattered lines of a
+// thread-per-segment binary traversal (which is L1-wavefront bound).  Leaf
+// children are exact-tested by the lane that found them, internal hits are
+// pushed in parallel onto the group's shared-memory stack.
+constexpr int kQuadThreads = 128;
+constexpr int kQuadGroups = kQuadThreads / 4;
+constexpr int kQuadStack = 96;  // 4-wide depth <= 31 (binary height <= 61) x 3 pushes
+constexpr int kQuadRefill = 2;  // refill when >= 2 groups of the warp are idle
+
+__device__ __forceinline__ void ld_slot(const RsSlot* p, float f[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(f[0]), "=f"(f[1]), "=f"(f[2]), "=f"(f[3]), "=f"(f[4]), "=f"(f[5]),
+                   "=f"(f[6]), "=f"(f[7])
+                 : "l"(p));
+}
+
+template <int MODE, bool STATS>
+__global__ void __launch_bounds__(kQuadThreads) k_query_quad(QueryArgs a) {
+    __shared__ int stk[kQuadStack][kQuadGroups];
+    const unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int q = lane & 3;
+    const int gshift = lane & ~3;
+    const int gid = threadIdx.x >> 2;
+    const int n_int = a.n_int;
+    const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    long long ray = -1;
+    Ray r;
+    int node = 0, top = 0;
+    Hit h;
+    h.det = 0; h.n_hits = 0; h.best_tri = -1; h.best_t = 0.0;
+    bool exhausted = false;
+    unsigned long long visits = 0, mts = 0;
+    for (;;) {
+        const unsigned idle = __ballot_sync(kFull, ray < 0);
+        const int idle_groups = __popc(idle) >> 2;
+        if (!exhausted && idle_groups >= kQuadRefill) {
+            const int leader = __ffs(idle) - 1;
+            unsigned long long base = 0;
+            if (lane == leader)
+                base = atomicAdd(&a.status->tile_counter, (unsigned long long)idle_groups);
+            base = __shfl_sync(kFull, base, leader);
+            if (base + idle_groups >= (unsigned long long)a.n_r) exhausted = true;
+            if (ray < 0) {
+                const long long mine =
+                    (long long)base + (__popc(idle & ((1u << gshift) - 1u)) >> 2);
+                if (mine < a.n_r) {
+                    ray = mine;
+                    load_ray(a.starts, a.ends, ray, r);
+                    node = root;
+                    top = 0;
+                    h.det = 0; h.n_hits = 0; h.best_tri = -1; h.best_t = 0.0;
+                }
+            }
+        } else if (idle == kFull) {
+            break;
+        }
+        const bool active = ray >= 0;
+        bool ihit = false;
+        int ref = kEmpty;
+        if (active) {
+            float f[8];
+            ld_slot(&a.nodes4[node].s[q], f);
+            ref = __float_as_int(f[6]);
+            const bool hit = ref >= 0 && overlap6(r.box, f[0], f[1], f[2], f[3], f[4], f[5]);
+            if (STATS && q == 0) ++visits;
+            if (hit && ref >= n_int) test_leaf<MODE>(a.leaves, ref - n_int, r, h, mts);
+            ihit = hit && ref < n_int;
+        }
+        const unsigned gmask = (__ballot_sync(kFull, ihit) >> gshift) & 0xFu;
+        bool finish = false;
+        if (MODE == kBoolean) finish = ((__ballot_sync(kFull, h.det != 0) >> gshift) & 0xFu) != 0;
+        bool ovf = false;
+        if (active && !finish) {
+            const int k = __popc(gmask);
+            if (top + k > kQuadStack) {
+                ovf = finish = true;
+            } else {
+                if (ihit) stk[top + __popc(gmask & ((1u << q) - 1u))][gid] = ref;
+                top += k;
+                if (top == 0) finish = true;
+            }
+        }
+        __syncwarp();
+        if (active && !finish) node = stk[--top][gid];
+        if (__any_sync(kFull, active && finish)) {
+            // reduce the group's per-lane partial results (lanes of other
+            // groups shuffle within their own group; results are ignored)
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                const int od = __shfl_xor_sync(kFull, h.det, o);
+                const int on = __shfl_xor_sync(kFull, h.n_hits, o);
+                const int ot = __shfl_xor_sync(kFull, h.best_tri, o);
+                const double obt = __shfl_xor_sync(kFull, h.best_t, o);
+                h.det |= od;
+                h.n_hits += on;
+                if (ot >= 0 && (h.best_tri < 0 || obt < h.best_t || (obt == h.best_t && ot < h.best_tri))) {
+                    h.best_t = obt;
+                    h.best_tri = ot;
+                }
+            }
+            if (active && finish) {
+                if (q == 0) {
+                    if (ovf) atomicAdd(&a.status->internal, 1ull);
+                    else write_dense<MODE>(a, ray, r, h);
+                }
+                ray = -1;
+            }
+        }
+        __syncwarp();
+    }
+    if (STATS) flush_stats(a, visits, mts);
+}
+
 // Barycentric with fused ordered compaction (engine.py:206-215): each CTA
 // takes a dynamic tile id, traces its rays, block-scans the hit flags and
 // chains a decoupled look-back over the tile prefixes, then writes its hits at
@@ -413,6 +536,19 @@ static void go(const QueryArgs& a, bool compact, bool stats, cudaStream_t s) {
             if (stats) k_query_compact<REF, KS, true><<<grid, kQueryThreads, 0, s>>>(a);
             else k_query_compact<REF, KS, false><<<grid, kQueryThreads, 0, s>>>(a);
         }
+        return;
+    }
+    if (!REF && a.nodes4 && !g_binary_fast) {
+        auto kq = stats ? k_query_quad<MODE, true> : k_query_quad<MODE, false>;
+        static int occ_q[2] = {0, 0};
+        int& oq = occ_q[stats ? 1 : 0];
+        if (!oq) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oq, kq, kQuadThreads, 0);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        long long want = (a.n_r + kQuadGroups - 1) / kQuadGroups;
+        long long pg = (long long)sms * (oq > 0 ? oq : 1);
+        kq<<<(unsigned)(want < pg ? want : pg), kQuadThreads, 0, s>>>(a);
         return;
     }
     if (g_simple_query) {

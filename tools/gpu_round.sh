@@ -15,6 +15,7 @@ for w in $WHAT; do
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.txt" 2>&1; echo "smoke rc=$?" >> "$OUT/smoke.txt";;
     bench) timeout 600 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?" >> "$OUT/bench.err";;
     bench_simple) RS_SIMPLE_QUERY=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_simple.json" 2>> "$OUT/bench.err";;
+    bench_binary) RS_BINARY_FAST=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_binary.json" 2>> "$OUT/bench.err";;
     benchq) timeout 600 python bench.py --no-cpu-baseline > "$OUT/bench.json" 2>> "$OUT/bench.err";;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
