@@ -424,20 +424,22 @@ __global__ void __launch_bounds__(kQuadThreads) k_query_quad(QueryArgs a) {
         if (__any_sync(kFull, active && finish)) {
             // reduce the group's per-lane partial results (lanes of other
             // groups shuffle within their own group; results are ignored)
+            Hit g = h;
 #pragma unroll
             for (int o = 1; o <= 2; o <<= 1) {
-                const int od = __shfl_xor_sync(kFull, h.det, o);
-                const int on = __shfl_xor_sync(kFull, h.n_hits, o);
-                const int ot = __shfl_xor_sync(kFull, h.best_tri, o);
-                const double obt = __shfl_xor_sync(kFull, h.best_t, o);
-                h.det |= od;
-                h.n_hits += on;
-                if (ot >= 0 && (h.best_tri < 0 || obt < h.best_t || (obt == h.best_t && ot < h.best_tri))) {
-                    h.best_t = obt;
-                    h.best_tri = ot;
+                const int od = __shfl_xor_sync(kFull, g.det, o);
+                const int on = __shfl_xor_sync(kFull, g.n_hits, o);
+                const int ot = __shfl_xor_sync(kFull, g.best_tri, o);
+                const double obt = __shfl_xor_sync(kFull, g.best_t, o);
+                g.det |= od;
+                g.n_hits += on;
+                if (ot >= 0 && (g.best_tri < 0 || obt < g.best_t || (obt == g.best_t && ot < g.best_tri))) {
+                    g.best_t = obt;
+                    g.best_tri = ot;
                 }
             }
             if (active && finish) {
+                h = g;
                 if (q == 0) {
                     if (ovf) atomicAdd(&a.status->internal, 1ull);
                     else write_dense<MODE>(a, ray, r, h);
