@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -33,6 +34,12 @@ struct rs_tree {
 namespace {
 
 thread_local std::string g_err;
+
+// RS_BINARY_FAST=1: traverse fast trees with the binary kernels (A/B tuning).
+const bool g_binary_fast = [] {
+    const char* e = getenv("RS_BINARY_FAST");
+    return e && e[0] == '1';
+}();
 
 // Phase timing (engine.py's timings dict, measured on device): when enabled,
 // events bracket the build and the query kernel on the caller's stream.
@@ -325,6 +332,101 @@ int rs_free(rs_tree* t, void* stream) {
     return RS_OK;
 }
 
+// Fast-tree query: 4-lane traversal -> collision buffer -> exact tests (->
+// barycentric compaction).  Outputs: boolean/count -> flags (dense); bary ->
+// compact rows (c_*) or dense rows (det/tri/dist/pts).  The collision buffer
+// starts at 2 x n_r entries; if the traversal claimed more, everything is
+// re-launched once with a buffer of exactly the claimed size.
+struct FastOut {
+    int32_t* flags = nullptr;
+    int32_t *det = nullptr, *tri = nullptr;
+    float *dist = nullptr, *pts = nullptr;
+    int32_t *c_ray = nullptr, *c_tri = nullptr;
+    float *c_dist = nullptr, *c_pt = nullptr;
+    long long ray_offset = 0;
+};
+
+struct FastScratch {
+    char* blk = nullptr;
+    RsStatus* st = nullptr;
+    int2* cand = nullptr;
+    int* chunk_fill = nullptr;
+    unsigned long long *best_t = nullptr, *cand_t = nullptr, *tiles = nullptr, *tile_ctr = nullptr;
+    int* best_tri = nullptr;
+    long long cap = 0;
+};
+
+static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cudaStream_t s) {
+    cap = ((cap + kCandChunk - 1) / kCandChunk) * kCandChunk;
+    const bool bary = mode == kBarycentric;
+    const size_t b_st = align256(sizeof(RsStatus));
+    const size_t b_cand = align256(8ull * cap);
+    const size_t b_fill = align256(4ull * (cap / kCandChunk + 1));
+    const size_t b_bt = bary ? align256(8ull * n_r) : 0;
+    const size_t b_btri = bary ? align256(4ull * n_r) : 0;
+    const size_t b_ct = bary ? align256(8ull * cap) : 0;
+    const size_t b_tiles = bary ? align256(bary_compact_scratch(n_r)) : 0;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk),
+                       b_st + b_cand + b_fill + b_bt + b_btri + b_ct + b_tiles + 256, s));
+    Carver c{f.blk};
+    f.st = c.take<RsStatus>(1);
+    f.cand = c.take<int2>(cap);
+    f.chunk_fill = c.take<int>(cap / kCandChunk + 1);
+    if (bary) {
+        f.best_t = c.take<unsigned long long>(n_r);
+        f.best_tri = c.take<int>(n_r);
+        f.cand_t = c.take<unsigned long long>(cap);
+        f.tiles = c.take<unsigned long long>(bary_compact_scratch(n_r) / 8);
+        f.tile_ctr = f.tiles + (bary_compact_scratch(n_r) / 8 - 1);
+    }
+    f.cap = cap;
+    return RS_OK;
+}
+
+static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
+                       const FastOut& o, FastScratch& f, bool stats, cudaStream_t s) {
+    const bool bary = mode == kBarycentric;
+    CK(cudaMemsetAsync(f.st, 0, sizeof(RsStatus), s));
+    if (!bary) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
+    if (bary) {
+        CK(cudaMemsetAsync(f.best_t, 0xFF, 8ull * n_r, s));
+        CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
+        CK(cudaMemsetAsync(f.tiles, 0, bary_compact_scratch(n_r), s));
+    }
+    TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill, f.st};
+    ev_record(1, s);
+    launch_trav(ta, stats, s);
+    ExactArgs ea{f.cand, &f.st->cand_count, f.cap, f.chunk_fill, d_s, d_e, t->leaves,
+                 o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
+    launch_exact(ea, mode, stats, s);
+    if (bary) {
+        CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
+                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset};
+        if (o.c_ray) launch_bary_compact(ca, s);
+        else launch_bary_dense(ca, o.det, o.tri, o.dist, o.pts, s);
+    }
+    CK(cudaGetLastError());
+    ev_record(2, s);
+    return RS_OK;
+}
+
+static int fast_query(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
+                      const FastOut& o, bool stats, RsStatus* h, cudaStream_t s) {
+    FastScratch f;
+    long long cap = 2ll * n_r + 4096;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        int rc = fast_alloc(f, n_r, mode, cap, s);
+        if (rc) return rc;
+        rc = fast_launch(t, d_s, d_e, n_r, mode, o, f, stats, s);
+        if (!rc) rc = read_status(f.st, s, h);
+        CK(cudaFreeAsync(f.blk, s));
+        if (rc) return rc;
+        if ((long long)h->cand_count <= f.cap) return RS_OK;
+        cap = (long long)h->cand_count;  // collision buffer overflow: re-launch once, sized
+    }
+    return fail(RS_INTERNAL, "collision buffer overflow after re-launch");
+}
+
 static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
                       int max_coll, int max_stack, int ref, int32_t* det, int32_t* cnt,
                       int32_t* tri, float* dist, float* pts, int32_t* c_ray, float* c_dist,
@@ -335,6 +437,19 @@ static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int6
     if (rc) return rc;
     if (n_r < 0) return fail(RS_INVALID_ARG, "negative segment count");
     if (n_r > 2147483647ll) return fail(RS_INVALID_ARG, "segment count exceeds int32 indexing");
+    if (t->kind == kTreeFast && n_r > 0 && !g_binary_fast) {
+        FastOut o;
+        o.flags = mode == kCount ? cnt : det;
+        o.det = det; o.tri = tri; o.dist = dist; o.pts = pts;
+        o.c_ray = c_ray; o.c_dist = c_dist; o.c_tri = c_tri; o.c_pt = c_pt;
+        RsStatus h{};
+        rc = fast_query(t, d_s, d_e, n_r, mode, o, stats, &h, s);
+        if (rc) return rc;
+        if (n_hits) *n_hits = (int64_t)h.hits;
+        if (visits) *visits = (int64_t)h.visits;
+        if (mts) *mts = (int64_t)h.mts;
+        return status_code(h, bad);
+    }
     const bool compact = c_ray != nullptr;
     const size_t cs = compact ? compact_scratch_bytes(n_r) : 0;
     char* blk = nullptr;
@@ -532,6 +647,13 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
         return rc;
     }
     const int ref = tree_kind == kTreeReference;
+    const bool fast = tree_kind == kTreeFast && !g_binary_fast;
+    FastScratch fs[2];
+    if (fast)
+        for (int b = 0; b < 2; ++b) {
+            rc = fast_alloc(fs[b], chunk_rays, mode, 2 * chunk_rays + 4096, s);
+            if (rc) return rc;
+        }
     // The copy stream must see the memset/mesh copies ordered before chunk 0.
     CK(cudaEventRecord(g_pipe.ev_q[1], s));
     CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[1], 0));
@@ -546,6 +668,25 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
         CK(cudaEventRecord(g_pipe.ev_in[b], cp));
         CK(cudaStreamWaitEvent(s, g_pipe.ev_in[b], 0));
         if (k >= 2 && !bary) CK(cudaStreamWaitEvent(s, g_pipe.ev_out[b], 0));
+        if (fast) {
+            fs[b].st = st + k;
+            FastOut o;
+            o.ray_offset = lo;
+            if (bary) {
+                o.c_ray = dray + lo; o.c_dist = ddist + lo; o.c_tri = dtri + lo; o.c_pt = dpt + 3 * lo;
+            } else {
+                o.flags = dflag[b];
+            }
+            rc = fast_launch(t, din[b][0], din[b][1], cnt, mode, o, fs[b], false, s);
+            if (rc) return rc;
+            CK(cudaEventRecord(g_pipe.ev_q[b], s));
+            if (!bary) {
+                CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));
+                CK(cudaMemcpyAsync(h_flags + lo, dflag[b], 4ull * cnt, cudaMemcpyDeviceToHost, cp));
+                CK(cudaEventRecord(g_pipe.ev_out[b], cp));
+            }
+            continue;
+        }
         QueryArgs a = make_args(t, din[b][0], din[b][1], cnt, max_coll, max_stack, st + k);
         a.ray_offset = lo;
         if (bary) {
@@ -578,6 +719,32 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[(nchunks - 1) & 1], 0));
     CK(cudaMemcpyAsync(hst, st, sizeof(RsStatus) * nchunks, cudaMemcpyDeviceToHost, cp));
     CK(cudaStreamSynchronize(cp));
+    if (fast) {
+        for (int b = 0; b < 2; ++b) CK(cudaFreeAsync(fs[b].blk, s));
+        // collision-buffer overflow in a chunk: redo that chunk with a buffer
+        // sized to what its traversal claimed
+        for (int64_t k = 0; k < nchunks; ++k) {
+            if ((long long)hst[k].cand_count <= fs[0].cap) continue;
+            const int64_t lo = k * chunk_rays;
+            const int64_t cnt = (lo + chunk_rays <= n_r) ? chunk_rays : n_r - lo;
+            CK(cudaStreamSynchronize(cp));
+            CK(cudaMemcpyAsync(din[0][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(din[0][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, s));
+            FastOut o;
+            o.ray_offset = lo;
+            if (bary) {
+                o.c_ray = dray + lo; o.c_dist = ddist + lo; o.c_tri = dtri + lo; o.c_pt = dpt + 3 * lo;
+            } else {
+                o.flags = dflag[0];
+            }
+            rc = fast_query(t, din[0][0], din[0][1], cnt, mode, o, false, hst + k, s);
+            if (rc) return rc;
+            if (!bary) {
+                CK(cudaMemcpyAsync(h_flags + lo, dflag[0], 4ull * cnt, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+            }
+        }
+    }
     unsigned long long badv = 0, internal = 0;
     for (int64_t k = 0; k < nchunks; ++k) {
         if (hst[k].bad && (!badv || ~hst[k].bad < ~badv)) badv = hst[k].bad;

@@ -67,7 +67,11 @@ struct RsStatus {
     unsigned long long tile_counter;
     unsigned long long visits;    // optional stats
     unsigned long long mts;
+    unsigned long long cand_count;  // collision-buffer entries claimed (may exceed capacity)
+    unsigned long long pad;
 };
+
+constexpr int kCandChunk = 128;  // collision-buffer entries claimed per warp atomic
 
 // ---- ordered encodings so atomics on u64 give min/max of doubles ----------
 __device__ __forceinline__ unsigned long long ord_of(double d) {

@@ -83,6 +83,55 @@ int launch_query(const QueryArgs& a, int mode, bool ref_semantics, bool compact,
                  bool stats, cudaStream_t s);
 size_t compact_scratch_bytes(long long n_r);
 
+// Fast-tree path (rs_trav.cu): traversal -> collision buffer -> exact tests.
+struct TravArgs {
+    const RsNode4* nodes4;
+    const RsHeader* hdr;
+    int n_int;
+    const float* starts;
+    const float* ends;
+    long long n_r;
+    int2* cand;            // collision buffer (segment, leaf)
+    long long cand_cap;    // multiple of kCandChunk
+    int* chunk_fill;       // entries used per chunk
+    RsStatus* status;
+};
+struct ExactArgs {
+    const int2* cand;
+    const unsigned long long* cand_count;
+    long long cand_cap;
+    const int* chunk_fill;
+    const float* starts;
+    const float* ends;
+    const RsLeaf* leaves;
+    int* flags;                  // boolean: crossing (pre-zeroed); count: counts (pre-zeroed)
+    unsigned long long* best_t;  // barycentric: min t key per segment (pre-set to ~0)
+    int* best_tri;               // barycentric: winning triangle (pre-set to -1)
+    unsigned long long* cand_t;  // barycentric: t key per candidate
+    unsigned long long* mts;
+};
+struct CompactArgs {
+    long long n_r;
+    const unsigned long long* best_t;
+    const int* best_tri;
+    const float* starts;
+    const float* ends;
+    int* ray;
+    float* dist;
+    int* tri;
+    float* point;
+    unsigned long long* tile_status;
+    unsigned long long* tile_counter;
+    unsigned long long* n_hits;
+    long long ray_offset;
+};
+void launch_trav(const TravArgs& a, bool stats, cudaStream_t s);
+void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);
+size_t bary_compact_scratch(long long n_r);
+void launch_bary_compact(const CompactArgs& a, cudaStream_t s);
+void launch_bary_dense(const CompactArgs& a, int* detected, int* tri, float* dist, float* points,
+                       cudaStream_t s);
+
 struct BaselineArgs {
     const float* V;
     const int* T;
