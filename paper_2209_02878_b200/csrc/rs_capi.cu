@@ -354,6 +354,7 @@ struct FastScratch {
     unsigned long long *best_t = nullptr, *cand_t = nullptr, *tiles = nullptr, *tile_ctr = nullptr;
     int* best_tri = nullptr;
     long long cap = 0;
+    size_t tiles_bytes = 0;
 };
 
 static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cudaStream_t s) {
@@ -378,6 +379,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         f.cand_t = c.take<unsigned long long>(cap);
         f.tiles = c.take<unsigned long long>(bary_compact_scratch(n_r) / 8);
         f.tile_ctr = f.tiles + (bary_compact_scratch(n_r) / 8 - 1);
+        f.tiles_bytes = bary_compact_scratch(n_r);
     }
     f.cap = cap;
     return RS_OK;
@@ -391,7 +393,7 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
     if (bary) {
         CK(cudaMemsetAsync(f.best_t, 0xFF, 8ull * n_r, s));
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
-        CK(cudaMemsetAsync(f.tiles, 0, bary_compact_scratch(n_r), s));
+        CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
     }
     TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill, f.st};
     ev_record(1, s);

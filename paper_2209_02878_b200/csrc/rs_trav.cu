@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(256) k_tiebreak(ExactArgs a) {
         const unsigned long long k = a.cand_t[i];
         if (k == ~0ull) continue;
         const int2 c = a.cand[i];
-        if (k == a.best_t[c.x]) atomicMin(a.best_tri + c.x, __float_as_int(__ldg(&a.leaves[c.y].p2.y)));
+        if (k == a.best_t[c.x])  // unsigned min: the 0xFFFFFFFF (-1) preset is the largest key
+            atomicMin(reinterpret_cast<unsigned*>(a.best_tri) + c.x,
+                      (unsigned)__float_as_int(__ldg(&a.leaves[c.y].p2.y)));
     }
 }
 
