@@ -43,7 +43,9 @@ __device__ __forceinline__ void ld_slot8(const RsSlot* p, float f[8]) {
 template <bool STATS>
 __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
     __shared__ int stk[kTravStack][kTravGroups];
+    __shared__ float4 qs[kTravThreads / 32][32][2];  // per-warp queue: box + segment id
     const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int q = lane & 3;
     const int gshift = lane & ~3;
     const int gid = threadIdx.x >> 2;
@@ -52,10 +54,7 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
     const int n_int = a.n_int;
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
 
-    // per-warp segment queue: lane j holds queue slot j
-    int qray = -1;
-    float qb[6];
-    int qhead = 32, qcount = 32;  // empty
+    int qhead = 0, qcount = 0;  // live segments queued in qs[warp][qhead, qcount)
     bool exhausted = false;
     // per-group traversal state (replicated in the group's 4 lanes)
     int ray = -1, node = 0, top = 0;
@@ -68,45 +67,60 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
     for (;;) {
         const unsigned idle = __ballot_sync(kFull, ray < 0) & kGroupBits;
         if (idle) {
-            if (qhead == qcount && !exhausted) {  // refill the queue
+            // refill: claim 32 segments, cull those that miss every child of
+            // the root (their result is the pre-zeroed default), queue the rest
+            while (qhead == qcount && !exhausted) {
                 unsigned long long base = 0;
                 if (lane == 0) base = atomicAdd(&a.status->tile_counter, 32ull);
                 base = __shfl_sync(kFull, base, 0);
-                const long long rid = (long long)base + lane;
-                qcount = (long long)base + 32 <= a.n_r ? 32 : (int)(a.n_r > (long long)base ? a.n_r - (long long)base : 0);
                 exhausted = (long long)base + 32 >= a.n_r;
-                qhead = 0;
-                qray = -1;
-                if (lane < qcount) {
-                    qray = (int)rid;
-                    const float* s = a.starts + 3 * rid;
-                    const float* e = a.ends + 3 * rid;
-                    const float s0 = __ldg(s), s1 = __ldg(s + 1), s2 = __ldg(s + 2);
-                    const float e0 = __ldg(e), e1 = __ldg(e + 1), e2 = __ldg(e + 2);
-                    qb[0] = fminf(s0, e0); qb[1] = fmaxf(s0, e0);  // engine.py:115-122
-                    qb[2] = fminf(s1, e1); qb[3] = fmaxf(s1, e1);
-                    qb[4] = fminf(s2, e2); qb[5] = fmaxf(s2, e2);
+                const long long rid = (long long)base + lane;
+                bool live = false;
+                float bx[6];
+                if (rid < a.n_r) {
+                    const float* sp = a.starts + 3 * rid;
+                    const float* ep = a.ends + 3 * rid;
+                    const float s0 = __ldg(sp), s1 = __ldg(sp + 1), s2 = __ldg(sp + 2);
+                    const float e0 = __ldg(ep), e1 = __ldg(ep + 1), e2 = __ldg(ep + 2);
+                    bx[0] = fminf(s0, e0); bx[1] = fmaxf(s0, e0);  // engine.py:115-122
+                    bx[2] = fminf(s1, e1); bx[3] = fmaxf(s1, e1);
+                    bx[4] = fminf(s2, e2); bx[5] = fmaxf(s2, e2);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float f[8];
+                        ld_slot8(&a.nodes4[root].s[j], f);
+                        live |= __float_as_int(f[6]) >= 0 && bx[0] <= f[1] && bx[1] >= f[0] &&
+                                bx[2] <= f[3] && bx[3] >= f[2] && bx[4] <= f[5] && bx[5] >= f[4];
+                    }
                 }
+                const unsigned lm = __ballot_sync(kFull, live);
+                if (live) {
+                    const int at = __popc(lm & lt);
+                    qs[warp][at][0] = make_float4(bx[0], bx[1], bx[2], bx[3]);
+                    qs[warp][at][1] = make_float4(bx[4], bx[5], __int_as_float((int)rid), 0.f);
+                }
+                qhead = 0;
+                qcount = __popc(lm);
+                __syncwarp();
             }
-            const int nidle = __popc(idle);
             const int avail = qcount - qhead;
-            const int take = nidle < avail ? nidle : avail;
-            const int rank = __popc(idle & ((1u << gshift) - 1u));
-            const bool mine = ray < 0 && rank < take;
-            const int src = mine ? qhead + rank : lane;
-            const int r_ = __shfl_sync(kFull, qray, src);
-            float nb[6];
-#pragma unroll
-            for (int j = 0; j < 6; ++j) nb[j] = __shfl_sync(kFull, qb[j], src);
-            if (mine) {
-                ray = r_;
-#pragma unroll
-                for (int j = 0; j < 6; ++j) b[j] = nb[j];
-                node = root;
-                top = 0;
+            if (avail > 0) {
+                const int nidle = __popc(idle);
+                const int take = nidle < avail ? nidle : avail;
+                const int rank = __popc(idle & ((1u << gshift) - 1u));
+                if (ray < 0 && rank < take) {
+                    const float4 u = qs[warp][qhead + rank][0];
+                    const float4 v = qs[warp][qhead + rank][1];
+                    b[0] = u.x; b[1] = u.y; b[2] = u.z; b[3] = u.w; b[4] = v.x; b[5] = v.y;
+                    ray = __float_as_int(v.z);
+                    node = root;
+                    top = 0;
+                }
+                qhead += take;
+            } else if (exhausted && idle == kGroupBits) {
+                break;
             }
-            qhead += take;
-            if (exhausted && qhead == qcount && __all_sync(kFull, ray < 0)) break;
+            __syncwarp();
         }
         const bool active = ray >= 0;
         bool hit = false;
@@ -142,23 +156,19 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
         }
         // ---- push internal hits, pop the next node ----
         const unsigned gm = (__ballot_sync(kFull, ihit) >> gshift) & 0xFu;
-        const int k = __popc(gm);
-        bool done = false;
         if (active) {
-            if (top + k > kTravStack) {
-                done = true;  // cannot happen for fast trees (height <= 61)
+            const int k = __popc(gm);
+            if (top + k > kTravStack) {  // cannot happen for fast trees (height <= 61)
                 if (q == 0) atomicAdd(&a.status->internal, 1ull);
+                ray = -1;
             } else {
                 if (ihit) stk[top + __popc(gm & ((1u << q) - 1u))][gid] = ref;
                 top += k;
-                done = top == 0;
+                if (top == 0) ray = -1;
             }
         }
         __syncwarp();
-        if (active) {
-            if (done) ray = -1;
-            else node = stk[--top][gid];
-        }
+        if (ray >= 0) node = stk[--top][gid];
     }
     if (lane == 0 && cbase >= 0 && cbase < a.cand_cap) a.chunk_fill[cbase / kCandChunk] = cfill;
     if (STATS) {
