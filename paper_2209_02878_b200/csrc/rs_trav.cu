@@ -5,8 +5,8 @@
 //   k_trav_quad   one segment per 4-lane group, one child slot per lane: a
 //                 node visit is one 256-bit load per lane (the group reads one
 //                 128-B line).  Leaf children whose exact f32 AABB overlaps the
-//                 segment AABB are appended to the collision buffer through
-//                 per-warp 128-entry chunks (one global atomic per chunk);
+//                 segment AABB are appended to the collision buffer (staged
+//                 per warp in shared memory, flushed 32 per atomic);
 //                 internal hits are pushed in parallel onto the group's
 //                 shared-memory stack.  Segments are fed through a per-warp
 //                 queue of 32 prefetched ids/boxes (one atomic per 32).
@@ -18,9 +18,11 @@
 //   k_bary_compact ordered compaction of barycentric rows (decoupled
 //                 look-back), point/distance computed from the winning t.
 //
-// Capacity: the buffer is pre-sized (2 x segments by default); the append
-// counter keeps counting past the end, so the host sees the true size and
-// re-launches with a buffer that fits (rs_capi.cu).
+// Candidates are staged per warp in shared memory and written 32 at a time
+// behind one atomicAdd, so the buffer is dense (no gaps).  Capacity: the
+// buffer is pre-sized (2 x segments by default); the append counter keeps
+// counting past the end, so the host sees the true size and re-launches with
+// a buffer that fits (rs_capi.cu).
 #include <cuda/atomic>
 
 #include "rs_common.cuh"
@@ -34,7 +36,7 @@ constexpr int kTravStack = 96;  // 4-wide depth <= 31 x 3 pending pushes
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ void ld_slot8(const RsSlot* p, float f[8]) {
-    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(f[0]), "=f"(f[1]), "=f"(f[2]), "=f"(f[3]), "=f"(f[4]), "=f"(f[5]),
                    "=f"(f[6]), "=f"(f[7])
                  : "l"(p));
@@ -42,26 +44,29 @@ __device__ __forceinline__ void ld_slot8(const RsSlot* p, float f[8]) {
 
 template <bool STATS>
 __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
-    __shared__ int stk[kTravStack][kTravGroups];
+    __shared__ int stk[kTravStack + 4][kTravGroups];
     __shared__ float4 qs[kTravThreads / 32][32][2];  // per-warp queue: box + segment id
+    __shared__ int2 cs[kTravThreads / 32][64];       // per-warp candidate staging
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int q = lane & 3;
     const int gshift = lane & ~3;
-    const int gid = threadIdx.x >> 2;
     const unsigned lt = (1u << lane) - 1u;
+    const unsigned lt_in_group = (1u << q) - 1u;
     const unsigned kGroupBits = 0x11111111u;
     const int n_int = a.n_int;
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    int* const my_stk = &stk[0][threadIdx.x >> 2];  // this group's column, stride kTravGroups
+    int2* const my_cs = cs[warp];
+    const RsSlot* const slots = &a.nodes4[0].s[q];  // + 4 * node
 
     int qhead = 0, qcount = 0;  // live segments queued in qs[warp][qhead, qcount)
     bool exhausted = false;
+    int cn = 0;                 // staged candidates (warp-uniform)
     // per-group traversal state (replicated in the group's 4 lanes)
-    int ray = -1, node = 0, top = 0;
-    float b[6];
-    // per-warp candidate chunk
-    long long cbase = -1;
-    int cfill = kCandChunk;
+    int ray = -1, node = root, top = 0;
+    float b0 = INFINITY, b1 = -INFINITY, b2 = INFINITY, b3 = -INFINITY, b4 = INFINITY,
+          b5 = -INFINITY;  // empty box: overlaps nothing
     unsigned long long visits = 0;
 
     for (;;) {
@@ -104,73 +109,78 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
                 __syncwarp();
             }
             const int avail = qcount - qhead;
-            if (avail > 0) {
-                const int nidle = __popc(idle);
-                const int take = nidle < avail ? nidle : avail;
-                const int rank = __popc(idle & ((1u << gshift) - 1u));
-                if (ray < 0 && rank < take) {
-                    const float4 u = qs[warp][qhead + rank][0];
-                    const float4 v = qs[warp][qhead + rank][1];
-                    b[0] = u.x; b[1] = u.y; b[2] = u.z; b[3] = u.w; b[4] = v.x; b[5] = v.y;
-                    ray = __float_as_int(v.z);
-                    node = root;
-                    top = 0;
-                }
-                qhead += take;
-            } else if (exhausted && idle == kGroupBits) {
-                break;
+            if (avail <= 0 && exhausted && idle == kGroupBits) break;
+            const int nidle = __popc(idle);
+            const int take = nidle < avail ? nidle : avail;
+            const int rank = __popc(idle & ((1u << gshift) - 1u));
+            if (ray < 0 && rank < take) {
+                const float4 u = qs[warp][qhead + rank][0];
+                const float4 v = qs[warp][qhead + rank][1];
+                b0 = u.x; b1 = u.y; b2 = u.z; b3 = u.w; b4 = v.x; b5 = v.y;
+                ray = __float_as_int(v.z);
+                node = root;
+                top = 0;
             }
+            qhead += take > 0 ? take : 0;
             __syncwarp();
         }
-        const bool active = ray >= 0;
-        bool hit = false;
-        int ref = kEmpty;
-        if (active) {
-            float f[8];
-            ld_slot8(&a.nodes4[node].s[q], f);
-            ref = __float_as_int(f[6]);
-            hit = ref >= 0 && b[0] <= f[1] && b[1] >= f[0] && b[2] <= f[3] && b[3] >= f[2] &&
-                  b[4] <= f[5] && b[5] >= f[4];
-            if (STATS && q == 0) ++visits;
-        }
+        // ---- one node visit per group: one 256-bit slot load per lane ----
+        // (idle groups keep an empty box and re-read the root slot: no branch)
+        float f[8];
+        ld_slot8(slots + 4 * node, f);
+        const int ref = __float_as_int(f[6]);
+        const bool hit = ref >= 0 && b0 <= f[1] && b1 >= f[0] && b2 <= f[3] && b3 >= f[2] &&
+                         b4 <= f[5] && b5 >= f[4];
+        if (STATS && q == 0 && ray >= 0) ++visits;
         const bool leafhit = hit && ref >= n_int;
         const bool ihit = hit && ref < n_int;
-        // ---- collision buffer append (warp-aggregated, chunked) ----
+        // ---- stage leaf candidates; flush 32 at a time (one atomic each) ----
         const unsigned lb = __ballot_sync(kFull, leafhit);
-        if (lb) {
-            const int k = __popc(lb);
-            if (cfill + k > kCandChunk) {
-                long long nb_ = 0;
-                if (lane == 0) {
-                    if (cbase >= 0 && cbase < a.cand_cap) a.chunk_fill[cbase / kCandChunk] = cfill;
-                    nb_ = (long long)atomicAdd(&a.status->cand_count, (unsigned long long)kCandChunk);
-                }
-                cbase = __shfl_sync(kFull, nb_, 0);
-                cfill = 0;
-            }
-            if (leafhit) {
-                const long long at = cbase + cfill + __popc(lb & lt);
-                if (at < a.cand_cap) a.cand[at] = make_int2(ray, ref - n_int);
-            }
-            cfill += k;
+        if (leafhit) my_cs[cn + __popc(lb & lt)] = make_int2(ray, ref - n_int);
+        cn += __popc(lb);
+        if (cn >= 32) {
+            __syncwarp();
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&a.status->cand_count, 32ull);
+            base = __shfl_sync(kFull, base, 0);
+            const int2 c = my_cs[lane];
+            const int2 rest = my_cs[32 + lane];
+            if (base + lane < (unsigned long long)a.cand_cap) a.cand[base + lane] = c;
+            __syncwarp();
+            cn -= 32;
+            if (lane < cn) my_cs[lane] = rest;
         }
-        // ---- push internal hits, pop the next node ----
+        // ---- push internal hits in parallel, pop the next node ----
         const unsigned gm = (__ballot_sync(kFull, ihit) >> gshift) & 0xFu;
-        if (active) {
-            const int k = __popc(gm);
-            if (top + k > kTravStack) {  // cannot happen for fast trees (height <= 61)
+        if (ihit) my_stk[(top + __popc(gm & lt_in_group)) * kTravGroups] = ref;
+        top += __popc(gm);
+        __syncwarp();
+        if (ray >= 0) {
+            if (top == 0) {
+                ray = -1;
+                b0 = b2 = b4 = INFINITY; b1 = b3 = b5 = -INFINITY;
+                node = root;
+            } else if (top > kTravStack) {  // cannot happen for fast trees (height <= 61)
                 if (q == 0) atomicAdd(&a.status->internal, 1ull);
                 ray = -1;
+                top = 0;
+                b0 = b2 = b4 = INFINITY; b1 = b3 = b5 = -INFINITY;
+                node = root;
             } else {
-                if (ihit) stk[top + __popc(gm & ((1u << q) - 1u))][gid] = ref;
-                top += k;
-                if (top == 0) ray = -1;
+                node = my_stk[--top * kTravGroups];
             }
+        } else {
+            top = 0;
         }
-        __syncwarp();
-        if (ray >= 0) node = stk[--top][gid];
     }
-    if (lane == 0 && cbase >= 0 && cbase < a.cand_cap) a.chunk_fill[cbase / kCandChunk] = cfill;
+    // flush the staged tail
+    __syncwarp();
+    if (cn > 0) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&a.status->cand_count, (unsigned long long)cn);
+        base = __shfl_sync(kFull, base, 0);
+        if (lane < cn && base + lane < (unsigned long long)a.cand_cap) a.cand[base + lane] = my_cs[lane];
+    }
     if (STATS) {
         for (int o = 16; o; o >>= 1) visits += __shfl_xor_sync(kFull, visits, o);
         if (lane == 0) atomicAdd(&a.status->visits, visits);
@@ -189,10 +199,6 @@ __global__ void __launch_bounds__(256) k_exact(ExactArgs a) {
                                      ? *a.cand_count : (unsigned long long)a.cand_cap;
     unsigned long long mts = 0;
     for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
-        if ((int)(i % kCandChunk) >= __ldg(a.chunk_fill + i / kCandChunk)) {
-            if (MODE == kBarycentric) a.cand_t[i] = ~0ull;
-            continue;
-        }
         const int2 c = a.cand[i];
         const float* s = a.starts + 3ll * c.x;
         const float* e = a.ends + 3ll * c.x;
