@@ -28,6 +28,8 @@
 #include "rs_common.cuh"
 #include "rs_internal.h"
 
+#include <cstdlib>
+
 namespace rs {
 
 constexpr int kTravThreads = 128;
@@ -42,38 +44,40 @@ __device__ __forceinline__ void ld_slot8(const RsSlot* p, float f[8]) {
                  : "l"(p));
 }
 
-template <bool STATS>
-__global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
-    __shared__ int stk[kTravStack + 4][kTravGroups];
+// G lanes per segment (G = 2: "pairs", each lane tests 2 of the 4 slots;
+// G = 4: "quads", one slot per lane).  A visit is G x (4/G) 256-bit loads
+// within one 128-B node line.
+template <int G, bool STATS>
+__global__ void __launch_bounds__(kTravThreads) k_trav_group(TravArgs a) {
+    constexpr int SL = 4 / G;                 // slots per lane
+    constexpr int GPW = 32 / G;               // groups per warp
+    constexpr int GPC = kTravThreads / G;     // groups per CTA
+    constexpr unsigned kGroupBits = G == 2 ? 0x55555555u : 0x11111111u;
+    __shared__ int stk[kTravStack + 4][GPC];
     __shared__ float4 qs[kTravThreads / 32][32][2];  // per-warp queue: box + segment id
-    __shared__ int2 cs[kTravThreads / 32][64];       // per-warp candidate staging
+    __shared__ int2 cs[kTravThreads / 32][64 + 32 * SL];  // per-warp candidate staging
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int q = lane & 3;
-    const int gshift = lane & ~3;
+    const int h = lane & (G - 1);             // lane within the group
+    const int gshift = lane & ~(G - 1);
     const unsigned lt = (1u << lane) - 1u;
-    const unsigned lt_in_group = (1u << q) - 1u;
-    const unsigned kGroupBits = 0x11111111u;
     const int n_int = a.n_int;
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
-    int* const my_stk = &stk[0][threadIdx.x >> 2];  // this group's column, stride kTravGroups
+    int* const my_stk = &stk[0][threadIdx.x / G];
     int2* const my_cs = cs[warp];
-    const RsSlot* const slots = &a.nodes4[0].s[q];  // + 4 * node
+    const RsSlot* const slots = &a.nodes4[0].s[h * SL];
 
-    int qhead = 0, qcount = 0;  // live segments queued in qs[warp][qhead, qcount)
+    int qhead = 0, qcount = 0;
     bool exhausted = false;
-    int cn = 0;                 // staged candidates (warp-uniform)
-    // per-group traversal state (replicated in the group's 4 lanes)
+    int cn = 0;
     int ray = -1, node = root, top = 0;
-    float b0 = INFINITY, b1 = -INFINITY, b2 = INFINITY, b3 = -INFINITY, b4 = INFINITY,
-          b5 = -INFINITY;  // empty box: overlaps nothing
+    float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f, b4 = 0.f, b5 = 0.f;
     unsigned long long visits = 0;
+    (void)GPW;
 
     for (;;) {
         const unsigned idle = __ballot_sync(kFull, ray < 0) & kGroupBits;
         if (idle) {
-            // refill: claim 32 segments, cull those that miss every child of
-            // the root (their result is the pre-zeroed default), queue the rest
             while (qhead == qcount && !exhausted) {
                 unsigned long long base = 0;
                 if (lane == 0) base = atomicAdd(&a.status->tile_counter, 32ull);
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
             const int avail = qcount - qhead;
             if (avail <= 0 && exhausted && idle == kGroupBits) break;
             const int nidle = __popc(idle);
-            const int take = nidle < avail ? nidle : avail;
+            const int take = nidle < avail ? nidle : (avail > 0 ? avail : 0);
             const int rank = __popc(idle & ((1u << gshift) - 1u));
             if (ray < 0 && rank < take) {
                 const float4 u = qs[warp][qhead + rank][0];
@@ -121,65 +125,99 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_quad(TravArgs a) {
                 node = root;
                 top = 0;
             }
-            qhead += take > 0 ? take : 0;
+            qhead += take;
             __syncwarp();
         }
-        // ---- one node visit per group: one 256-bit slot load per lane ----
-        // (idle groups keep an empty box and re-read the root slot: no branch)
-        float f[8];
-        ld_slot8(slots + 4 * node, f);
-        const int ref = __float_as_int(f[6]);
-        const bool hit = ref >= 0 && b0 <= f[1] && b1 >= f[0] && b2 <= f[3] && b3 >= f[2] &&
-                         b4 <= f[5] && b5 >= f[4];
-        if (STATS && q == 0 && ray >= 0) ++visits;
-        const bool leafhit = hit && ref >= n_int;
-        const bool ihit = hit && ref < n_int;
-        // ---- stage leaf candidates; flush 32 at a time (one atomic each) ----
-        const unsigned lb = __ballot_sync(kFull, leafhit);
-        if (leafhit) my_cs[cn + __popc(lb & lt)] = make_int2(ray, ref - n_int);
-        cn += __popc(lb);
+        const bool live = ray >= 0;
+        // ---- one node visit: SL 256-bit slot loads per lane ----
+        unsigned lbits = 0, ibits = 0;
+        int refs[SL];
+#pragma unroll
+        for (int j = 0; j < SL; ++j) {
+            float f[8];
+            ld_slot8(slots + 4 * node + j, f);
+            refs[j] = __float_as_int(f[6]);
+            const bool hit = live && refs[j] >= 0 && b0 <= f[1] && b1 >= f[0] && b2 <= f[3] &&
+                             b3 >= f[2] && b4 <= f[5] && b5 >= f[4];
+            lbits |= (hit && refs[j] >= n_int) ? (1u << j) : 0u;
+            ibits |= (hit && refs[j] < n_int) ? (1u << j) : 0u;
+        }
+        if (STATS && h == 0 && live) ++visits;
+        // ---- stage leaf candidates (warp prefix over per-lane counts) ----
+        {
+            const int c = __popc(lbits);
+            unsigned pre = 0, tot = 0;
+#pragma unroll
+            for (int bit = 0; bit < (SL == 2 ? 2 : 1); ++bit) {
+                const unsigned bm = __ballot_sync(kFull, (c >> bit) & 1);
+                pre += __popc(bm & lt) << bit;
+                tot += __popc(bm) << bit;
+            }
+            if (c) {
+                int at = cn + pre;
+#pragma unroll
+                for (int j = 0; j < SL; ++j)
+                    if (lbits & (1u << j)) my_cs[at++] = make_int2(ray, refs[j] - n_int);
+            }
+            cn += tot;
+        }
         if (cn >= 32) {
             __syncwarp();
             unsigned long long base = 0;
             if (lane == 0) base = atomicAdd(&a.status->cand_count, 32ull);
             base = __shfl_sync(kFull, base, 0);
-            const int2 c = my_cs[lane];
-            const int2 rest = my_cs[32 + lane];
-            if (base + lane < (unsigned long long)a.cand_cap) a.cand[base + lane] = c;
+            const int2 c0 = my_cs[lane];
+            const int2 c1 = my_cs[32 + lane];
+            const int2 c2 = SL == 2 ? my_cs[64 + lane] : make_int2(0, 0);
+            if (base + lane < (unsigned long long)a.cand_cap) a.cand[base + lane] = c0;
             __syncwarp();
             cn -= 32;
-            if (lane < cn) my_cs[lane] = rest;
+            if (lane < cn) my_cs[lane] = c1;
+            if (SL == 2 && lane + 32 < cn) my_cs[32 + lane] = c2;
         }
-        // ---- push internal hits in parallel, pop the next node ----
-        const unsigned gm = (__ballot_sync(kFull, ihit) >> gshift) & 0xFu;
-        if (ihit) my_stk[(top + __popc(gm & lt_in_group)) * kTravGroups] = ref;
-        top += __popc(gm);
+        // ---- push internal hits, pop the next node ----
+        {
+            const int c = __popc(ibits);
+            int off = 0, tot = c;
+            if (G == 2) {
+                const int other = __shfl_xor_sync(kFull, c, 1);
+                off = h ? other : 0;
+                tot = c + other;
+            } else {
+                const unsigned bm = (__ballot_sync(kFull, ibits != 0) >> gshift) & 0xFu;
+                off = __popc(bm & ((1u << h) - 1u));
+                tot = __popc(bm);
+            }
+            if (c) {
+                int at = top + off;
+#pragma unroll
+                for (int j = 0; j < SL; ++j)
+                    if (ibits & (1u << j)) my_stk[(at++) * GPC] = refs[j];
+            }
+            top += tot;
+        }
         __syncwarp();
-        if (ray >= 0) {
+        if (live) {
             if (top == 0) {
                 ray = -1;
-                b0 = b2 = b4 = INFINITY; b1 = b3 = b5 = -INFINITY;
-                node = root;
             } else if (top > kTravStack) {  // cannot happen for fast trees (height <= 61)
-                if (q == 0) atomicAdd(&a.status->internal, 1ull);
+                if (h == 0) atomicAdd(&a.status->internal, 1ull);
                 ray = -1;
                 top = 0;
-                b0 = b2 = b4 = INFINITY; b1 = b3 = b5 = -INFINITY;
-                node = root;
             } else {
-                node = my_stk[--top * kTravGroups];
+                node = my_stk[--top * GPC];
             }
         } else {
             top = 0;
         }
     }
-    // flush the staged tail
     __syncwarp();
     if (cn > 0) {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(&a.status->cand_count, (unsigned long long)cn);
         base = __shfl_sync(kFull, base, 0);
-        if (lane < cn && base + lane < (unsigned long long)a.cand_cap) a.cand[base + lane] = my_cs[lane];
+        for (int k = lane; k < cn; k += 32)
+            if (base + k < (unsigned long long)a.cand_cap) a.cand[base + k] = my_cs[k];
     }
     if (STATS) {
         for (int o = 16; o; o >>= 1) visits += __shfl_xor_sync(kFull, visits, o);
@@ -346,11 +384,16 @@ static int sm_count() {
 void launch_trav(const TravArgs& a, bool stats, cudaStream_t s) {
     if (a.n_r <= 0) return;
     count_launches(1);
-    auto k = stats ? k_trav_quad<true> : k_trav_quad<false>;
-    static int occ[2] = {0, 0};
-    int& o = occ[stats ? 1 : 0];
+    static const int lanes = [] {
+        const char* e = getenv("RS_TRAV_LANES");
+        return e && e[0] == '4' ? 4 : 2;
+    }();
+    auto k = lanes == 4 ? (stats ? k_trav_group<4, true> : k_trav_group<4, false>)
+                        : (stats ? k_trav_group<2, true> : k_trav_group<2, false>);
+    static int occ[4] = {0, 0, 0, 0};
+    int& o = occ[(stats ? 1 : 0) + (lanes == 4 ? 2 : 0)];
     if (!o) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kTravThreads, 0);
-    const long long want = (a.n_r + kTravGroups - 1) / kTravGroups;
+    const long long want = (a.n_r + kTravThreads / lanes - 1) / (kTravThreads / lanes);
     const long long pg = (long long)sm_count() * (o > 0 ? o : 1);
     k<<<(unsigned)(want < pg ? want : pg), kTravThreads, 0, s>>>(a);
 }
