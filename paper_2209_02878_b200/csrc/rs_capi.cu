@@ -355,6 +355,7 @@ struct FastScratch {
     int* best_tri = nullptr;
     long long cap = 0;
     size_t tiles_bytes = 0;
+    int* gstack = nullptr;
 };
 
 static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cudaStream_t s) {
@@ -367,8 +368,9 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     const size_t b_btri = bary ? align256(4ull * n_r) : 0;
     const size_t b_ct = bary ? align256(8ull * cap) : 0;
     const size_t b_tiles = bary ? align256(bary_compact_scratch(n_r)) : 0;
+    const size_t b_gst = align256(4 * trav_gstack_ints());
     CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk),
-                       b_st + b_cand + b_fill + b_bt + b_btri + b_ct + b_tiles + 256, s));
+                       b_st + b_cand + b_fill + b_bt + b_btri + b_ct + b_tiles + b_gst + 256, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
     f.cand = c.take<int2>(cap);
@@ -381,6 +383,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         f.tile_ctr = f.tiles + (bary_compact_scratch(n_r) / 8 - 1);
         f.tiles_bytes = bary_compact_scratch(n_r);
     }
+    f.gstack = c.take<int>(trav_gstack_ints());
     f.cap = cap;
     return RS_OK;
 }
@@ -395,7 +398,8 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
         CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
     }
-    TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill, f.st};
+    TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill, f.st,
+                f.gstack};
     ev_record(1, s);
     launch_trav(ta, stats, s);
     ExactArgs ea{f.cand, &f.st->cand_count, f.cap, f.chunk_fill, d_s, d_e, t->leaves,

@@ -95,7 +95,9 @@ struct TravArgs {
     long long cand_cap;    // multiple of kCandChunk
     int* chunk_fill;       // entries used per chunk
     RsStatus* status;
+    int* gstack;           // per-group traversal stack overflow (trav_gstack_ints())
 };
+size_t trav_gstack_ints();
 struct ExactArgs {
     const int2* cand;
     const unsigned long long* cand_count;

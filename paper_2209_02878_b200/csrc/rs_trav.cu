@@ -35,6 +35,7 @@ namespace rs {
 constexpr int kTravThreads = 128;
 constexpr int kTravGroups = kTravThreads / 4;
 constexpr int kTravStack = 96;  // 4-wide depth <= 31 x 3 pending pushes
+constexpr int kSmemStack = 12;  // entries kept in shared memory; deeper ones in global
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ void ld_slot8(const RsSlot* p, float f[8]) {
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_group(TravArgs a) {
     constexpr int GPW = 32 / G;               // groups per warp
     constexpr int GPC = kTravThreads / G;     // groups per CTA
     constexpr unsigned kGroupBits = G == 2 ? 0x55555555u : 0x11111111u;
-    __shared__ int stk[kTravStack + 4][GPC];
+    __shared__ int stk[kSmemStack][GPC];
     __shared__ float4 qs[kTravThreads / 32][32][2];  // per-warp queue: box + segment id
     __shared__ int2 cs[kTravThreads / 32][64 + 32 * SL];  // per-warp candidate staging
     const int lane = threadIdx.x & 31;
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_group(TravArgs a) {
     const int n_int = a.n_int;
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
     int* const my_stk = &stk[0][threadIdx.x / G];
+    int* const my_gstk = a.gstack + ((long long)blockIdx.x * GPC + threadIdx.x / G) * kTravStack;
     int2* const my_cs = cs[warp];
     const RsSlot* const slots = &a.nodes4[0].s[h * SL];
 
@@ -175,37 +177,45 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_group(TravArgs a) {
             if (lane < cn) my_cs[lane] = c1;
             if (SL == 2 && lane + 32 < cn) my_cs[32 + lane] = c2;
         }
-        // ---- push internal hits, pop the next node ----
-        {
-            const int c = __popc(ibits);
-            int off = 0, tot = c;
-            if (G == 2) {
-                const int other = __shfl_xor_sync(kFull, c, 1);
-                off = h ? other : 0;
-                tot = c + other;
-            } else {
-                const unsigned bm = (__ballot_sync(kFull, ibits != 0) >> gshift) & 0xFu;
-                off = __popc(bm & ((1u << h) - 1u));
-                tot = __popc(bm);
-            }
-            if (c) {
-                int at = top + off;
+        // ---- next node: the first internal hit (in registers); the other
+        //      internal hits are pushed; pop only when nothing was hit ----
+        unsigned gm;
+        if (G == 2) {
+            const unsigned o = __shfl_xor_sync(kFull, ibits, 1);
+            gm = h ? (o | (ibits << 2)) : (ibits | (o << 2));
+        } else {
+            gm = (__ballot_sync(kFull, ibits != 0) >> gshift) & 0xFu;
+        }
+        const int first = gm ? __ffs(gm) - 1 : 0;
+        const int nxt = __shfl_sync(kFull, SL == 2 ? ((first & 1) ? refs[SL - 1] : refs[0]) : refs[0],
+                                    gshift + first / SL);
+        const unsigned rest = gm & (gm - 1u);
+        if (rest) {
 #pragma unroll
-                for (int j = 0; j < SL; ++j)
-                    if (ibits & (1u << j)) my_stk[(at++) * GPC] = refs[j];
+            for (int j = 0; j < SL; ++j) {
+                const int bit = h * SL + j;
+                if (rest & (1u << bit)) {
+                    const int pos = top + __popc(rest & ((1u << bit) - 1u));
+                    if (pos < kSmemStack) my_stk[pos * GPC] = refs[j];
+                    else if (pos < kTravStack) my_gstk[pos] = refs[j];
+                }
             }
-            top += tot;
+            top += __popc(rest);
         }
         __syncwarp();
         if (live) {
-            if (top == 0) {
+            if (gm) {
+                node = nxt;
+                if (top > kTravStack) {  // cannot happen for fast trees (height <= 61)
+                    if (h == 0) atomicAdd(&a.status->internal, 1ull);
+                    ray = -1;
+                    top = 0;
+                }
+            } else if (top == 0) {
                 ray = -1;
-            } else if (top > kTravStack) {  // cannot happen for fast trees (height <= 61)
-                if (h == 0) atomicAdd(&a.status->internal, 1ull);
-                ray = -1;
-                top = 0;
             } else {
-                node = my_stk[--top * GPC];
+                --top;
+                node = top < kSmemStack ? my_stk[top * GPC] : my_gstk[top];
             }
         } else {
             top = 0;
@@ -381,6 +391,9 @@ static int sm_count() {
     return sms;
 }
 
+// persistent grid: at most 16 CTAs per SM of kTravThreads, <= kTravThreads/2 groups each
+size_t trav_gstack_ints() { return (size_t)sm_count() * 16 * (kTravThreads / 2) * kTravStack; }
+
 void launch_trav(const TravArgs& a, bool stats, cudaStream_t s) {
     if (a.n_r <= 0) return;
     count_launches(1);
@@ -394,7 +407,7 @@ void launch_trav(const TravArgs& a, bool stats, cudaStream_t s) {
     int& o = occ[(stats ? 1 : 0) + (lanes == 4 ? 2 : 0)];
     if (!o) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kTravThreads, 0);
     const long long want = (a.n_r + kTravThreads / lanes - 1) / (kTravThreads / lanes);
-    const long long pg = (long long)sm_count() * (o > 0 ? o : 1);
+    const long long pg = (long long)sm_count() * (o > 0 ? (o < 16 ? o : 16) : 1);
     k<<<(unsigned)(want < pg ? want : pg), kTravThreads, 0, s>>>(a);
 }
 
