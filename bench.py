@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--tree", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--presort", action="store_true",
+                    help="experiment: Morton-order the segments on the host before upload")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -203,6 +205,9 @@ def main():
     n_tri, n_rays, mode, layers, desc = CONFIGS[cfg]
     sc = make_scene(cfg)
     mesh_h, seg_h = sc.mesh, sc.segments
+    if args.presort:
+        seg_h, perm = rs.sort_segments_by_morton(seg_h)
+        sc.expected_crossings = sc.expected_crossings[perm]
     dev = torch.device("cuda", local)
     mesh_d = rs.Mesh.from_arrays(torch.from_numpy(mesh_h.vertices).to(dev),
                                  torch.from_numpy(mesh_h.triangles).to(dev))
