@@ -433,6 +433,12 @@ static int fast_query(const rs_tree* t, const float* d_s, const float* d_e, int6
     return fail(RS_INTERNAL, "collision buffer overflow after re-launch");
 }
 
+// The pair traversal keeps a bounded shared-memory stack; a tree deep enough
+// to exceed it (pathological inputs only) is re-queried with the binary
+// kernels, whose stack covers the fast tree's full height.
+static int binary_query(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r,
+                        int mode, const FastOut& o, RsStatus* h, cudaStream_t s);
+
 static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
                       int max_coll, int max_stack, int ref, int32_t* det, int32_t* cnt,
                       int32_t* tri, float* dist, float* pts, int32_t* c_ray, float* c_dist,
@@ -451,6 +457,10 @@ static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int6
         RsStatus h{};
         rc = fast_query(t, d_s, d_e, n_r, mode, o, stats, &h, s);
         if (rc) return rc;
+        if (h.internal) {
+            rc = binary_query(t, d_s, d_e, n_r, mode, o, &h, s);
+            if (rc) return rc;
+        }
         if (n_hits) *n_hits = (int64_t)h.hits;
         if (visits) *visits = (int64_t)h.visits;
         if (mts) *mts = (int64_t)h.mts;
@@ -479,6 +489,30 @@ static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int6
     if (visits) *visits = (int64_t)h.visits;
     if (mts) *mts = (int64_t)h.mts;
     return status_code(h, bad);
+}
+
+static int binary_query(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r,
+                        int mode, const FastOut& o, RsStatus* h, cudaStream_t s) {
+    const bool compact = o.c_ray != nullptr;
+    char* blk = nullptr;
+    const size_t cs = compact ? compact_scratch_bytes(n_r) : 0;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
+    CK(cudaMemsetAsync(blk, 0, align256(sizeof(RsStatus)) + cs, s));
+    RsStatus* st = reinterpret_cast<RsStatus*>(blk);
+    QueryArgs a = make_args(t, d_s, d_e, n_r, 32, 1 << 30, st);
+    a.detected = mode == kCount ? nullptr : (mode == kBarycentric ? o.det : o.flags);
+    a.counts = o.flags;
+    a.tri = o.tri; a.dist = o.dist; a.points = o.pts;
+    a.c_ray = o.c_ray; a.c_dist = o.c_dist; a.c_tri = o.c_tri; a.c_point = o.c_pt;
+    a.ray_offset = o.ray_offset;
+    a.tile_status = reinterpret_cast<unsigned long long*>(blk + align256(sizeof(RsStatus)));
+    a.nodes4 = nullptr;  // binary kernels
+    if (launch_query(a, mode, false, compact, 64, false, s))
+        return fail(RS_INTERNAL, "no binary kernel variant");
+    CK(cudaGetLastError());
+    int rc = read_status(st, s, h);
+    CK(cudaFreeAsync(blk, s));
+    return rc;
 }
 
 int rs_query(const rs_tree* t, const float* d_starts, const float* d_ends, int64_t n_r, int mode,

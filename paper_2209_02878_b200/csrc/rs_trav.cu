@@ -36,6 +36,7 @@ constexpr int kTravThreads = 128;
 constexpr int kTravGroups = kTravThreads / 4;
 constexpr int kTravStack = 96;  // 4-wide depth <= 31 x 3 pending pushes
 constexpr int kSmemStack = 12;  // entries kept in shared memory; deeper ones in global
+constexpr int kPairStack = 32;  // pair kernel: shared-memory stack entries per segment
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ void ld_slot8(const RsSlot* p, float f[8]) {
@@ -235,6 +236,164 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_group(TravArgs a) {
     }
 }
 
+// Pairs, written branch-light: two lanes per segment, lane h tests slots 2h
+// and 2h+1 of the 4-wide node (two 256-bit loads from one 128-B line).
+// Candidate staging, stack pushes and the next-node choice are predicated
+// stores / selects rather than branches.
+__device__ __forceinline__ bool box_hit(const float f[8], float b0, float b1, float b2, float b3,
+                                        float b4, float b5) {
+    return (b0 <= f[1]) & (b1 >= f[0]) & (b2 <= f[3]) & (b3 >= f[2]) & (b4 <= f[5]) & (b5 >= f[4]);
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(kTravThreads) k_trav_pair(TravArgs a) {
+    constexpr int GPC = kTravThreads / 2;
+    constexpr unsigned kGroupBits = 0x55555555u;
+    __shared__ int stk[kPairStack][GPC];
+    __shared__ float4 qs[kTravThreads / 32][32][2];
+    __shared__ int2 cs[kTravThreads / 32][128];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int h = lane & 1;
+    const int gshift = lane & ~1;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned below_me = (1u << (2 * h)) - 1u;  // group slot bits owned by lane 0 if h==1
+    const int n_int = a.n_int;
+    const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    const int gid = threadIdx.x >> 1;
+    int2* const my_cs = cs[warp];
+    const RsSlot* const slots = &a.nodes4[0].s[2 * h];
+
+    int qhead = 0, qcount = 0;
+    bool exhausted = false;
+    int cn = 0;
+    int ray = -1, node = root, top = 0;
+    float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f, b4 = 0.f, b5 = 0.f;
+    unsigned long long visits = 0;
+
+    for (;;) {
+        const unsigned idle = __ballot_sync(kFull, ray < 0) & kGroupBits;
+        if (idle) {
+            while (qhead == qcount && !exhausted) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(&a.status->tile_counter, 32ull);
+                base = __shfl_sync(kFull, base, 0);
+                exhausted = (long long)base + 32 >= a.n_r;
+                const long long rid = (long long)base + lane;
+                bool live = false;
+                float bx[6];
+                if (rid < a.n_r) {
+                    const float* sp = a.starts + 3 * rid;
+                    const float* ep = a.ends + 3 * rid;
+                    const float s0 = __ldg(sp), s1 = __ldg(sp + 1), s2 = __ldg(sp + 2);
+                    const float e0 = __ldg(ep), e1 = __ldg(ep + 1), e2 = __ldg(ep + 2);
+                    bx[0] = fminf(s0, e0); bx[1] = fmaxf(s0, e0);  // engine.py:115-122
+                    bx[2] = fminf(s1, e1); bx[3] = fmaxf(s1, e1);
+                    bx[4] = fminf(s2, e2); bx[5] = fmaxf(s2, e2);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float f[8];
+                        ld_slot8(&a.nodes4[root].s[j], f);
+                        live |= (__float_as_int(f[6]) >= 0) & box_hit(f, bx[0], bx[1], bx[2], bx[3], bx[4], bx[5]);
+                    }
+                }
+                const unsigned lm = __ballot_sync(kFull, live);
+                if (live) {
+                    const int at = __popc(lm & lt);
+                    qs[warp][at][0] = make_float4(bx[0], bx[1], bx[2], bx[3]);
+                    qs[warp][at][1] = make_float4(bx[4], bx[5], __int_as_float((int)rid), 0.f);
+                }
+                qhead = 0;
+                qcount = __popc(lm);
+                __syncwarp();
+            }
+            const int avail = qcount - qhead;
+            if (avail <= 0 && exhausted && idle == kGroupBits) break;
+            const int nidle = __popc(idle);
+            const int take = nidle < avail ? nidle : (avail > 0 ? avail : 0);
+            const int rank = __popc(idle & ((1u << gshift) - 1u));
+            if (ray < 0 && rank < take) {
+                const float4 u = qs[warp][qhead + rank][0];
+                const float4 v = qs[warp][qhead + rank][1];
+                b0 = u.x; b1 = u.y; b2 = u.z; b3 = u.w; b4 = v.x; b5 = v.y;
+                ray = __float_as_int(v.z);
+                node = root;
+                top = 0;
+            }
+            qhead += take;
+            __syncwarp();
+        }
+        const bool live = ray >= 0;
+        float fa[8], fb[8];
+        ld_slot8(slots + 4 * node, fa);
+        ld_slot8(slots + 4 * node + 1, fb);
+        const int ra = __float_as_int(fa[6]), rb = __float_as_int(fb[6]);
+        const bool ha = live & (ra >= 0) & box_hit(fa, b0, b1, b2, b3, b4, b5);
+        const bool hb = live & (rb >= 0) & box_hit(fb, b0, b1, b2, b3, b4, b5);
+        const bool la = ha & (ra >= n_int), lb = hb & (rb >= n_int);
+        const bool ia = ha & (ra < n_int), ib = hb & (rb < n_int);
+        if (STATS) visits += (h == 0) & live;
+        // ---- candidates: predicated staging stores ----
+        const unsigned ba = __ballot_sync(kFull, la), bb = __ballot_sync(kFull, lb);
+        const int pa = cn + __popc(ba & lt) + __popc(bb & lt);
+        if (la) my_cs[pa] = make_int2(ray, ra - n_int);
+        if (lb) my_cs[pa + la] = make_int2(ray, rb - n_int);
+        cn += __popc(ba) + __popc(bb);
+        if (cn >= 32) {
+            __syncwarp();
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&a.status->cand_count, 32ull);
+            base = __shfl_sync(kFull, base, 0);
+            const int2 c0 = my_cs[lane];
+            const int2 c1 = my_cs[32 + lane];
+            const int2 c2 = my_cs[64 + lane];
+            if (base + lane < (unsigned long long)a.cand_cap) a.cand[base + lane] = c0;
+            __syncwarp();
+            cn -= 32;
+            if (lane < cn) my_cs[lane] = c1;
+            if (lane + 32 < cn) my_cs[32 + lane] = c2;
+        }
+        // ---- next node: first internal hit; push the others; else pop ----
+        const unsigned mine = (unsigned)ia | ((unsigned)ib << 1);
+        const unsigned other = __shfl_xor_sync(kFull, mine, 1);
+        const unsigned gm = h ? (other | (mine << 2)) : (mine | (other << 2));
+        const int first = __ffs(gm) - 1;  // -1 when gm == 0
+        const int nxt = __shfl_sync(kFull, (first & 1) ? rb : ra, gshift + ((first >> 1) & 1));
+        const unsigned rest = gm & (gm - 1u);
+        const bool pa_ = (rest >> (2 * h)) & 1u, pb_ = (rest >> (2 * h + 1)) & 1u;
+        const int qa = top + __popc(rest & below_me);
+        const int qb = qa + pa_;
+        if (pa_ & (qa < kPairStack)) stk[qa][gid] = ra;
+        if (pb_ & (qb < kPairStack)) stk[qb][gid] = rb;
+        top += __popc(rest);
+        __syncwarp();
+        const bool empty = gm == 0u;
+        const int popped = stk[top > 0 ? top - 1 : 0][gid];
+        const bool pop = live & empty & (top > 0);
+        node = empty ? popped : nxt;
+        top -= pop;
+        // a deeper stack than kPairStack: flag it; the host re-runs the
+        // query with the binary kernels (never seen on real trees)
+        const bool ovf = live & (top > kPairStack);
+        if (ovf & (h == 0)) atomicAdd(&a.status->internal, 1ull);
+        const bool done = !live | (empty & !pop) | ovf;
+        ray = done ? -1 : ray;
+        top = done ? 0 : top;
+    }
+    __syncwarp();
+    if (cn > 0) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&a.status->cand_count, (unsigned long long)cn);
+        base = __shfl_sync(kFull, base, 0);
+        for (int k = lane; k < cn; k += 32)
+            if (base + k < (unsigned long long)a.cand_cap) a.cand[base + k] = my_cs[k];
+    }
+    if (STATS) {
+        for (int o = 16; o; o >>= 1) visits += __shfl_xor_sync(kFull, visits, o);
+        if (lane == 0) atomicAdd(&a.status->visits, visits);
+    }
+}
+
 // t >= 0 for every hit, so the IEEE bits order like the values; -0.0 is
 // folded onto +0.0 (they compare equal in the reference's `t < best_t`).
 __device__ __forceinline__ unsigned long long t_key(double t) {
@@ -402,7 +561,7 @@ void launch_trav(const TravArgs& a, bool stats, cudaStream_t s) {
         return e && e[0] == '4' ? 4 : 2;
     }();
     auto k = lanes == 4 ? (stats ? k_trav_group<4, true> : k_trav_group<4, false>)
-                        : (stats ? k_trav_group<2, true> : k_trav_group<2, false>);
+                        : (stats ? k_trav_pair<true> : k_trav_pair<false>);
     static int occ[4] = {0, 0, 0, 0};
     int& o = occ[(stats ? 1 : 0) + (lanes == 4 ? 2 : 0)];
     if (!o) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kTravThreads, 0);
