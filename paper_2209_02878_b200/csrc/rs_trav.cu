@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(kTravThreads) k_trav_pair(TravArgs a) {
         const bool done = !live | (empty & !pop) | ovf;
         ray = done ? -1 : ray;
         top = done ? 0 : top;
+        node = done ? root : node;  // idle groups keep loading a valid node
     }
     __syncwarp();
     if (cn > 0) {
