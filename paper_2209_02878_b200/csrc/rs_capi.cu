@@ -356,21 +356,30 @@ struct FastScratch {
     long long cap = 0;
     size_t tiles_bytes = 0;
     int* gstack = nullptr;
+    unsigned *bins = nullptr, *cursor = nullptr, *n_live = nullptr;
+    float4* rec = nullptr;
 };
 
+// RS_FAST_PATH=buffer: pair traversal -> collision buffer -> exact pass
+// (A/B tuning); default: coherent sorted traversal.
+static const bool g_buffer_path = [] {
+    const char* e = getenv("RS_FAST_PATH");
+    return e && e[0] == 'b';
+}();
+
 static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cudaStream_t s) {
+    if (!g_buffer_path) cap = kCandChunk;  // the sorted path has no collision buffer
     cap = ((cap + kCandChunk - 1) / kCandChunk) * kCandChunk;
     const bool bary = mode == kBarycentric;
-    const size_t b_st = align256(sizeof(RsStatus));
-    const size_t b_cand = align256(8ull * cap);
-    const size_t b_fill = align256(4ull * (cap / kCandChunk + 1));
-    const size_t b_bt = bary ? align256(8ull * n_r) : 0;
-    const size_t b_btri = bary ? align256(4ull * n_r) : 0;
-    const size_t b_ct = bary ? align256(8ull * cap) : 0;
-    const size_t b_tiles = bary ? align256(bary_compact_scratch(n_r)) : 0;
-    const size_t b_gst = align256(4 * trav_gstack_ints());
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk),
-                       b_st + b_cand + b_fill + b_bt + b_btri + b_ct + b_tiles + b_gst + 256, s));
+    size_t total = 256;
+    total += align256(sizeof(RsStatus));
+    total += align256(8ull * cap) + align256(4ull * (cap / kCandChunk + 1));
+    if (bary)
+        total += align256(8ull * n_r) + align256(4ull * n_r) + align256(8ull * cap) +
+                 align256(bary_compact_scratch(n_r));
+    if (g_buffer_path) total += align256(4 * trav_gstack_ints());
+    total += 2 * align256(4 * sorted_bins()) + align256(4 * 64) + align256(32ull * n_r);
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
     f.cand = c.take<int2>(cap);
@@ -383,7 +392,11 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         f.tile_ctr = f.tiles + (bary_compact_scratch(n_r) / 8 - 1);
         f.tiles_bytes = bary_compact_scratch(n_r);
     }
-    f.gstack = c.take<int>(trav_gstack_ints());
+    if (g_buffer_path) f.gstack = c.take<int>(trav_gstack_ints());
+    f.bins = c.take<unsigned>(sorted_bins());
+    f.cursor = c.take<unsigned>(sorted_bins());
+    f.n_live = c.take<unsigned>(64);
+    f.rec = c.take<float4>(2ull * n_r);
     f.cap = cap;
     return RS_OK;
 }
@@ -398,13 +411,20 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
         CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
     }
-    TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill, f.st,
-                f.gstack};
     ev_record(1, s);
-    launch_trav(ta, stats, s);
-    ExactArgs ea{f.cand, &f.st->cand_count, f.cap, f.chunk_fill, d_s, d_e, t->leaves,
-                 o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
-    launch_exact(ea, mode, stats, s);
+    if (g_buffer_path) {
+        TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill,
+                    f.st, f.gstack};
+        launch_trav(ta, stats, s);
+        ExactArgs ea{f.cand, &f.st->cand_count, f.cap, f.chunk_fill, d_s, d_e, t->leaves,
+                     o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
+        launch_exact(ea, mode, stats, s);
+    } else {
+        CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins(), s));
+        SortedArgs sa{t->nodes4, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.bins,
+                      f.cursor, f.n_live, f.rec, o.flags, f.best_t, f.best_tri, f.st};
+        launch_sorted(sa, mode, stats, s);
+    }
     if (bary) {
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
                        f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset};

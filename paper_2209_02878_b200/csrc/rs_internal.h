@@ -128,6 +128,28 @@ struct CompactArgs {
     long long ray_offset;
 };
 void launch_trav(const TravArgs& a, bool stats, cudaStream_t s);
+
+// Coherent fast path (rs_sorted.cu): root cull + counting sort into spatial
+// bins, then one thread per segment in bin order.
+struct SortedArgs {
+    const RsNode4* nodes4;
+    const RsLeaf* leaves;
+    const RsHeader* hdr;
+    int n_int;
+    const float* starts;
+    const float* ends;
+    long long n_r;
+    unsigned* bins;      // sorted_bins() counters (zeroed)
+    unsigned* cursor;    // sorted_bins() scatter cursors
+    unsigned* n_live;    // live segment count (written by the scan)
+    float4* rec;         // n_r x 32-B records (start, id, end)
+    int* flags;                  // boolean / count output (pre-zeroed)
+    unsigned long long* best_t;  // barycentric (pre-set ~0)
+    int* best_tri;               // barycentric (pre-set -1)
+    RsStatus* status;
+};
+size_t sorted_bins();
+void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s);
 void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);
 size_t bary_compact_scratch(long long n_r);
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s);

@@ -1,0 +1,303 @@
+// rs_sorted.cu -- the fast-tree hot path: coherent per-segment traversal.
+//
+// Segments arrive in caller order, which for random inputs means neighbouring
+// lanes walk unrelated parts of the tree and every node load is a scattered
+// 128-B line (L1-wavefront bound).  So the query first reorders the segments
+// spatially with a two-pass counting sort, fused with root culling:
+//
+//   k_bin_count    per segment: f32 AABB (engine.py:115-122), test against the
+//                  root's children (a segment overlapping none of them has no
+//                  candidates: its result is the pre-zeroed default and it is
+//                  dropped here), 16-bit isotropic Morton key of the box centre
+//                  over the root box, warp-aggregated histogram atomics.
+//   k_bin_scan     exclusive scan of the 65,536 bins (one CTA).
+//   k_bin_scatter  same key; each live segment's record (start, id, end; 32 B)
+//                  goes to its bin.
+//   k_trav_sorted  one thread per record, in bin order: stack traversal of the
+//                  4-wide BVH (four 256-bit slot loads per visit, exact f32
+//                  box tests), f64 Moller-Trumbore at the leaves in reference
+//                  op order, boolean early exit, result written to the
+//                  segment's original row.  Lanes of a warp hold spatially
+//                  adjacent segments, so their node loads coalesce.
+//
+// Results do not depend on the order: boolean = any, count = sum, barycentric
+// = min over (t, triangle id) (_core.pyx:304-322).
+#include "rs_common.cuh"
+#include "rs_internal.h"
+
+namespace rs {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+constexpr int kAxisBits = 6;                 // bins per axis = 64
+constexpr int kBinBits = 3 * kAxisBits;
+constexpr int kBins = 1 << kBinBits;
+constexpr int kSortedThreads = 128;
+constexpr int kSortedStack = 64;  // fast tree: <= 3 pending per 4-wide level; deeper -> fallback
+
+__device__ __forceinline__ void ld_slot(const RsSlot* p, float f[8]) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(f[0]), "=f"(f[1]), "=f"(f[2]), "=f"(f[3]), "=f"(f[4]), "=f"(f[5]), "=f"(f[6]),
+          "=f"(f[7])
+        : "l"(p));
+}
+
+__device__ __forceinline__ bool slot_hit(const float f[8], const float b[6]) {
+    return (__float_as_int(f[6]) >= 0) & (b[0] <= f[1]) & (b[1] >= f[0]) & (b[2] <= f[3]) &
+           (b[3] >= f[2]) & (b[4] <= f[5]) & (b[5] >= f[4]);
+}
+
+__device__ __forceinline__ unsigned spread_bits(unsigned v) {  // bit i -> bit 3i
+    unsigned r = 0;
+#pragma unroll
+    for (int i = 0; i < kAxisBits; ++i) r |= ((v >> i) & 1u) << (3 * i);
+    return r;
+}
+
+// Root box + culling helper shared by both binning passes.
+struct RootInfo {
+    float lo[3], inv[3];
+};
+
+__device__ __forceinline__ void root_info(const RsNode4* nodes4, int root, RootInfo& ri) {
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float f[8];
+        ld_slot(&nodes4[root].s[j], f);
+        if (__float_as_int(f[6]) >= 0) {
+            lo[0] = fminf(lo[0], f[0]); hi[0] = fmaxf(hi[0], f[1]);
+            lo[1] = fminf(lo[1], f[2]); hi[1] = fmaxf(hi[1], f[3]);
+            lo[2] = fminf(lo[2], f[4]); hi[2] = fmaxf(hi[2], f[5]);
+        }
+    }
+    const float ext = fmaxf(fmaxf(hi[0] - lo[0], hi[1] - lo[1]), fmaxf(hi[2] - lo[2], 1e-30f));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        ri.lo[k] = lo[k];
+        ri.inv[k] = ((float)(1 << kAxisBits) - 0.01f) / ext;
+    }
+}
+
+// Returns the bin of a live segment, or -1 when it overlaps no root child.
+__device__ __forceinline__ int seg_bin(const float* __restrict__ S, const float* __restrict__ E,
+                                       long long i, const RsNode4* nodes4, int root,
+                                       const RootInfo& ri, float s[3], float e[3]) {
+    s[0] = __ldg(S + 3 * i); s[1] = __ldg(S + 3 * i + 1); s[2] = __ldg(S + 3 * i + 2);
+    e[0] = __ldg(E + 3 * i); e[1] = __ldg(E + 3 * i + 1); e[2] = __ldg(E + 3 * i + 2);
+    float b[6];
+    b[0] = fminf(s[0], e[0]); b[1] = fmaxf(s[0], e[0]);
+    b[2] = fminf(s[1], e[1]); b[3] = fmaxf(s[1], e[1]);
+    b[4] = fminf(s[2], e[2]); b[5] = fmaxf(s[2], e[2]);
+    bool live = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        float f[8];
+        ld_slot(&nodes4[root].s[j], f);
+        live |= slot_hit(f, b);
+    }
+    if (!live) return -1;
+    unsigned key = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float c = 0.5f * (b[2 * k] + b[2 * k + 1]);
+        const float q = fminf(fmaxf((c - ri.lo[k]) * ri.inv[k], 0.f), (float)((1 << kAxisBits) - 1));
+        key |= spread_bits((unsigned)q) << k;
+    }
+    return (int)key;
+}
+
+__global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
+    const int root = a.n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    RootInfo ri;
+    root_info(a.nodes4, root, ri);
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < a.n_r; i += gridDim.x * 256ll) {
+        float s[3], e[3];
+        const int bin = seg_bin(a.starts, a.ends, i, a.nodes4, root, ri, s, e);
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, bin);
+        if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
+            atomicAdd(a.bins + bin, __popc(peers));
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_bin_scan(SortedArgs a) {
+    __shared__ unsigned warp_tot[32];
+    constexpr int per = kBins / 1024;
+    const int base = threadIdx.x * per;
+    const uint4* b4 = reinterpret_cast<const uint4*>(a.bins + base);
+    unsigned sum = 0;
+    for (int k = 0; k < per / 4; ++k) {
+        const uint4 v = b4[k];
+        sum += v.x + v.y + v.z + v.w;
+    }
+    // block exclusive scan of the per-thread sums
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned t = warp_tot[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(kFullMask, t, o);
+            if (lane >= o) t += y;
+        }
+        warp_tot[lane] = t;
+    }
+    __syncthreads();
+    unsigned run = x - sum + (w ? warp_tot[w - 1] : 0u);
+    uint4* c4 = reinterpret_cast<uint4*>(a.cursor + base);
+    for (int k = 0; k < per / 4; ++k) {
+        const uint4 v = b4[k];
+        uint4 o;
+        o.x = run; run += v.x;
+        o.y = run; run += v.y;
+        o.z = run; run += v.z;
+        o.w = run; run += v.w;
+        c4[k] = o;
+    }
+    if (threadIdx.x == 1023) *a.n_live = run;
+}
+
+__global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
+    const int root = a.n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    RootInfo ri;
+    root_info(a.nodes4, root, ri);
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < a.n_r; i += gridDim.x * 256ll) {
+        float s[3], e[3];
+        const int bin = seg_bin(a.starts, a.ends, i, a.nodes4, root, ri, s, e);
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, bin);
+        const int leader = __ffs(peers) - 1;
+        unsigned pos = 0;
+        if (bin >= 0 && leader == (int)(threadIdx.x & 31)) pos = atomicAdd(a.cursor + bin, __popc(peers));
+        pos = __shfl_sync(peers, pos, leader);
+        if (bin < 0) continue;
+        pos += __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
+        a.rec[2 * pos] = make_float4(s[0], s[1], s[2], __int_as_float((int)i));
+        a.rec[2 * pos + 1] = make_float4(e[0], e[1], e[2], 0.f);
+    }
+}
+
+template <int MODE, bool STATS>
+__global__ void __launch_bounds__(kSortedThreads) k_trav_sorted(SortedArgs a) {
+    const unsigned n_live = *a.n_live;
+    const int n_int = a.n_int;
+    const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    unsigned long long visits = 0, mts = 0;
+    int stack[kSortedStack];
+    for (unsigned idx = blockIdx.x * kSortedThreads + threadIdx.x; idx < n_live;
+         idx += gridDim.x * kSortedThreads) {
+        const float4 r0 = a.rec[2 * idx], r1 = a.rec[2 * idx + 1];
+        const int id = __float_as_int(r0.w);
+        float b[6];
+        b[0] = fminf(r0.x, r1.x); b[1] = fmaxf(r0.x, r1.x);
+        b[2] = fminf(r0.y, r1.y); b[3] = fmaxf(r0.y, r1.y);
+        b[4] = fminf(r0.z, r1.z); b[5] = fmaxf(r0.z, r1.z);
+        const double sx = r0.x, sy = r0.y, sz = r0.z;
+        const double dx = __dsub_rn((double)r1.x, sx), dy = __dsub_rn((double)r1.y, sy),
+                     dz = __dsub_rn((double)r1.z, sz);
+        int det = 0, nh = 0, btri = -1;
+        double bt = 0.0;
+        int top = 0, node = root;
+        bool ovf = false;
+        for (;;) {
+            if (STATS) ++visits;
+            int next = -1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float f[8];
+                ld_slot(&a.nodes4[node].s[j], f);
+                if (!slot_hit(f, b)) continue;
+                const int ref = __float_as_int(f[6]);
+                if (ref >= n_int) {  // leaf: exact test (_core.pyx:304-320)
+                    const RsLeaf* L = a.leaves + (ref - n_int);
+                    const float4 p0 = __ldg(&L->p0), p1 = __ldg(&L->p1), p2 = __ldg(&L->p2);
+                    double t;
+                    if (STATS) ++mts;
+                    if (mt_hit(p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, p2.x, sx, sy, sz, dx,
+                               dy, dz, &t)) {
+                        const int tid = __float_as_int(p2.y);
+                        det = 1;
+                        ++nh;
+                        if (MODE == kBarycentric &&
+                            (btri < 0 || t < bt || (t == bt && tid < btri))) {
+                            bt = t;
+                            btri = tid;
+                        }
+                    }
+                } else if (next < 0) {
+                    next = ref;
+                } else if (top < kSortedStack) {
+                    stack[top++] = ref;
+                } else {
+                    ovf = true;
+                }
+            }
+            if (MODE == kBoolean && det) break;
+            if (next >= 0) {
+                node = next;
+            } else if (top > 0) {
+                node = stack[--top];
+            } else {
+                break;
+            }
+        }
+        if (ovf) atomicAdd(&a.status->internal, 1ull);
+        if (MODE == kBoolean) {
+            if (det) a.flags[id] = 1;
+        } else if (MODE == kCount) {
+            if (nh) a.flags[id] = nh;
+        } else if (btri >= 0) {
+            a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
+            a.best_tri[id] = btri;
+        }
+    }
+    if (STATS) {
+        for (int o = 16; o; o >>= 1) {
+            visits += __shfl_xor_sync(kFullMask, visits, o);
+            mts += __shfl_xor_sync(kFullMask, mts, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&a.status->visits, visits);
+            atomicAdd(&a.status->mts, mts);
+        }
+    }
+}
+
+// ------------------------------------------------------------ host glue ---
+
+size_t sorted_bins() { return kBins; }
+
+void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
+    if (a.n_r <= 0) return;
+    count_launches(4);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long long want = (a.n_r + 255) / 256;
+    const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
+    k_bin_count<<<g, 256, 0, s>>>(a);
+    k_bin_scan<<<1, 1024, 0, s>>>(a);
+    k_bin_scatter<<<g, 256, 0, s>>>(a);
+    const long long wt = (a.n_r + kSortedThreads - 1) / kSortedThreads;
+    const unsigned gt = (unsigned)(wt < sms * 64ll ? wt : sms * 64ll);
+    if (mode == kBoolean) {
+        if (stats) k_trav_sorted<kBoolean, true><<<gt, kSortedThreads, 0, s>>>(a);
+        else k_trav_sorted<kBoolean, false><<<gt, kSortedThreads, 0, s>>>(a);
+    } else if (mode == kCount) {
+        if (stats) k_trav_sorted<kCount, true><<<gt, kSortedThreads, 0, s>>>(a);
+        else k_trav_sorted<kCount, false><<<gt, kSortedThreads, 0, s>>>(a);
+    } else {
+        if (stats) k_trav_sorted<kBarycentric, true><<<gt, kSortedThreads, 0, s>>>(a);
+        else k_trav_sorted<kBarycentric, false><<<gt, kSortedThreads, 0, s>>>(a);
+    }
+}
+
+}  // namespace rs

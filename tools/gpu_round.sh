@@ -22,9 +22,10 @@ for w in $WHAT; do
                    RS_BINARY_FAST=1 timeout 600 python bench.py --presort --no-cpu-baseline --no-e2e > "$OUT/bench_presort_binary.json" 2>> "$OUT/bench.err";;
     bench_presort_simple) RS_SIMPLE_QUERY=1 RS_BINARY_FAST=1 timeout 600 python bench.py --presort --no-cpu-baseline --no-e2e > "$OUT/bench_presort_simple.json" 2>> "$OUT/bench.err";
                    RS_SIMPLE_QUERY=1 RS_BINARY_FAST=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_simple.json" 2>> "$OUT/bench.err";;
+    bench_buffer) RS_FAST_PATH=buffer timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_buffer.json" 2>> "$OUT/bench.err";;
     benchq) timeout 600 python bench.py --no-cpu-baseline > "$OUT/bench.json" 2>> "$OUT/bench.err";;
     stats) timeout 300 python tools/stats.py c2 > "$OUT/stats_c2.json" 2>&1;;
-    ncuq) timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_query|k_trav|k_exact' -s 3 -c 2 \
+    ncuq) timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_query|k_trav|k_exact|k_bin' -s 6 -c 5 \
         -o "$OUT/query" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_full.log" 2>&1;;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
