@@ -378,7 +378,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         total += align256(8ull * n_r) + align256(4ull * n_r) + align256(8ull * cap) +
                  align256(bary_compact_scratch(n_r));
     if (g_buffer_path) total += align256(4 * trav_gstack_ints());
-    total += 2 * align256(4 * sorted_bins()) + align256(4 * 64) + align256(32ull * n_r);
+    total += 3 * align256(4 * sorted_bins()) + align256(4 * 64) + align256(32ull * n_r);
     CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
@@ -393,7 +393,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         f.tiles_bytes = bary_compact_scratch(n_r);
     }
     if (g_buffer_path) f.gstack = c.take<int>(trav_gstack_ints());
-    f.bins = c.take<unsigned>(sorted_bins());
+    f.bins = c.take<unsigned>(2 * sorted_bins());  // counters + look-back words (zeroed together)
     f.cursor = c.take<unsigned>(sorted_bins());
     f.n_live = c.take<unsigned>(64);
     f.rec = c.take<float4>(2ull * n_r);
@@ -420,9 +420,11 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
                      o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
         launch_exact(ea, mode, stats, s);
     } else {
-        CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins(), s));
+        CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 8 * (sorted_bins() / 1024), s));
         SortedArgs sa{t->nodes4, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.bins,
-                      f.cursor, f.n_live, f.rec, o.flags, f.best_t, f.best_tri, f.st};
+                      f.cursor, f.n_live,
+                      reinterpret_cast<unsigned long long*>(f.bins + sorted_bins()), f.rec,
+                      o.flags, f.best_t, f.best_tri, f.st};
         launch_sorted(sa, mode, stats, s);
     }
     if (bary) {

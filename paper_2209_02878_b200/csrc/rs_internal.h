@@ -142,6 +142,7 @@ struct SortedArgs {
     unsigned* bins;      // sorted_bins() counters (zeroed)
     unsigned* cursor;    // sorted_bins() scatter cursors
     unsigned* n_live;    // live segment count (written by the scan)
+    unsigned long long* scan_status;  // sorted_bins()/1024 look-back words (zeroed)
     float4* rec;         // n_r x 32-B records (start, id, end)
     int* flags;                  // boolean / count output (pre-zeroed)
     unsigned long long* best_t;  // barycentric (pre-set ~0)

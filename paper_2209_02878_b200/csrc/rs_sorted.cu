@@ -120,17 +120,17 @@ __global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
     }
 }
 
-__global__ void __launch_bounds__(1024) k_bin_scan(SortedArgs a) {
-    __shared__ unsigned warp_tot[32];
-    constexpr int per = kBins / 1024;
-    const int base = threadIdx.x * per;
-    const uint4* b4 = reinterpret_cast<const uint4*>(a.bins + base);
-    unsigned sum = 0;
-    for (int k = 0; k < per / 4; ++k) {
-        const uint4 v = b4[k];
-        sum += v.x + v.y + v.z + v.w;
-    }
-    // block exclusive scan of the per-thread sums
+// Exclusive scan of the bin counters: one CTA per 1024 bins, chained with a
+// decoupled look-back (status words in scan_status, zeroed with the bins).
+constexpr int kScanTile = 1024;
+
+__global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
+    __shared__ unsigned warp_tot[8];
+    __shared__ unsigned s_prefix;
+    const int tile = blockIdx.x;
+    const int base = tile * kScanTile + threadIdx.x * 4;
+    const uint4 v = *reinterpret_cast<const uint4*>(a.bins + base);
+    const unsigned sum = v.x + v.y + v.z + v.w;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned x = sum;
     for (int o = 1; o < 32; o <<= 1) {
@@ -139,27 +139,43 @@ __global__ void __launch_bounds__(1024) k_bin_scan(SortedArgs a) {
     }
     if (lane == 31) warp_tot[w] = x;
     __syncthreads();
-    if (w == 0) {
-        unsigned t = warp_tot[lane];
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(kFullMask, t, o);
-            if (lane >= o) t += y;
+    if (threadIdx.x == 0) {
+        unsigned agg = 0;
+        for (int k = 0; k < 8; ++k) {
+            const unsigned c = warp_tot[k];
+            warp_tot[k] = agg;
+            agg += c;
         }
-        warp_tot[lane] = t;
+        unsigned long long excl = 0;
+        volatile unsigned long long* st = a.scan_status;
+        if (tile == 0) {
+            __threadfence();
+            st[0] = (2ull << 62) | agg;
+        } else {
+            __threadfence();
+            st[tile] = (1ull << 62) | agg;
+            for (int j = tile - 1; j >= 0;) {
+                const unsigned long long sv = st[j];
+                const unsigned flag = (unsigned)(sv >> 62);
+                if (flag == 0) continue;
+                excl += sv & ((1ull << 62) - 1);
+                if (flag == 2) break;
+                --j;
+            }
+            __threadfence();
+            st[tile] = (2ull << 62) | (excl + agg);
+        }
+        s_prefix = (unsigned)excl;
+        if (tile == gridDim.x - 1) *a.n_live = (unsigned)(excl + agg);
     }
     __syncthreads();
-    unsigned run = x - sum + (w ? warp_tot[w - 1] : 0u);
-    uint4* c4 = reinterpret_cast<uint4*>(a.cursor + base);
-    for (int k = 0; k < per / 4; ++k) {
-        const uint4 v = b4[k];
-        uint4 o;
-        o.x = run; run += v.x;
-        o.y = run; run += v.y;
-        o.z = run; run += v.z;
-        o.w = run; run += v.w;
-        c4[k] = o;
-    }
-    if (threadIdx.x == 1023) *a.n_live = run;
+    unsigned run = s_prefix + warp_tot[w] + x - sum;
+    uint4 o;
+    o.x = run; run += v.x;
+    o.y = run; run += v.y;
+    o.z = run; run += v.z;
+    o.w = run;
+    *reinterpret_cast<uint4*>(a.cursor + base) = o;
 }
 
 __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
@@ -189,8 +205,13 @@ __global__ void __launch_bounds__(kSortedThreads) k_trav_sorted(SortedArgs a) {
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
     unsigned long long visits = 0, mts = 0;
     int stack[kSortedStack];
-    for (unsigned idx = blockIdx.x * kSortedThreads + threadIdx.x; idx < n_live;
-         idx += gridDim.x * kSortedThreads) {
+    // each CTA walks one contiguous run of records (one spatial region), so
+    // the subtree it touches stays resident in its SM's L1
+    const unsigned per_cta = ((n_live + gridDim.x - 1) / gridDim.x + kSortedThreads - 1) /
+                             kSortedThreads * kSortedThreads;
+    const unsigned beg = blockIdx.x * per_cta;
+    const unsigned end = beg + per_cta < n_live ? beg + per_cta : n_live;
+    for (unsigned idx = beg + threadIdx.x; idx < end; idx += kSortedThreads) {
         const float4 r0 = a.rec[2 * idx], r1 = a.rec[2 * idx + 1];
         const int id = __float_as_int(r0.w);
         float b[6];
@@ -284,10 +305,19 @@ void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
     const long long want = (a.n_r + 255) / 256;
     const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
     k_bin_count<<<g, 256, 0, s>>>(a);
-    k_bin_scan<<<1, 1024, 0, s>>>(a);
+    k_bin_scan<<<kBins / kScanTile, 256, 0, s>>>(a);
     k_bin_scatter<<<g, 256, 0, s>>>(a);
+    static int occ[3] = {0, 0, 0};
+    int& o = occ[mode];
+    if (!o) {
+        const void* k = mode == kBoolean ? (const void*)k_trav_sorted<kBoolean, false>
+                        : mode == kCount ? (const void*)k_trav_sorted<kCount, false>
+                                         : (const void*)k_trav_sorted<kBarycentric, false>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kSortedThreads, 0);
+        if (o < 1) o = 1;
+    }
     const long long wt = (a.n_r + kSortedThreads - 1) / kSortedThreads;
-    const unsigned gt = (unsigned)(wt < sms * 64ll ? wt : sms * 64ll);
+    const unsigned gt = (unsigned)(wt < (long long)sms * o ? wt : (long long)sms * o);
     if (mode == kBoolean) {
         if (stats) k_trav_sorted<kBoolean, true><<<gt, kSortedThreads, 0, s>>>(a);
         else k_trav_sorted<kBoolean, false><<<gt, kSortedThreads, 0, s>>>(a);
