@@ -421,7 +421,7 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
         launch_exact(ea, mode, stats, s);
     } else {
         CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 8 * (sorted_bins() / 1024), s));
-        SortedArgs sa{t->nodes4, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.bins,
+        SortedArgs sa{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.bins,
                       f.cursor, f.n_live,
                       reinterpret_cast<unsigned long long*>(f.bins + sorted_bins()), f.rec,
                       o.flags, f.best_t, f.best_tri, f.st};

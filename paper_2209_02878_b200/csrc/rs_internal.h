@@ -133,6 +133,7 @@ void launch_trav(const TravArgs& a, bool stats, cudaStream_t s);
 // bins, then one thread per segment in bin order.
 struct SortedArgs {
     const RsNode4* nodes4;
+    const RsNode* nodes;
     const RsLeaf* leaves;
     const RsHeader* hdr;
     int n_int;

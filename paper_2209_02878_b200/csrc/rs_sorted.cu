@@ -25,6 +25,8 @@
 #include "rs_common.cuh"
 #include "rs_internal.h"
 
+#include <cstdlib>
+
 namespace rs {
 
 constexpr unsigned kFullMask = 0xffffffffu;
@@ -289,6 +291,94 @@ __global__ void __launch_bounds__(kSortedThreads) k_trav_sorted(SortedArgs a) {
     }
 }
 
+// Binary-node variant (A/B: RS_SORTED_BINARY=1): the same coherent order over
+// the 64-B RsNode records (two 256-bit loads per visit).
+template <int MODE>
+__global__ void __launch_bounds__(kSortedThreads) k_trav_sorted_bin(SortedArgs a) {
+    const unsigned n_live = *a.n_live;
+    const int n_int = a.n_int;
+    const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    int stack[kSortedStack];
+    const unsigned per_cta = ((n_live + gridDim.x - 1) / gridDim.x + kSortedThreads - 1) /
+                             kSortedThreads * kSortedThreads;
+    const unsigned beg = blockIdx.x * per_cta;
+    const unsigned end = beg + per_cta < n_live ? beg + per_cta : n_live;
+    for (unsigned idx = beg + threadIdx.x; idx < end; idx += kSortedThreads) {
+        const float4 r0 = a.rec[2 * idx], r1 = a.rec[2 * idx + 1];
+        const int id = __float_as_int(r0.w);
+        float b[6];
+        b[0] = fminf(r0.x, r1.x); b[1] = fmaxf(r0.x, r1.x);
+        b[2] = fminf(r0.y, r1.y); b[3] = fmaxf(r0.y, r1.y);
+        b[4] = fminf(r0.z, r1.z); b[5] = fmaxf(r0.z, r1.z);
+        const double sx = r0.x, sy = r0.y, sz = r0.z;
+        const double dx = __dsub_rn((double)r1.x, sx), dy = __dsub_rn((double)r1.y, sy),
+                     dz = __dsub_rn((double)r1.z, sz);
+        int det = 0, nh = 0, btri = -1;
+        double bt = 0.0;
+        int top = 0, node = root;
+        bool ovf = false;
+        auto leaf_test = [&](int leaf) {
+            const RsLeaf* L = a.leaves + leaf;
+            const float4 p0 = __ldg(&L->p0), p1 = __ldg(&L->p1), p2 = __ldg(&L->p2);
+            double t;
+            if (mt_hit(p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, p2.x, sx, sy, sz, dx, dy, dz, &t)) {
+                const int tid = __float_as_int(p2.y);
+                det = 1;
+                ++nh;
+                if (MODE == kBarycentric && (btri < 0 || t < bt || (t == bt && tid < btri))) {
+                    bt = t;
+                    btri = tid;
+                }
+            }
+        };
+        if (n_int == 0) {  // single triangle: the leaf's box is slot 0 of nodes4[0]
+            float f[8];
+            ld_slot(&a.nodes4[0].s[0], f);
+            if (slot_hit(f, b)) leaf_test(0);
+        } else {
+            for (;;) {
+                float f0[8], f1[8];
+                const RsSlot* np = reinterpret_cast<const RsSlot*>(a.nodes + node);
+                ld_slot(np, f0);
+                ld_slot(np + 1, f1);
+                // RsNode: [l.x0 l.x1 l.y0 l.y1 l.z0 l.z1 r.x0 r.x1] [r.y0 r.y1 r.z0 r.z1 lref rref - -]
+                const int ca = __float_as_int(f1[4]), cb = __float_as_int(f1[5]);
+                const bool oa = (b[0] <= f0[1]) & (b[1] >= f0[0]) & (b[2] <= f0[3]) & (b[3] >= f0[2]) &
+                                (b[4] <= f0[5]) & (b[5] >= f0[4]);
+                const bool ob = (b[0] <= f0[7]) & (b[1] >= f0[6]) & (b[2] <= f1[1]) & (b[3] >= f1[0]) &
+                                (b[4] <= f1[3]) & (b[5] >= f1[2]);
+                const bool la = ca >= n_int, lb = cb >= n_int;
+                if (oa & la) leaf_test(ca - n_int);
+                if (ob & lb) leaf_test(cb - n_int);
+                if (MODE == kBoolean && det) break;
+                const bool ta = oa & !la, tb = ob & !lb;
+                if (ta) {
+                    node = ca;
+                    if (tb) {
+                        if (top < kSortedStack) stack[top++] = cb;
+                        else ovf = true;
+                    }
+                } else if (tb) {
+                    node = cb;
+                } else if (top > 0) {
+                    node = stack[--top];
+                } else {
+                    break;
+                }
+            }
+        }
+        if (ovf) atomicAdd(&a.status->internal, 1ull);
+        if (MODE == kBoolean) {
+            if (det) a.flags[id] = 1;
+        } else if (MODE == kCount) {
+            if (nh) a.flags[id] = nh;
+        } else if (btri >= 0) {
+            a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
+            a.best_tri[id] = btri;
+        }
+    }
+}
+
 // ------------------------------------------------------------ host glue ---
 
 size_t sorted_bins() { return kBins; }
@@ -318,6 +408,16 @@ void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
     }
     const long long wt = (a.n_r + kSortedThreads - 1) / kSortedThreads;
     const unsigned gt = (unsigned)(wt < (long long)sms * o ? wt : (long long)sms * o);
+    static const bool bin_nodes = [] {
+        const char* e = getenv("RS_SORTED_BINARY");
+        return e && e[0] == '1';
+    }();
+    if (bin_nodes && !stats) {
+        if (mode == kBoolean) k_trav_sorted_bin<kBoolean><<<gt, kSortedThreads, 0, s>>>(a);
+        else if (mode == kCount) k_trav_sorted_bin<kCount><<<gt, kSortedThreads, 0, s>>>(a);
+        else k_trav_sorted_bin<kBarycentric><<<gt, kSortedThreads, 0, s>>>(a);
+        return;
+    }
     if (mode == kBoolean) {
         if (stats) k_trav_sorted<kBoolean, true><<<gt, kSortedThreads, 0, s>>>(a);
         else k_trav_sorted<kBoolean, false><<<gt, kSortedThreads, 0, s>>>(a);
