@@ -30,7 +30,7 @@
 namespace rs {
 
 constexpr unsigned kFullMask = 0xffffffffu;
-constexpr int kAxisBits = 6;                 // bins per axis = 64
+constexpr int kAxisBits = 7;                 // bins per axis = 128
 constexpr int kBinBits = 3 * kAxisBits;
 constexpr int kBins = 1 << kBinBits;
 constexpr int kSortedThreads = 128;
