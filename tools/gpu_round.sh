@@ -30,10 +30,10 @@ for w in $WHAT; do
         -o "$OUT/query" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_full.log" 2>&1;;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
-      timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+      timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_bench.log" 2>&1
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_query|k_trav|k_exact' -s 3 -c 2 \
-        -o "$OUT/query" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_full.log" 2>&1;;
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_|onesweep' -s 40 -c 20 \
+        -o "$OUT/full" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_full.log" 2>&1;;
   esac
 done
 ls -la "$OUT"
