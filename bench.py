@@ -85,7 +85,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -177,7 +177,7 @@ def run_reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--config", default="c2", choices=tuple(CONFIGS))
@@ -241,8 +241,8 @@ def main():
     else:
         assert np.array_equal(res.ray_index.cpu().numpy(), np.nonzero(truth)[0])
 
-    build_ms, query_ms = [], []
-    bms, qms = C.c_float(), C.c_float()
+    build_ms, query_ms, hot_ms = [], [], []
+    bms, qms, hms = C.c_float(), C.c_float(), C.c_float()
     stream = torch.cuda.current_stream()
     if world > 1:
         dist.barrier()
@@ -254,9 +254,10 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             step()
-            lib.rs_last_timings(C.byref(bms), C.byref(qms))
+            lib.rs_last_timings(C.byref(bms), C.byref(qms), C.byref(hms))
             build_ms.append(bms.value)
             query_ms.append(qms.value)
+            hot_ms.append(hms.value)
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = lib.rs_kernel_launches() - launches0
@@ -294,10 +295,12 @@ def main():
                "ms_per_step": round(1e3 * e2e_t.item(), 3),
                "path": "run_batch(numpy pinned) -> rs_run_batch_host: chunked H2D/query/D2H"}
 
-    # roofline of the dominant kernel (the query): compulsory bytes per segment
+    # roofline of the dominant kernel (the traversal): SURVEY 8(d) compulsory
+    # bytes per segment x segments per launch / its CUDA-event duration
     b_ray = 24 + (4 if mode != "barycentric" else 24 * 0.5)
     q_ms = float(np.mean(query_ms))
-    achieved = b_ray * n / (q_ms / 1e3) / 1e9
+    h_ms = float(np.mean(hot_ms)) if hot_ms and min(hot_ms) > 0 else q_ms
+    achieved = b_ray * n / (h_ms / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
     traffic = None
     tf = REPO / "profiles" / f"traffic_{cfg}.json"
@@ -312,10 +315,11 @@ def main():
         "config": {"workload": desc, "mode": mode, "n_triangles": mesh_h.num_triangles,
                    "segments_per_gpu": n, "tree": kind, "l2": "inputs (240 MB) larger than L2",
                    "parallelism": f"ray shards x{world}, mesh/BVH replicated"},
-        "phase_ms": {"build": round(float(np.mean(build_ms)), 4), "query": round(q_ms, 4)},
+        "phase_ms": {"build": round(float(np.mean(build_ms)), 4), "query": round(q_ms, 4),
+                     "traversal_kernel": round(h_ms, 4)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "k_query_dense", "peak_kind": peak_kind,
+                     "kernel": "k_trav_sorted_bin", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_segment": b_ray},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),

@@ -146,10 +146,11 @@ RS_API int rs_run_batch_host(const float *h_verts, int64_t n_v, const int32_t *h
 
 /* Device phase timing for rs_run_batch_device (the reference's
  * ResultSet.timings "construct"/"query", engine.py:238-288): when enabled,
- * CUDA events on the caller's stream bracket the build and the query kernel;
- * rs_last_timings returns the last call's milliseconds. */
+ * CUDA events on the caller's stream bracket the build, the whole query and
+ * the dominant (traversal) kernel; rs_last_timings returns the last call's
+ * milliseconds. */
 RS_API int rs_set_timing(int enable);
-RS_API int rs_last_timings(float *build_ms, float *query_ms);
+RS_API int rs_last_timings(float *build_ms, float *query_ms, float *hot_kernel_ms);
 
 /* Cumulative number of kernels this library has launched. */
 RS_API long long rs_kernel_launches(void);

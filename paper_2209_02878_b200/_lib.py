@@ -39,7 +39,7 @@ _SIGS = {
     "rs_run_batch_host": (i32, [p, i64, p, i64, p, p, i64, i32, i32, i32, i32, i64,
                                 p, p, p, p, p, p, p, p]),
     "rs_set_timing": (i32, [i32]),
-    "rs_last_timings": (i32, [p, p]),
+    "rs_last_timings": (i32, [p, p, p]),
     "rs_kernel_launches": (C.c_longlong, []),
 }
 

@@ -162,8 +162,24 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const unsigned* __restrict__ ghist, unsigned long long* status, unsigned* tile_counter) {
     __shared__ unsigned warp_cnt[kSortWarps][256];
     __shared__ unsigned long long gbase[256];
+    __shared__ unsigned wsum[kSortWarps];
     __shared__ int s_tile;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    // exclusive scan of this pass's global digit histogram (digit = thread)
+    unsigned dig_excl;
+    {
+        const unsigned hv = ghist[threadIdx.x];
+        unsigned x = hv;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        if (l == 31) wsum[w] = x;
+        __syncthreads();
+        unsigned before = 0;
+        for (int i = 0; i < w; ++i) before += wsum[i];
+        dig_excl = before + x - hv;
+    }
     for (int i = threadIdx.x; i < kSortWarps * 256; i += blockDim.x) (&warp_cnt[0][0])[i] = 0;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
     __syncthreads();
@@ -224,10 +240,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
             }
             me.store((2ull << 62) | (excl + tot), cuda::memory_order_release);
         }
-        // exclusive global digit base: sum of ghist[< d] + tiles before us
-        unsigned long long gb = 0;
-        for (int i = 0; i < d; ++i) gb += ghist[i];
-        gbase[d] = gb + excl;
+        // exclusive global digit base: keys with smaller digits + tiles before us
+        gbase[d] = (unsigned long long)dig_excl + excl;
     }
     __syncthreads();
 #pragma unroll

@@ -16,6 +16,7 @@
 using namespace rs;
 
 namespace rs {
+void hot_kernel_mark(int which, cudaStream_t s);
 static std::atomic<long long> g_launches{0};
 void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 }  // namespace rs
@@ -44,8 +45,8 @@ const bool g_binary_fast = [] {
 // Phase timing (engine.py's timings dict, measured on device): when enabled,
 // events bracket the build and the query kernel on the caller's stream.
 thread_local bool g_timing = false;
-thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
-thread_local float g_build_ms = 0.f, g_query_ms = 0.f;
+thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+thread_local float g_build_ms = 0.f, g_query_ms = 0.f, g_hot_ms = 0.f;
 thread_local bool g_ev_valid = false;
 
 void ev_record(int k, cudaStream_t s) {
@@ -250,8 +251,8 @@ int status_code(const RsStatus& h, int64_t* bad_segment) {
 // Per-thread cached pipeline resources for rs_run_batch_host.
 struct Pipe {
     int device = -1;
-    cudaStream_t copy = nullptr;
-    cudaEvent_t ev_in[2], ev_q[2], ev_out[2];
+    cudaStream_t copy = nullptr, copy2 = nullptr;  // starts / ends H2D on two DMA queues
+    cudaEvent_t ev_in[2], ev_in2[2], ev_q[2], ev_out[2];
 };
 thread_local Pipe g_pipe;
 
@@ -260,8 +261,10 @@ int pipe_init() {
     CK(cudaGetDevice(&dev));
     if (g_pipe.device == dev) return RS_OK;
     CK(cudaStreamCreateWithFlags(&g_pipe.copy, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g_pipe.copy2, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
         CK(cudaEventCreateWithFlags(&g_pipe.ev_in[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g_pipe.ev_in2[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g_pipe.ev_q[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g_pipe.ev_out[k], cudaEventDisableTiming));
     }
@@ -420,10 +423,9 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
                      o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
         launch_exact(ea, mode, stats, s);
     } else {
-        CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 8 * (sorted_bins() / 1024), s));
+        CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 4 * (sorted_bins() / 1024), s));
         SortedArgs sa{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.bins,
-                      f.cursor, f.n_live,
-                      reinterpret_cast<unsigned long long*>(f.bins + sorted_bins()), f.rec,
+                      f.cursor, f.n_live, f.bins + sorted_bins(), f.rec,
                       o.flags, f.best_t, f.best_tri, f.st};
         launch_sorted(sa, mode, stats, s);
     }
@@ -622,6 +624,8 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
     if (g_timing && !rc) {
         cudaEventElapsedTime(&g_build_ms, g_ev[0], g_ev[1]);
         cudaEventElapsedTime(&g_query_ms, g_ev[1], g_ev[2]);
+        g_hot_ms = 0.f;
+        if (g_ev[3] && g_ev[4]) cudaEventElapsedTime(&g_hot_ms, g_ev[3], g_ev[4]);
         g_ev_valid = true;
     }
     return rc ? rc : rc2;
@@ -633,14 +637,21 @@ RS_API int rs_set_timing(int enable) {
     return RS_OK;
 }
 
-RS_API int rs_last_timings(float* build_ms, float* query_ms) {
+RS_API int rs_last_timings(float* build_ms, float* query_ms, float* hot_ms) {
     if (!g_ev_valid) return fail(RS_INVALID_ARG, "no timed rs_run_batch_device call yet");
     if (build_ms) *build_ms = g_build_ms;
     if (query_ms) *query_ms = g_query_ms;
+    if (hot_ms) *hot_ms = g_hot_ms;
     return RS_OK;
 }
 
 RS_API long long rs_kernel_launches(void) { return g_launches.load(); }
+
+}  // extern "C"
+
+void rs::hot_kernel_mark(int which, cudaStream_t s) { ev_record(3 + which, s); }
+
+extern "C" {
 
 int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, int64_t n_t,
                       const float* h_starts, const float* h_ends, int64_t n_r, int mode,
@@ -719,16 +730,23 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     // The copy stream must see the memset/mesh copies ordered before chunk 0.
     CK(cudaEventRecord(g_pipe.ev_q[1], s));
     CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[1], 0));
+    CK(cudaStreamWaitEvent(g_pipe.copy2, g_pipe.ev_q[1], 0));
     unsigned long long running = 0;  // barycentric rows already placed
     for (int64_t k = 0; k < nchunks; ++k) {
         const int b = (int)(k & 1);
         const int64_t lo = k * chunk_rays;
         const int64_t cnt = (lo + chunk_rays <= n_r) ? chunk_rays : n_r - lo;
-        if (k >= 2) CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));  // buffer b free again
+        if (k >= 2) {  // buffer b free again
+            CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));
+            CK(cudaStreamWaitEvent(g_pipe.copy2, g_pipe.ev_q[b], 0));
+        }
         CK(cudaMemcpyAsync(din[b][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, cp));
-        CK(cudaMemcpyAsync(din[b][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, cp));
+        CK(cudaMemcpyAsync(din[b][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice,
+                           g_pipe.copy2));
         CK(cudaEventRecord(g_pipe.ev_in[b], cp));
+        CK(cudaEventRecord(g_pipe.ev_in2[b], g_pipe.copy2));
         CK(cudaStreamWaitEvent(s, g_pipe.ev_in[b], 0));
+        CK(cudaStreamWaitEvent(s, g_pipe.ev_in2[b], 0));
         if (k >= 2 && !bary) CK(cudaStreamWaitEvent(s, g_pipe.ev_out[b], 0));
         if (fast) {
             fs[b].st = st + k;

@@ -9,6 +9,8 @@ namespace rs {
 
 // Number of kernels this library has launched (bench.py's gpu_launches).
 void count_launches(long long k);
+// Device timing of the dominant kernel (bench.py roofline): 0 before, 1 after.
+void hot_kernel_mark(int which, cudaStream_t s);
 
 // The reference BvhTree SoA fields (lbvh.py:39-55) plus climb scratch.
 struct TreeArrays {
@@ -143,7 +145,7 @@ struct SortedArgs {
     unsigned* bins;      // sorted_bins() counters (zeroed)
     unsigned* cursor;    // sorted_bins() scatter cursors
     unsigned* n_live;    // live segment count (written by the scan)
-    unsigned long long* scan_status;  // sorted_bins()/1024 look-back words (zeroed)
+    unsigned* tile_sum;  // sorted_bins()/1024 per-tile counts (zeroed) -> tile offsets
     float4* rec;         // n_r x 32-B records (start, id, end)
     int* flags;                  // boolean / count output (pre-zeroed)
     unsigned long long* best_t;  // barycentric (pre-set ~0)

@@ -8,9 +8,10 @@
 //   k_bin_count    per segment: f32 AABB (engine.py:115-122), test against the
 //                  root's children (a segment overlapping none of them has no
 //                  candidates: its result is the pre-zeroed default and it is
-//                  dropped here), 16-bit isotropic Morton key of the box centre
+//                  dropped here), 21-bit isotropic Morton key of the box centre
 //                  over the root box, warp-aggregated histogram atomics.
-//   k_bin_scan     exclusive scan of the 65,536 bins (one CTA).
+//   k_tile_scan +  two-level exclusive scan of the 2M bins.
+//   k_bin_scan
 //   k_bin_scatter  same key; each live segment's record (start, id, end; 32 B)
 //                  goes to its bin.
 //   k_trav_sorted  one thread per record, in bin order: stack traversal of the
@@ -25,6 +26,7 @@
 #include "rs_common.cuh"
 #include "rs_internal.h"
 
+#include <cstdint>
 #include <cstdlib>
 
 namespace rs {
@@ -33,6 +35,9 @@ constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kAxisBits = 7;                 // bins per axis = 128
 constexpr int kBinBits = 3 * kAxisBits;
 constexpr int kBins = 1 << kBinBits;
+constexpr int kScanShift = 10;
+constexpr int kScanTile = 1 << kScanShift;
+constexpr int kScanTiles = kBins / kScanTile;
 constexpr int kSortedThreads = 128;
 constexpr int kSortedStack = 64;  // fast tree: <= 3 pending per 4-wide level; deeper -> fallback
 
@@ -81,11 +86,8 @@ __device__ __forceinline__ void root_info(const RsNode4* nodes4, int root, RootI
 }
 
 // Returns the bin of a live segment, or -1 when it overlaps no root child.
-__device__ __forceinline__ int seg_bin(const float* __restrict__ S, const float* __restrict__ E,
-                                       long long i, const RsNode4* nodes4, int root,
-                                       const RootInfo& ri, float s[3], float e[3]) {
-    s[0] = __ldg(S + 3 * i); s[1] = __ldg(S + 3 * i + 1); s[2] = __ldg(S + 3 * i + 2);
-    e[0] = __ldg(E + 3 * i); e[1] = __ldg(E + 3 * i + 1); e[2] = __ldg(E + 3 * i + 2);
+__device__ __forceinline__ int seg_bin(const float s[3], const float e[3], const RsNode4* nodes4,
+                                       int root, const RootInfo& ri) {
     float b[6];
     b[0] = fminf(s[0], e[0]); b[1] = fmaxf(s[0], e[0]);
     b[2] = fminf(s[1], e[1]); b[3] = fmaxf(s[1], e[1]);
@@ -108,70 +110,112 @@ __device__ __forceinline__ int seg_bin(const float* __restrict__ S, const float*
     return (int)key;
 }
 
+// Four consecutive segments per thread: 3 x 16-B loads per endpoint array
+// (the (N,3) f32 AoS rows of segments 4t..4t+3 are 48 contiguous bytes).
+template <bool VEC>
+__device__ __forceinline__ int load4(const float* __restrict__ S, const float* __restrict__ E,
+                                     long long q, long long n, float s[4][3], float e[4][3]) {
+    const long long i0 = 4 * q;
+    const int cnt = n - i0 >= 4 ? 4 : (int)(n - i0);
+    if (VEC && cnt == 4) {
+        const float4* s4 = reinterpret_cast<const float4*>(S + 3 * i0);
+        const float4* e4 = reinterpret_cast<const float4*>(E + 3 * i0);
+        float fs[12], fe[12];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float4 a = __ldg(s4 + k), c = __ldg(e4 + k);
+            fs[4 * k] = a.x; fs[4 * k + 1] = a.y; fs[4 * k + 2] = a.z; fs[4 * k + 3] = a.w;
+            fe[4 * k] = c.x; fe[4 * k + 1] = c.y; fe[4 * k + 2] = c.z; fe[4 * k + 3] = c.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                s[j][k] = fs[3 * j + k];
+                e[j][k] = fe[3 * j + k];
+            }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                s[j][k] = j < cnt ? __ldg(S + 3 * (i0 + j) + k) : 0.f;
+                e[j][k] = j < cnt ? __ldg(E + 3 * (i0 + j) + k) : 0.f;
+            }
+    }
+    return cnt;
+}
+
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
     const int root = a.n_int > 0 ? __ldg(&a.hdr->root) : 0;
     RootInfo ri;
     root_info(a.nodes4, root, ri);
-    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < a.n_r; i += gridDim.x * 256ll) {
-        float s[3], e[3];
-        const int bin = seg_bin(a.starts, a.ends, i, a.nodes4, root, ri, s, e);
-        const unsigned act = __activemask();
-        const unsigned peers = __match_any_sync(act, bin);
-        if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
-            atomicAdd(a.bins + bin, __popc(peers));
+    const long long nq = (a.n_r + 3) / 4;
+    for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
+        float s[4][3], e[4][3];
+        const int cnt = load4<VEC>(a.starts, a.ends, q, a.n_r, s, e);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int bin = j < cnt ? seg_bin(s[j], e[j], a.nodes4, root, ri) : -1;
+            const unsigned act = __activemask();
+            const unsigned peers = __match_any_sync(act, bin);
+            if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) {
+                atomicAdd(a.bins + bin, __popc(peers));
+                atomicAdd(a.tile_sum + (bin >> kScanShift), __popc(peers));
+            }
+        }
     }
 }
 
-// Exclusive scan of the bin counters: one CTA per 1024 bins, chained with a
-// decoupled look-back (status words in scan_status, zeroed with the bins).
-constexpr int kScanTile = 1024;
+// Exclusive scan of the bin counters in two levels: k_tile_scan scans the
+// per-1024-bin tile sums (accumulated by k_bin_count) in one CTA, then
+// k_bin_scan scans each tile's bins from its tile offset.
 
-__global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
-    __shared__ unsigned warp_tot[8];
-    __shared__ unsigned s_prefix;
-    const int tile = blockIdx.x;
-    const int base = tile * kScanTile + threadIdx.x * 4;
-    const uint4 v = *reinterpret_cast<const uint4*>(a.bins + base);
-    const unsigned sum = v.x + v.y + v.z + v.w;
+__device__ __forceinline__ unsigned block_excl_scan_256(unsigned v, unsigned* wtot, unsigned* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    unsigned x = sum;
+    unsigned x = v;
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned y = __shfl_up_sync(kFullMask, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) warp_tot[w] = x;
+    if (lane == 31) wtot[w] = x;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned agg = 0;
-        for (int k = 0; k < 8; ++k) {
-            const unsigned c = warp_tot[k];
-            warp_tot[k] = agg;
-            agg += c;
-        }
-        unsigned long long excl = 0;
-        volatile unsigned long long* st = a.scan_status;
-        if (tile == 0) {
-            __threadfence();
-            st[0] = (2ull << 62) | agg;
-        } else {
-            __threadfence();
-            st[tile] = (1ull << 62) | agg;
-            for (int j = tile - 1; j >= 0;) {
-                const unsigned long long sv = st[j];
-                const unsigned flag = (unsigned)(sv >> 62);
-                if (flag == 0) continue;
-                excl += sv & ((1ull << 62) - 1);
-                if (flag == 2) break;
-                --j;
-            }
-            __threadfence();
-            st[tile] = (2ull << 62) | (excl + agg);
-        }
-        s_prefix = (unsigned)excl;
-        if (tile == gridDim.x - 1) *a.n_live = (unsigned)(excl + agg);
+    unsigned before = 0, all = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+        if (k < w) before += wtot[k];
+        all += wtot[k];
     }
-    __syncthreads();
-    unsigned run = s_prefix + warp_tot[w] + x - sum;
+    if (total) *total = all;
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(256) k_tile_scan(SortedArgs a) {
+    __shared__ unsigned wtot[8];
+    constexpr int per = kScanTiles / 256;
+    unsigned v[per], sum = 0;
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+        v[k] = a.tile_sum[threadIdx.x * per + k];
+        sum += v[k];
+    }
+    unsigned total;
+    unsigned run = block_excl_scan_256(sum, wtot, &total);
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+        a.tile_sum[threadIdx.x * per + k] = run;  // becomes the tile offset
+        run += v[k];
+    }
+    if (threadIdx.x == 0) *a.n_live = total;
+}
+
+__global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
+    __shared__ unsigned wtot[8];
+    const int tile = blockIdx.x;
+    const int base = tile * kScanTile + threadIdx.x * 4;
+    const uint4 v = *reinterpret_cast<const uint4*>(a.bins + base);
+    unsigned run = __ldg(a.tile_sum + tile) +
+                   block_excl_scan_256(v.x + v.y + v.z + v.w, wtot, nullptr);
     uint4 o;
     o.x = run; run += v.x;
     o.y = run; run += v.y;
@@ -180,23 +224,31 @@ __global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
     *reinterpret_cast<uint4*>(a.cursor + base) = o;
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
     const int root = a.n_int > 0 ? __ldg(&a.hdr->root) : 0;
     RootInfo ri;
     root_info(a.nodes4, root, ri);
-    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < a.n_r; i += gridDim.x * 256ll) {
-        float s[3], e[3];
-        const int bin = seg_bin(a.starts, a.ends, i, a.nodes4, root, ri, s, e);
-        const unsigned act = __activemask();
-        const unsigned peers = __match_any_sync(act, bin);
-        const int leader = __ffs(peers) - 1;
-        unsigned pos = 0;
-        if (bin >= 0 && leader == (int)(threadIdx.x & 31)) pos = atomicAdd(a.cursor + bin, __popc(peers));
-        pos = __shfl_sync(peers, pos, leader);
-        if (bin < 0) continue;
-        pos += __popc(peers & ((1u << (threadIdx.x & 31)) - 1u));
-        a.rec[2 * pos] = make_float4(s[0], s[1], s[2], __int_as_float((int)i));
-        a.rec[2 * pos + 1] = make_float4(e[0], e[1], e[2], 0.f);
+    const long long nq = (a.n_r + 3) / 4;
+    const int lane = threadIdx.x & 31;
+    for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
+        float s[4][3], e[4][3];
+        const int cnt = load4<VEC>(a.starts, a.ends, q, a.n_r, s, e);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int bin = j < cnt ? seg_bin(s[j], e[j], a.nodes4, root, ri) : -1;
+            const unsigned act = __activemask();
+            const unsigned peers = __match_any_sync(act, bin);
+            const int leader = __ffs(peers) - 1;
+            unsigned pos = 0;
+            if (bin >= 0 && leader == lane) pos = atomicAdd(a.cursor + bin, __popc(peers));
+            pos = __shfl_sync(peers, pos, leader);
+            if (bin < 0) continue;
+            pos += __popc(peers & ((1u << lane) - 1u));
+            const long long id = 4 * q + j;
+            a.rec[2 * pos] = make_float4(s[j][0], s[j][1], s[j][2], __int_as_float((int)id));
+            a.rec[2 * pos + 1] = make_float4(e[j][0], e[j][1], e[j][2], 0.f);
+        }
     }
 }
 
@@ -385,18 +437,22 @@ size_t sorted_bins() { return kBins; }
 
 void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
     if (a.n_r <= 0) return;
-    count_launches(4);
+    count_launches(5);
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const long long want = (a.n_r + 255) / 256;
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.starts) | reinterpret_cast<uintptr_t>(a.ends)) & 15) == 0;
+    const long long want = (a.n_r + 1023) / 1024;
     const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
-    k_bin_count<<<g, 256, 0, s>>>(a);
-    k_bin_scan<<<kBins / kScanTile, 256, 0, s>>>(a);
-    k_bin_scatter<<<g, 256, 0, s>>>(a);
+    if (vec) k_bin_count<true><<<g, 256, 0, s>>>(a);
+    else k_bin_count<false><<<g, 256, 0, s>>>(a);
+    k_tile_scan<<<1, 256, 0, s>>>(a);
+    k_bin_scan<<<kScanTiles, 256, 0, s>>>(a);
+    if (vec) k_bin_scatter<true><<<g, 256, 0, s>>>(a);
+    else k_bin_scatter<false><<<g, 256, 0, s>>>(a);
     static int occ[3] = {0, 0, 0};
     int& o = occ[mode];
     if (!o) {
@@ -414,10 +470,12 @@ void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
         const char* e = getenv("RS_SORTED_WIDE");
         return !(e && e[0] == '1');
     }();
+    hot_kernel_mark(0, s);
     if (bin_nodes && !stats) {
         if (mode == kBoolean) k_trav_sorted_bin<kBoolean><<<gt, kSortedThreads, 0, s>>>(a);
         else if (mode == kCount) k_trav_sorted_bin<kCount><<<gt, kSortedThreads, 0, s>>>(a);
         else k_trav_sorted_bin<kBarycentric><<<gt, kSortedThreads, 0, s>>>(a);
+        hot_kernel_mark(1, s);
         return;
     }
     if (mode == kBoolean) {
@@ -430,6 +488,7 @@ void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
         if (stats) k_trav_sorted<kBarycentric, true><<<gt, kSortedThreads, 0, s>>>(a);
         else k_trav_sorted<kBarycentric, false><<<gt, kSortedThreads, 0, s>>>(a);
     }
+    hot_kernel_mark(1, s);
 }
 
 }  // namespace rs

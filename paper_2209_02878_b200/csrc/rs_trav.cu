@@ -33,7 +33,6 @@
 namespace rs {
 
 constexpr int kTravThreads = 128;
-constexpr int kTravGroups = kTravThreads / 4;
 constexpr int kTravStack = 96;  // 4-wide depth <= 31 x 3 pending pushes
 constexpr int kSmemStack = 12;  // entries kept in shared memory; deeper ones in global
 constexpr int kPairStack = 32;  // pair kernel: shared-memory stack entries per segment
