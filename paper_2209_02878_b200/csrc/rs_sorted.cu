@@ -160,17 +160,15 @@ __global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
             const int bin = j < cnt ? seg_bin(s[j], e[j], a.nodes4, root, ri) : -1;
             const unsigned act = __activemask();
             const unsigned peers = __match_any_sync(act, bin);
-            if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31)) {
+            if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
                 atomicAdd(a.bins + bin, __popc(peers));
-                atomicAdd(a.tile_sum + (bin >> kScanShift), __popc(peers));
-            }
         }
     }
 }
 
-// Exclusive scan of the bin counters in two levels: k_tile_scan scans the
-// per-1024-bin tile sums (accumulated by k_bin_count) in one CTA, then
-// k_bin_scan scans each tile's bins from its tile offset.
+// Exclusive scan of the bin counters in two levels: k_tile_reduce sums each
+// 1024-bin tile, k_tile_scan scans the tile sums in one CTA, then k_bin_scan
+// scans each tile's bins from its tile offset.
 
 __device__ __forceinline__ unsigned block_excl_scan_256(unsigned v, unsigned* wtot, unsigned* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -188,6 +186,14 @@ __device__ __forceinline__ unsigned block_excl_scan_256(unsigned v, unsigned* wt
     }
     if (total) *total = all;
     return before + x - v;
+}
+
+__global__ void __launch_bounds__(256) k_tile_reduce(SortedArgs a) {
+    __shared__ unsigned wtot[8];
+    const uint4 v = *reinterpret_cast<const uint4*>(a.bins + blockIdx.x * kScanTile + threadIdx.x * 4);
+    unsigned total;
+    block_excl_scan_256(v.x + v.y + v.z + v.w, wtot, &total);
+    if (threadIdx.x == 0) a.tile_sum[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(256) k_tile_scan(SortedArgs a) {
@@ -437,7 +443,7 @@ size_t sorted_bins() { return kBins; }
 
 void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
     if (a.n_r <= 0) return;
-    count_launches(5);
+    count_launches(6);
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -449,6 +455,7 @@ void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
     const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
     if (vec) k_bin_count<true><<<g, 256, 0, s>>>(a);
     else k_bin_count<false><<<g, 256, 0, s>>>(a);
+    k_tile_reduce<<<kScanTiles, 256, 0, s>>>(a);
     k_tile_scan<<<1, 256, 0, s>>>(a);
     k_bin_scan<<<kScanTiles, 256, 0, s>>>(a);
     if (vec) k_bin_scatter<true><<<g, 256, 0, s>>>(a);
