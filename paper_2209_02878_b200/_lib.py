@@ -14,7 +14,9 @@ from pathlib import Path
 from .exceptions import TraversalStackOverflow, ValidationError
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libraysurf_b200.so"
+import os as _os
+
+LIB_PATH = Path(_os.environ.get("RS_LIB", PKG / "lib" / "libraysurf_b200.so"))  # RS_LIB: A/B builds
 HEADER = PKG.parent / "include" / "raysurf_b200.h"
 
 RS_OK, RS_STACK_OVERFLOW, RS_CUDA_ERROR, RS_INVALID_ARG, RS_INTERNAL = range(5)

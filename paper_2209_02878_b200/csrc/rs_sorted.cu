@@ -39,7 +39,11 @@ constexpr int kScanShift = 10;
 constexpr int kScanTile = 1 << kScanShift;
 constexpr int kScanTiles = kBins / kScanTile;
 constexpr int kSortedThreads = 128;
-constexpr int kSortedStack = 64;  // fast tree: <= 3 pending per 4-wide level; deeper -> fallback
+constexpr int kSortedStack = 64;
+#ifndef RS_SORTED_MIN_BLOCKS
+#define RS_SORTED_MIN_BLOCKS 12
+#endif
+constexpr int kSortedMinBlocks = RS_SORTED_MIN_BLOCKS;  // 12 x 128 threads: <= 42 registers  // fast tree: <= 3 pending per 4-wide level; deeper -> fallback
 
 __device__ __forceinline__ void ld_slot(const RsSlot* p, float f[8]) {
     asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kSortedThreads) k_trav_sorted(SortedArgs a) {
 // Binary-node traversal (default): the same coherent order over the 64-B
 // RsNode records (two 256-bit loads per visit).
 template <int MODE>
-__global__ void __launch_bounds__(kSortedThreads) k_trav_sorted_bin(SortedArgs a) {
+__global__ void __launch_bounds__(kSortedThreads, kSortedMinBlocks) k_trav_sorted_bin(SortedArgs a) {
     const unsigned n_live = *a.n_live;
     const int n_int = a.n_int;
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
@@ -368,14 +372,16 @@ __global__ void __launch_bounds__(kSortedThreads) k_trav_sorted_bin(SortedArgs a
         b[0] = fminf(r0.x, r1.x); b[1] = fmaxf(r0.x, r1.x);
         b[2] = fminf(r0.y, r1.y); b[3] = fmaxf(r0.y, r1.y);
         b[4] = fminf(r0.z, r1.z); b[5] = fmaxf(r0.z, r1.z);
-        const double sx = r0.x, sy = r0.y, sz = r0.z;
-        const double dx = __dsub_rn((double)r1.x, sx), dy = __dsub_rn((double)r1.y, sy),
-                     dz = __dsub_rn((double)r1.z, sz);
         int det = 0, nh = 0, btri = -1;
         double bt = 0.0;
         int top = 0, node = root;
         bool ovf = false;
         auto leaf_test = [&](int leaf) {
+            // f64 start / direction rebuilt here (rare) to keep registers for
+            // occupancy in the traversal loop
+            const double sx = r0.x, sy = r0.y, sz = r0.z;
+            const double dx = __dsub_rn((double)r1.x, sx), dy = __dsub_rn((double)r1.y, sy),
+                         dz = __dsub_rn((double)r1.z, sz);
             const RsLeaf* L = a.leaves + leaf;
             const float4 p0 = __ldg(&L->p0), p1 = __ldg(&L->p1), p2 = __ldg(&L->p2);
             double t;
