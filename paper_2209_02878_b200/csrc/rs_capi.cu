@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/raysurf_b200.h"
@@ -52,7 +54,12 @@ thread_local bool g_ev_valid = false;
 void ev_record(int k, cudaStream_t s) {
     if (!g_timing) return;
     if (!g_ev[k]) cudaEventCreate(&g_ev[k]);
-    cudaEventRecord(g_ev[k], s);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive)  // becomes a timing node of the graph
+        cudaEventRecordWithFlags(g_ev[k], s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(g_ev[k], s);
 }
 
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
@@ -596,20 +603,14 @@ int rs_baseline(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_
     return RS_OK;
 }
 
-int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
-                        const float* d_starts, const float* d_ends, int64_t n_r, int mode,
-                        int tree_kind, int max_coll, int max_stack, int32_t* d_flags,
-                        int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
-                        int64_t* n_hits, int64_t* bad, void* stream) {
-    int rc = check_query(mode, max_coll, max_stack);
-    if (rc) return rc;
-    if (bad) *bad = -1;
-    if (n_hits) *n_hits = 0;
-    if (n_r == 0 || n_t == 0) return RS_OK;  // engine.py:233-234 (caller pre-zeroes d_flags)
-    cudaStream_t s = S(stream);
+static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d_tris,
+                             int64_t n_t, const float* d_starts, const float* d_ends, int64_t n_r,
+                             int mode, int tree_kind, int max_coll, int max_stack, int32_t* d_flags,
+                             int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
+                             int64_t* n_hits, int64_t* bad, cudaStream_t s) {
     rs_tree* t = nullptr;
     ev_record(0, s);
-    rc = rs_build(d_verts, n_v, d_tris, n_t, tree_kind, stream, &t);
+    int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t);
     if (rc) return rc;
     const int ref = tree_kind == kTreeReference;
     if (mode == kBarycentric)
@@ -620,15 +621,162 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         rc = query_impl(t, d_starts, d_ends, n_r, mode, max_coll, max_stack, ref, d_flags, d_flags,
                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, bad,
                         false, nullptr, nullptr, s);
-    const int rc2 = rs_free(t, stream);
-    if (g_timing && !rc) {
+    const int rc2 = rs_free(t, s);
+    return rc ? rc : rc2;
+}
+
+// Everything rs_run_batch_device does, enqueued without a host sync so it can
+// be captured into one CUDA graph: build, query, status -> pinned host.
+static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t* d_tris,
+                                int64_t n_t, const float* d_starts, const float* d_ends,
+                                int64_t n_r, int mode, int tree_kind, int max_coll, int max_stack,
+                                int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri,
+                                float* d_pt, RsStatus* h_status, cudaStream_t s) {
+    rs_tree* t = nullptr;
+    ev_record(0, s);
+    int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t);
+    if (rc) return rc;
+    if (tree_kind == kTreeFast && !g_binary_fast) {
+        FastOut o;
+        o.flags = d_flags;
+        o.c_ray = d_ray; o.c_dist = d_dist; o.c_tri = d_tri; o.c_pt = d_pt;
+        FastScratch f;
+        rc = fast_alloc(f, n_r, mode, 2ll * n_r + 4096, s);
+        if (rc) return rc;
+        rc = fast_launch(t, d_starts, d_ends, n_r, mode, o, f, false, s);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(h_status, f.st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(f.blk, s));
+    } else {
+        const bool compact = mode == kBarycentric;
+        const size_t cs = compact ? compact_scratch_bytes(n_r) : 0;
+        char* blk = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
+        CK(cudaMemsetAsync(blk, 0, align256(sizeof(RsStatus)) + cs, s));
+        RsStatus* st = reinterpret_cast<RsStatus*>(blk);
+        const int ref = tree_kind == kTreeReference;
+        QueryArgs a = make_args(t, d_starts, d_ends, n_r, max_coll, max_stack, st);
+        a.detected = d_flags; a.counts = d_flags;
+        a.c_ray = d_ray; a.c_dist = d_dist; a.c_tri = d_tri; a.c_point = d_pt;
+        a.tile_status = reinterpret_cast<unsigned long long*>(blk + align256(sizeof(RsStatus)));
+        ev_record(1, s);
+        if (launch_query(a, mode, ref != 0, compact, kstack_for(ref != 0, max_stack), false, s))
+            return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
+        ev_record(2, s);
+        CK(cudaMemcpyAsync(h_status, st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(blk, s));
+    }
+    return rs_free(t, s);
+}
+
+struct GraphKey {
+    const void* p[9];
+    int64_t n_v, n_t, n_r;
+    int mode, kind, mc, ms, timing;
+    bool operator<(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) < 0; }
+};
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    RsStatus* h_status = nullptr;  // pinned
+    unsigned long long stamp = 0;
+};
+static std::mutex g_graph_mu;
+static std::map<GraphKey, GraphEntry> g_graphs;
+static unsigned long long g_graph_clock = 0;
+static const bool g_use_graphs = [] {
+    const char* e = getenv("RS_NO_GRAPH");
+    return !(e && e[0] == '1');
+}();
+
+int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
+                        const float* d_starts, const float* d_ends, int64_t n_r, int mode,
+                        int tree_kind, int max_coll, int max_stack, int32_t* d_flags,
+                        int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
+                        int64_t* n_hits, int64_t* bad, void* stream) {
+    int rc = check_query(mode, max_coll, max_stack);
+    if (rc) return rc;
+    if (bad) *bad = -1;
+    if (n_hits) *n_hits = 0;
+    if (n_r == 0 || n_t == 0) return RS_OK;  // engine.py:233-234 (caller pre-zeroes d_flags)
+    rc = check_mesh(n_v, n_t);
+    if (rc) return rc;
+    if (n_r > 2147483647ll) return fail(RS_INVALID_ARG, "segment count exceeds int32 indexing");
+    if (tree_kind != kTreeReference && tree_kind != kTreeFast)
+        return fail(RS_INVALID_ARG, "unknown tree kind %d", tree_kind);
+    cudaStream_t s = S(stream);
+    bool done = false;
+    if (g_use_graphs) {
+        // The whole step (about 20 launches, memsets and stream-ordered
+        // allocations) is captured once per argument set and replayed as one
+        // CUDA graph launch.
+        rc = configure_pool();
+        if (rc) return rc;
+        GraphKey key{};
+        const void* ptrs[9] = {d_verts, d_tris, d_starts, d_ends, d_flags, d_ray, d_dist, d_tri, d_pt};
+        std::memcpy(key.p, ptrs, sizeof ptrs);
+        key.n_v = n_v; key.n_t = n_t; key.n_r = n_r;
+        key.mode = mode; key.kind = tree_kind; key.mc = max_coll; key.ms = max_stack;
+        key.timing = g_timing ? 1 : 0;
+        GraphEntry* ge = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_graph_mu);
+            auto it = g_graphs.find(key);
+            if (it != g_graphs.end()) ge = &it->second;
+        }
+        if (!ge) {
+            GraphEntry e;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&e.h_status), sizeof(RsStatus), cudaHostAllocDefault));
+            cudaGraph_t g = nullptr;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            const int erc = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
+                                                 tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
+                                                 d_tri, d_pt, e.h_status, s);
+            const cudaError_t ce = cudaStreamEndCapture(s, &g);
+            if (erc == RS_OK && ce == cudaSuccess && g &&
+                cudaGraphInstantiate(&e.exec, g, 0) == cudaSuccess) {
+                std::lock_guard<std::mutex> lk(g_graph_mu);
+                if (g_graphs.size() >= 8) {  // bounded cache: evict the least recently used
+                    auto victim = g_graphs.begin();
+                    for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+                        if (it->second.stamp < victim->second.stamp) victim = it;
+                    cudaGraphExecDestroy(victim->second.exec);
+                    cudaFreeHost(victim->second.h_status);
+                    g_graphs.erase(victim);
+                }
+                ge = &(g_graphs[key] = e);
+            } else {
+                cudaGetLastError();
+                cudaFreeHost(e.h_status);
+            }
+            if (g) cudaGraphDestroy(g);
+        }
+        if (ge) {
+            ge->stamp = ++g_graph_clock;
+            CK(cudaGraphLaunch(ge->exec, s));
+            CK(cudaStreamSynchronize(s));
+            const RsStatus h = *ge->h_status;
+            if (!h.internal) {
+                if (n_hits) *n_hits = (int64_t)h.hits;
+                rc = status_code(h, bad);
+                done = true;
+            }
+            // internal capacity flag: fall through to the direct path, which
+            // re-queries with the binary kernels
+        }
+    }
+    if (!done) {
+        rc = run_device_direct(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode, tree_kind,
+                               max_coll, max_stack, d_flags, d_ray, d_dist, d_tri, d_pt, n_hits, bad,
+                               s);
+    }
+    if (g_timing && (rc == RS_OK || rc == RS_STACK_OVERFLOW)) {
         cudaEventElapsedTime(&g_build_ms, g_ev[0], g_ev[1]);
         cudaEventElapsedTime(&g_query_ms, g_ev[1], g_ev[2]);
         g_hot_ms = 0.f;
         if (g_ev[3] && g_ev[4]) cudaEventElapsedTime(&g_hot_ms, g_ev[3], g_ev[4]);
         g_ev_valid = true;
     }
-    return rc ? rc : rc2;
+    return rc;
 }
 
 RS_API int rs_set_timing(int enable) {

@@ -39,11 +39,11 @@ constexpr int kScanShift = 10;
 constexpr int kScanTile = 1 << kScanShift;
 constexpr int kScanTiles = kBins / kScanTile;
 constexpr int kSortedThreads = 128;
-constexpr int kSortedStack = 64;
+constexpr int kSortedStack = 64;  // fast tree: <= 3 pending per 4-wide level; deeper -> fallback
 #ifndef RS_SORTED_MIN_BLOCKS
-#define RS_SORTED_MIN_BLOCKS 12
+#define RS_SORTED_MIN_BLOCKS 8
 #endif
-constexpr int kSortedMinBlocks = RS_SORTED_MIN_BLOCKS;  // 12 x 128 threads: <= 42 registers  // fast tree: <= 3 pending per 4-wide level; deeper -> fallback
+constexpr int kSortedMinBlocks = RS_SORTED_MIN_BLOCKS;  // 8 x 128 threads: <= 64 registers
 
 __device__ __forceinline__ void ld_slot(const RsSlot* p, float f[8]) {
     asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"

@@ -25,6 +25,7 @@ for w in $WHAT; do
     bench_buffer) RS_FAST_PATH=buffer timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_buffer.json" 2>> "$OUT/bench.err";;
     bench_sbin) RS_SORTED_BINARY=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_sbin.json" 2>> "$OUT/bench.err";;
     bench_mb) for mb in 8 10; do RS_LIB=paper_2209_02878_b200/lib/libraysurf_b200_mb$mb.so timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_mb$mb.json" 2>> "$OUT/bench.err"; done;;
+    bench_nograph) RS_NO_GRAPH=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_nograph.json" 2>> "$OUT/bench.err";;
     benchq) timeout 600 python bench.py --no-cpu-baseline > "$OUT/bench.json" 2>> "$OUT/bench.err";;
     stats) timeout 300 python tools/stats.py c2 > "$OUT/stats_c2.json" 2>&1;;
     ncuq) timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_query|k_trav|k_exact|k_bin' -s 6 -c 5 \
