@@ -726,12 +726,16 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         if (!ge) {
             GraphEntry e;
             CK(cudaHostAlloc(reinterpret_cast<void**>(&e.h_status), sizeof(RsStatus), cudaHostAllocDefault));
+            // capture on a private stream (the caller's may be the legacy
+            // default stream, which cannot be captured); replay on the caller's
+            static thread_local cudaStream_t cap = nullptr;
+            if (!cap) CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
             cudaGraph_t g = nullptr;
-            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
             const int erc = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
                                                  tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
-                                                 d_tri, d_pt, e.h_status, s);
-            const cudaError_t ce = cudaStreamEndCapture(s, &g);
+                                                 d_tri, d_pt, e.h_status, cap);
+            const cudaError_t ce = cudaStreamEndCapture(cap, &g);
             if (erc == RS_OK && ce == cudaSuccess && g &&
                 cudaGraphInstantiate(&e.exec, g, 0) == cudaSuccess) {
                 std::lock_guard<std::mutex> lk(g_graph_mu);
