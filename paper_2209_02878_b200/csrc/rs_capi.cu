@@ -679,6 +679,7 @@ struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     RsStatus* h_status = nullptr;  // pinned
     unsigned long long stamp = 0;
+    long long kernels = 0;         // kernel nodes in the graph (for rs_kernel_launches)
 };
 static std::mutex g_graph_mu;
 static std::map<GraphKey, GraphEntry> g_graphs;
@@ -731,11 +732,14 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
             static thread_local cudaStream_t cap = nullptr;
             if (!cap) CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
             cudaGraph_t g = nullptr;
+            const long long k0 = rs::g_launches.load();
             CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
             const int erc = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
                                                  tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
                                                  d_tri, d_pt, e.h_status, cap);
             const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+            e.kernels = rs::g_launches.load() - k0;
+            rs::g_launches.fetch_sub(e.kernels);  // counted when replayed
             if (erc == RS_OK && ce == cudaSuccess && g &&
                 cudaGraphInstantiate(&e.exec, g, 0) == cudaSuccess) {
                 std::lock_guard<std::mutex> lk(g_graph_mu);
@@ -757,6 +761,7 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         if (ge) {
             ge->stamp = ++g_graph_clock;
             CK(cudaGraphLaunch(ge->exec, s));
+            rs::g_launches.fetch_add(ge->kernels);
             CK(cudaStreamSynchronize(s));
             const RsStatus h = *ge->h_status;
             if (!h.internal) {

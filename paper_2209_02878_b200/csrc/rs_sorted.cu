@@ -353,77 +353,81 @@ __global__ void __launch_bounds__(kSortedThreads) k_trav_sorted(SortedArgs a) {
     }
 }
 
-// Binary-node traversal (default): the same coherent order over the 64-B
+// Exact test of one candidate leaf, kept out of line: it runs ~1.5 times per
+// segment against ~18 node visits, and inlining it into the traversal loop
+// costs registers and reconvergence bookkeeping on every visit.
+template <int MODE>
+__device__ __noinline__ void leaf_exact(const RsLeaf* __restrict__ leaves, int leaf, float4 r0,
+                                        float4 r1, int& det, int& nh, int& btri, double& bt) {
+    const double sx = r0.x, sy = r0.y, sz = r0.z;
+    const double dx = __dsub_rn((double)r1.x, sx), dy = __dsub_rn((double)r1.y, sy),
+                 dz = __dsub_rn((double)r1.z, sz);
+    const RsLeaf* L = leaves + leaf;
+    const float4 p0 = __ldg(&L->p0), p1 = __ldg(&L->p1), p2 = __ldg(&L->p2);
+    double t;
+    if (mt_hit(p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, p2.x, sx, sy, sz, dx, dy, dz, &t)) {
+        const int tid = __float_as_int(p2.y);
+        det = 1;
+        ++nh;
+        if (MODE == kBarycentric && (btri < 0 || t < bt || (t == bt && tid < btri))) {
+            bt = t;
+            btri = tid;
+        }
+    }
+}
+
+// Binary-node traversal (default): the coherent record order over the 64-B
 // RsNode records (two 256-bit loads per visit).
 template <int MODE>
 __global__ void __launch_bounds__(kSortedThreads, kSortedMinBlocks) k_trav_sorted_bin(SortedArgs a) {
     const unsigned n_live = *a.n_live;
     const int n_int = a.n_int;
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
+    const RsSlot* const nodes = reinterpret_cast<const RsSlot*>(a.nodes);
+    const RsLeaf* const leaves = a.leaves;
+    const float4* const rec = a.rec;
     int stack[kSortedStack];
     const unsigned per_cta = ((n_live + gridDim.x - 1) / gridDim.x + kSortedThreads - 1) /
                              kSortedThreads * kSortedThreads;
     const unsigned beg = blockIdx.x * per_cta;
     const unsigned end = beg + per_cta < n_live ? beg + per_cta : n_live;
     for (unsigned idx = beg + threadIdx.x; idx < end; idx += kSortedThreads) {
-        const float4 r0 = a.rec[2 * idx], r1 = a.rec[2 * idx + 1];
+        const float4 r0 = rec[2 * idx], r1 = rec[2 * idx + 1];
         const int id = __float_as_int(r0.w);
-        float b[6];
-        b[0] = fminf(r0.x, r1.x); b[1] = fmaxf(r0.x, r1.x);
-        b[2] = fminf(r0.y, r1.y); b[3] = fmaxf(r0.y, r1.y);
-        b[4] = fminf(r0.z, r1.z); b[5] = fmaxf(r0.z, r1.z);
+        const float b0 = fminf(r0.x, r1.x), b1 = fmaxf(r0.x, r1.x);
+        const float b2 = fminf(r0.y, r1.y), b3 = fmaxf(r0.y, r1.y);
+        const float b4 = fminf(r0.z, r1.z), b5 = fmaxf(r0.z, r1.z);
         int det = 0, nh = 0, btri = -1;
         double bt = 0.0;
         int top = 0, node = root;
         bool ovf = false;
-        auto leaf_test = [&](int leaf) {
-            // f64 start / direction rebuilt here (rare) to keep registers for
-            // occupancy in the traversal loop
-            const double sx = r0.x, sy = r0.y, sz = r0.z;
-            const double dx = __dsub_rn((double)r1.x, sx), dy = __dsub_rn((double)r1.y, sy),
-                         dz = __dsub_rn((double)r1.z, sz);
-            const RsLeaf* L = a.leaves + leaf;
-            const float4 p0 = __ldg(&L->p0), p1 = __ldg(&L->p1), p2 = __ldg(&L->p2);
-            double t;
-            if (mt_hit(p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, p2.x, sx, sy, sz, dx, dy, dz, &t)) {
-                const int tid = __float_as_int(p2.y);
-                det = 1;
-                ++nh;
-                if (MODE == kBarycentric && (btri < 0 || t < bt || (t == bt && tid < btri))) {
-                    bt = t;
-                    btri = tid;
-                }
-            }
-        };
         if (n_int == 0) {  // single triangle: the leaf's box is slot 0 of nodes4[0]
             float f[8];
             ld_slot(&a.nodes4[0].s[0], f);
-            if (slot_hit(f, b)) leaf_test(0);
+            const float b[6] = {b0, b1, b2, b3, b4, b5};
+            if (slot_hit(f, b)) leaf_exact<MODE>(leaves, 0, r0, r1, det, nh, btri, bt);
         } else {
             for (;;) {
                 float f0[8], f1[8];
-                const RsSlot* np = reinterpret_cast<const RsSlot*>(a.nodes + node);
-                ld_slot(np, f0);
-                ld_slot(np + 1, f1);
+                ld_slot(nodes + 2 * node, f0);
+                ld_slot(nodes + 2 * node + 1, f1);
                 // RsNode: [l.x0 l.x1 l.y0 l.y1 l.z0 l.z1 r.x0 r.x1] [r.y0 r.y1 r.z0 r.z1 lref rref - -]
                 const int ca = __float_as_int(f1[4]), cb = __float_as_int(f1[5]);
-                const bool oa = (b[0] <= f0[1]) & (b[1] >= f0[0]) & (b[2] <= f0[3]) & (b[3] >= f0[2]) &
-                                (b[4] <= f0[5]) & (b[5] >= f0[4]);
-                const bool ob = (b[0] <= f0[7]) & (b[1] >= f0[6]) & (b[2] <= f1[1]) & (b[3] >= f1[0]) &
-                                (b[4] <= f1[3]) & (b[5] >= f1[2]);
+                const bool oa = (b0 <= f0[1]) & (b1 >= f0[0]) & (b2 <= f0[3]) & (b3 >= f0[2]) &
+                                (b4 <= f0[5]) & (b5 >= f0[4]);
+                const bool ob = (b0 <= f0[7]) & (b1 >= f0[6]) & (b2 <= f1[1]) & (b3 >= f1[0]) &
+                                (b4 <= f1[3]) & (b5 >= f1[2]);
                 const bool la = ca >= n_int, lb = cb >= n_int;
-                if (oa & la) leaf_test(ca - n_int);
-                if (ob & lb) leaf_test(cb - n_int);
+                if (oa & la) leaf_exact<MODE>(leaves, ca - n_int, r0, r1, det, nh, btri, bt);
+                if (ob & lb) leaf_exact<MODE>(leaves, cb - n_int, r0, r1, det, nh, btri, bt);
                 if (MODE == kBoolean && det) break;
                 const bool ta = oa & !la, tb = ob & !lb;
-                if (ta) {
-                    node = ca;
-                    if (tb) {
-                        if (top < kSortedStack) stack[top++] = cb;
-                        else ovf = true;
-                    }
-                } else if (tb) {
-                    node = cb;
+                if (ta & tb) {
+                    if (top < kSortedStack) stack[top++] = cb;
+                    else ovf = true;
+                }
+                if (ta | tb) {
+                    node = ta ? ca : cb;
                 } else if (top > 0) {
                     node = stack[--top];
                 } else {
