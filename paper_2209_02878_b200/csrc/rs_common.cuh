@@ -148,4 +148,48 @@ __device__ __forceinline__ void hit_point(double sx, double sy, double sz, doubl
     *pz_ = __double2float_rn(pz);
 }
 
+// ---- warp-parallel decoupled look-back --------------------------------------
+// status[t] = flag << 62 | value; flag 1 = tile aggregate, 2 = inclusive
+// prefix.  Called by all 32 lanes of one warp for tile `tile` with its
+// aggregate; returns the exclusive prefix (same value in every lane).  Each
+// round reads the 32 preceding tiles at once, so a walk over k still-running
+// predecessors costs k/32 L2 round trips instead of k.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* status, long long tile,
+                                                            unsigned long long agg) {
+    const unsigned kAll = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long kMask = (1ull << 62) - 1;
+    volatile unsigned long long* st = status;
+    if (tile == 0) {
+        if (lane == 0) {
+            __threadfence();
+            st[0] = (2ull << 62) | agg;
+        }
+        return 0;
+    }
+    if (lane == 0) {
+        __threadfence();
+        st[tile] = (1ull << 62) | agg;
+    }
+    unsigned long long excl = 0;
+    long long j = tile - 1;
+    for (;;) {
+        const long long k = j - lane;
+        const unsigned long long v = k >= 0 ? st[k] : (2ull << 62);
+        const unsigned flag = (unsigned)(v >> 62);
+        const unsigned incl = __ballot_sync(kAll, flag == 2);
+        const int first = incl ? __ffs(incl) - 1 : 32;
+        const unsigned upto = first >= 31 ? kAll : ((2u << first) - 1u);
+        if (__ballot_sync(kAll, flag == 0) & upto) continue;  // a predecessor is not ready: re-read
+        unsigned long long c = (lane <= first && k >= 0) ? (v & kMask) : 0ull;
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kAll, c, o);
+        excl += c;
+        if (first < 32) break;
+        j -= 32;
+    }
+    __threadfence();
+    if (lane == 0) st[tile] = (2ull << 62) | (excl + agg);
+    return excl;
+}
+
 }  // namespace rs

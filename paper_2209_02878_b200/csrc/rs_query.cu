@@ -482,33 +482,19 @@ __global__ void __launch_bounds__(kQueryThreads) k_query_compact(QueryArgs a) {
     const unsigned ball = __ballot_sync(0xffffffffu, hit);
     if (l == 0) s_warp[w] = __popc(ball);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned agg = 0;
+    if (w == 0) {
+        unsigned agg = 0, mine = 0;
         for (int k = 0; k < kQueryThreads / 32; ++k) {
-            const unsigned c = s_warp[k];
-            s_warp[k] = agg;
-            agg += c;
+            if (k == l) mine = agg;
+            agg += s_warp[k];
         }
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(a.tile_status[tile]);
-        unsigned long long excl = 0;
-        if (tile == 0) {
-            me.store((2ull << 62) | agg, cuda::memory_order_release);
-        } else {
-            me.store((1ull << 62) | agg, cuda::memory_order_release);
-            for (int j = tile - 1; j >= 0;) {
-                cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> prev(
-                    a.tile_status[j]);
-                const unsigned long long v = prev.load(cuda::memory_order_acquire);
-                const unsigned flag = (unsigned)(v >> 62);
-                if (flag == 0) continue;
-                excl += v & ((1ull << 62) - 1);
-                if (flag == 2) break;
-                --j;
-            }
-            me.store((2ull << 62) | (excl + agg), cuda::memory_order_release);
+        __syncwarp();
+        if (l < kQueryThreads / 32) s_warp[l] = mine;
+        const unsigned long long excl = lookback_warp(a.tile_status, tile, agg);
+        if (l == 0) {
+            s_prefix = excl;
+            if ((long long)(tile + 1) * kQueryThreads >= a.n_r) atomicMax(&a.status->hits, excl + agg);
         }
-        s_prefix = excl;
-        if ((long long)(tile + 1) * kQueryThreads >= a.n_r) atomicMax(&a.status->hits, excl + agg);
     }
     __syncthreads();
     if (hit) {

@@ -447,10 +447,14 @@ __global__ void __launch_bounds__(256) k_tiebreak(ExactArgs a) {
     }
 }
 
-// Ordered barycentric compaction over segments (engine.py:206-215): block scan
-// of hit flags + decoupled look-back across tiles; point/distance from the
+// Ordered barycentric compaction over segments (engine.py:206-215): each CTA
+// owns a tile of kCompactItems x 256 segments, block-scans the hit flags,
+// chains tiles with a warp-parallel decoupled look-back, and writes its rows
+// at their final ascending positions with point/distance computed from the
 // winning t in reference op order (_core.pyx:330-348).
 constexpr int kCompactThreads = 256;
+constexpr int kCompactItems = 16;
+constexpr int kCompactTile = kCompactThreads * kCompactItems;
 
 __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a) {
     __shared__ unsigned s_warp[kCompactThreads / 32];
@@ -458,47 +462,45 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
     __shared__ int s_tile;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1ull);
     __syncthreads();
-    const int tile = s_tile;
-    const long long i = (long long)tile * kCompactThreads + threadIdx.x;
-    int tri = -1;
-    if (i < a.n_r) tri = a.best_tri[i];
-    const bool hit = tri >= 0;
+    const long long tile = s_tile;
+    // thread t owns segments [base + t*16, base + t*16 + 16): contiguous rows
+    const long long i0 = tile * kCompactTile + (long long)threadIdx.x * kCompactItems;
+    int tri[kCompactItems];
+    unsigned cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        tri[k] = i0 + k < a.n_r ? a.best_tri[i0 + k] : -1;
+        cnt += tri[k] >= 0;
+    }
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const unsigned ball = __ballot_sync(kFull, hit);
-    if (l == 0) s_warp[w] = __popc(ball);
+    unsigned x = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(kFull, x, o);
+        if (l >= o) x += y;
+    }
+    if (l == 31) s_warp[w] = x;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned agg = 0;
+    if (w == 0) {
+        unsigned agg = 0, mine = 0;
         for (int k = 0; k < kCompactThreads / 32; ++k) {
-            const unsigned c = s_warp[k];
-            s_warp[k] = agg;
-            agg += c;
+            if (k == l) mine = agg;
+            agg += s_warp[k];
         }
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(a.tile_status[tile]);
-        unsigned long long excl = 0;
-        if (tile == 0) {
-            me.store((2ull << 62) | agg, cuda::memory_order_release);
-        } else {
-            me.store((1ull << 62) | agg, cuda::memory_order_release);
-            for (int j = tile - 1; j >= 0;) {
-                cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> prev(a.tile_status[j]);
-                const unsigned long long v = prev.load(cuda::memory_order_acquire);
-                const unsigned flag = (unsigned)(v >> 62);
-                if (flag == 0) continue;
-                excl += v & ((1ull << 62) - 1);
-                if (flag == 2) break;
-                --j;
-            }
-            me.store((2ull << 62) | (excl + agg), cuda::memory_order_release);
+        __syncwarp();
+        if (l < kCompactThreads / 32) s_warp[l] = mine;
+        const unsigned long long excl = lookback_warp(a.tile_status, tile, agg);
+        if (l == 0) {
+            s_prefix = excl;
+            if ((tile + 1) * kCompactTile >= a.n_r) *a.n_hits = excl + agg;
         }
-        s_prefix = excl;
-        if ((long long)(tile + 1) * kCompactThreads >= a.n_r) *a.n_hits = excl + agg;
     }
     __syncthreads();
-    if (hit) {
-        const unsigned long long pos = s_prefix + s_warp[w] + __popc(ball & ((1u << l) - 1u));
-        const unsigned long long k = a.best_t[i];
-        const double t = k == 0ull ? 0.0 : __longlong_as_double((long long)k);
+    unsigned long long pos = s_prefix + s_warp[w] + x - cnt;
+    for (int k = 0; k < kCompactItems; ++k) {
+        if (tri[k] < 0) continue;
+        const long long i = i0 + k;
+        const unsigned long long key = a.best_t[i];
+        const double t = key == 0ull ? 0.0 : __longlong_as_double((long long)key);
         const float* s = a.starts + 3 * i;
         const float* e = a.ends + 3 * i;
         const double sx = s[0], sy = s[1], sz = s[2];
@@ -507,10 +509,11 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
                   __dsub_rn((double)e[2], sz), t, &px, &py, &pz, &d);
         a.ray[pos] = (int)(i + a.ray_offset);
         a.dist[pos] = d;
-        a.tri[pos] = tri;
+        a.tri[pos] = tri[k];
         a.point[3 * pos] = px;
         a.point[3 * pos + 1] = py;
         a.point[3 * pos + 2] = pz;
+        ++pos;
     }
 }
 
@@ -587,14 +590,14 @@ void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s) {
 }
 
 size_t bary_compact_scratch(long long n_r) {
-    return (size_t)((n_r + kCompactThreads - 1) / kCompactThreads) * 8 + 8;
+    return (size_t)((n_r + kCompactTile - 1) / kCompactTile) * 8 + 8;
 }
 
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s) {
     if (a.n_r <= 0) return;
     count_launches(1);
-    k_bary_compact<<<(unsigned)((a.n_r + kCompactThreads - 1) / kCompactThreads), kCompactThreads,
-                     0, s>>>(a);
+    k_bary_compact<<<(unsigned)((a.n_r + kCompactTile - 1) / kCompactTile), kCompactThreads, 0,
+                     s>>>(a);
 }
 
 void launch_bary_dense(const CompactArgs& a, int* detected, int* tri, float* dist, float* points,
