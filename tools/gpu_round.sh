@@ -30,6 +30,7 @@ for w in $WHAT; do
     stats) timeout 300 python tools/stats.py c2 > "$OUT/stats_c2.json" 2>&1;;
     ncuq) timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_query|k_trav|k_exact|k_bin' -s 6 -c 5 \
         -o "$OUT/query" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_full.log" 2>&1;;
+    bench_c3) timeout 600 python bench.py --config c3 --no-cpu-baseline --steps 20 > "$OUT/bench_c3.json" 2>> "$OUT/bench.err";;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
