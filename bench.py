@@ -97,22 +97,31 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append([time.perf_counter()] + parts)
+
+    def wait_ready(self, timeout=5.0):
+        t0 = time.perf_counter()
+        while self.proc and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self):
+        return time.perf_counter()
 
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
-    def summary(self):
-        if not self.rows:
+    def summary(self, t0=None, t1=None):
+        rows = [r[1:] for r in self.rows if (t0 is None or r[0] >= t0) and (t1 is None or r[0] <= t1)]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[2 + k] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(self.rows[-1][1]) if self.rows[-1][1].isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": float(rows[-1][1]) if rows[-1][1].isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
 
 
 def cpu_reference(cfg, steps, warmup, sc=None):
@@ -249,6 +258,8 @@ def main():
     torch.cuda.synchronize()
     launches0 = lib.rs_kernel_launches()
     with ClockSampler(local) as clocks:
+        clocks.wait_ready()
+        t_start = clocks.mark()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
@@ -260,6 +271,8 @@ def main():
             hot_ms.append(hms.value)
         ev1.record(stream)
         torch.cuda.synchronize()
+        t_end = clocks.mark()
+        time.sleep(0.05)
     launches = lib.rs_kernel_launches() - launches0
     if world > 1:
         dist.barrier()
@@ -322,7 +335,7 @@ def main():
                      "kernel": "k_trav_sorted_bin", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_segment": b_ray},
         "gpu_launches": int(launches),
-        "clocks": clocks.summary(),
+        "clocks": clocks.summary(t_start, t_end + 0.02),
     }
     if e2e:
         line["e2e"] = e2e
