@@ -2,8 +2,9 @@
 //
 //   k_prep      per triangle: f64 centroid (morton.py:34-37), grid-wide
 //               support min/max (morton.py:40-45) via ordered-u64 atomics after
-//               a block reduction, and the reference's _reset_tree of internal
-//               slot j (lbvh.py:175-195).
+//               a block reduction, the root box (union of triangle boxes, for
+//               the query's binning), and the reference's _reset_tree of
+//               internal slot j (lbvh.py:175-195).
 //   k_keys      per triangle: quantise (morton.py:48-63 or the isotropic fast
 //               grid) and interleave (morton.py:117-128) -> (code, index).
 //   onesweep    stable LSD radix sort, 8-bit digits, one kernel per pass with
@@ -34,7 +35,9 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
                                               const int* __restrict__ T, int n, double* cent,
                                               RsHeader* hdr, TreeArrays ta, int do_centroids) {
     __shared__ double red[8][6];
+    __shared__ float fred[8][6];
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    float blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         // _reset_tree (lbvh.py:181-189) for internal slot j
         reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[0] = make_float2(0.f, 0.f);
@@ -46,41 +49,57 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
         ta.range_r[j] = -1;
         ta.int_tri[j] = -1;
         ta.visit[j] = 0;
-        if (do_centroids) {
-            const int ia = T[3ll * j], ib = T[3ll * j + 1], ic = T[3ll * j + 2];
+        const int ia = T[3ll * j], ib = T[3ll * j + 1], ic = T[3ll * j + 2];
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const double a = V[3ll * ia + k], b = V[3ll * ib + k], c = V[3ll * ic + k];
-                const double m = __ddiv_rn(__dadd_rn(__dadd_rn(a, b), c), 3.0);
+        for (int k = 0; k < 3; ++k) {
+            const float fa = V[3ll * ia + k], fb = V[3ll * ib + k], fc = V[3ll * ic + k];
+            blo[k] = fminf(blo[k], fminf(fminf(fa, fb), fc));  // root box = union of triangle boxes
+            bhi[k] = fmaxf(bhi[k], fmaxf(fmaxf(fa, fb), fc));
+            if (do_centroids) {
+                const double m = __ddiv_rn(__dadd_rn(__dadd_rn((double)fa, (double)fb), (double)fc), 3.0);
                 cent[3ll * j + k] = m;
                 lo[k] = fmin(lo[k], m);
                 hi[k] = fmax(hi[k], m);
             }
         }
     }
-    if (!do_centroids) return;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         lo[k] = warp_min(lo[k]);
         hi[k] = warp_max(hi[k]);
+        for (int o = 16; o; o >>= 1) {
+            blo[k] = fminf(blo[k], __shfl_xor_sync(0xffffffffu, blo[k], o));
+            bhi[k] = fmaxf(bhi[k], __shfl_xor_sync(0xffffffffu, bhi[k], o));
+        }
     }
     if (l == 0)
         for (int k = 0; k < 3; ++k) {
             red[w][k] = lo[k];
             red[w][3 + k] = hi[k];
+            fred[w][k] = blo[k];
+            fred[w][3 + k] = bhi[k];
         }
     __syncthreads();
     if (threadIdx.x < 6) {
         const int k = threadIdx.x;
         double v = red[0][k];
-        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+        float fv = fred[0][k];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
             v = k < 3 ? fmin(v, red[i][k]) : fmax(v, red[i][k]);
-        if (isfinite(v)) {
+            fv = k < 3 ? fminf(fv, fred[i][k]) : fmaxf(fv, fred[i][k]);
+        }
+        if (do_centroids && isfinite(v)) {
             if (k < 3)
                 atomicMax(&hdr->smin[k], ~ord_of(v));
             else
                 atomicMax(&hdr->smax[k - 3], ord_of(v));
+        }
+        if (isfinite(fv)) {
+            if (k < 3)
+                atomicMax(&hdr->bmin[k], ~ord32(fv));
+            else
+                atomicMax(&hdr->bmax[k - 3], ord32(fv));
         }
     }
 }

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -171,9 +172,21 @@ int alloc_tree(int64_t n, int kind, cudaStream_t s, rs_tree** out) {
     return RS_OK;
 }
 
+// nodes4 (the 4-wide collapse) is read only by the A/B traversal variants
+bool need_nodes4() {
+    static const bool need = [] {
+        const char* e = getenv("RS_FAST_PATH");
+        return (e && e[0] == 'b') || rs::sorted_wide();
+    }();
+    return need;
+}
+
+// after_prep (optional) runs on the host right after k_prep is enqueued on
+// `s`: the fast query forks its binning onto a second stream there, since it
+// needs only the root box k_prep computes.
 int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
                const uint64_t* sorted_codes, const int* sorted_ids, cudaStream_t s,
-               rs_tree** out) {
+               rs_tree** out, const std::function<int(rs_tree*)>& after_prep = nullptr) {
     int rc = check_mesh(n_v, n_t);
     if (rc) return rc;
     if (kind != kTreeReference && kind != kTreeFast)
@@ -202,10 +215,14 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
         int* vals2 = c.take<int>(n);
         void* sort_scratch = c.take<char>(sb);
         launch_prep(V, T, n, cent, t->hdr, t->ta, true, s);
+        if (after_prep) {
+            rc = after_prep(t);
+            if (rc) return rc;
+        }
         launch_keys(cent, n, t->hdr, kind, keys, vals, s);
         launch_sort(keys, vals, keys2, vals2, n, passes, sort_scratch, s);
         launch_climb(V, T, n, keys, vals, t->ta, t->nodes, t->leaves, t->hdr, s);
-        if (kind == kTreeFast) launch_collapse(n, t->ta, t->nodes, t->nodes4, t->hdr, s);
+        if (kind == kTreeFast && need_nodes4()) launch_collapse(n, t->ta, t->nodes, t->nodes4, t->hdr, s);
         CK(cudaFreeAsync(scratch, s));
     }
     CK(cudaGetLastError());
@@ -411,8 +428,18 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     return RS_OK;
 }
 
-static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
-                       const FastOut& o, FastScratch& f, bool stats, cudaStream_t s) {
+static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r,
+                              const FastOut& o, FastScratch& f) {
+    return SortedArgs{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r,
+                      f.bins, f.cursor, f.n_live, f.bins + sorted_bins(), f.rec, o.flags,
+                      f.best_t, f.best_tri, f.st};
+}
+
+// Phase 1 of the sorted fast path: output presets + spatial binning.  Needs
+// only the tree header's root box, so it may run concurrently with the rest
+// of the build on another stream.
+static int fast_bin(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
+                    const FastOut& o, FastScratch& f, cudaStream_t s) {
     const bool bary = mode == kBarycentric;
     CK(cudaMemsetAsync(f.st, 0, sizeof(RsStatus), s));
     if (!bary) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
@@ -421,21 +448,49 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
         CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
     }
+    CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 4 * (sorted_bins() / 1024), s));
+    launch_binning(sorted_args(t, d_s, d_e, n_r, o, f), s);
+    return RS_OK;
+}
+
+// Phase 2: traversal (+ barycentric compaction).
+static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
+                     const FastOut& o, FastScratch& f, bool stats, cudaStream_t s) {
     ev_record(1, s);
-    if (g_buffer_path) {
-        TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill,
-                    f.st, f.gstack};
-        launch_trav(ta, stats, s);
-        ExactArgs ea{f.cand, &f.st->cand_count, f.cap, f.chunk_fill, d_s, d_e, t->leaves,
-                     o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
-        launch_exact(ea, mode, stats, s);
-    } else {
-        CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 4 * (sorted_bins() / 1024), s));
-        SortedArgs sa{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.bins,
-                      f.cursor, f.n_live, f.bins + sorted_bins(), f.rec,
-                      o.flags, f.best_t, f.best_tri, f.st};
-        launch_sorted(sa, mode, stats, s);
+    launch_sorted_trav(sorted_args(t, d_s, d_e, n_r, o, f), mode, stats, s);
+    if (mode == kBarycentric) {
+        CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
+                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset};
+        if (o.c_ray) launch_bary_compact(ca, s);
+        else launch_bary_dense(ca, o.det, o.tri, o.dist, o.pts, s);
     }
+    CK(cudaGetLastError());
+    ev_record(2, s);
+    return RS_OK;
+}
+
+static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
+                       const FastOut& o, FastScratch& f, bool stats, cudaStream_t s) {
+    const bool bary = mode == kBarycentric;
+    if (!g_buffer_path) {
+        int rc = fast_bin(t, d_s, d_e, n_r, mode, o, f, s);
+        if (rc) return rc;
+        return fast_trav(t, d_s, d_e, n_r, mode, o, f, stats, s);
+    }
+    CK(cudaMemsetAsync(f.st, 0, sizeof(RsStatus), s));
+    if (!bary) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
+    if (bary) {
+        CK(cudaMemsetAsync(f.best_t, 0xFF, 8ull * n_r, s));
+        CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
+        CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
+    }
+    ev_record(1, s);
+    TravArgs ta{t->nodes4, t->hdr, (int)(t->n - 1), d_s, d_e, n_r, f.cand, f.cap, f.chunk_fill,
+                f.st, f.gstack};
+    launch_trav(ta, stats, s);
+    ExactArgs ea{f.cand, &f.st->cand_count, f.cap, f.chunk_fill, d_s, d_e, t->leaves,
+                 o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
+    launch_exact(ea, mode, stats, s);
     if (bary) {
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
                        f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset};
@@ -603,12 +658,74 @@ int rs_baseline(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_
     return RS_OK;
 }
 
+struct Fork {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t prep = nullptr, bin = nullptr;
+};
+static thread_local Fork g_fork;
+
+static int fork_init() {
+    if (g_fork.aux) return RS_OK;
+    CK(cudaStreamCreateWithFlags(&g_fork.aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g_fork.prep, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g_fork.bin, cudaEventDisableTiming));
+    return RS_OK;
+}
+
+// Fast-tree run_batch with the binning forked onto a second stream right
+// after k_prep: binning (two passes over the segments) overlaps keys, sort
+// and climb.  Leaves the status in f.st (device); the caller frees f.blk.
+static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t* d_tris,
+                               int64_t n_t, const float* d_starts, const float* d_ends,
+                               int64_t n_r, int mode, const FastOut& o, FastScratch& f,
+                               cudaStream_t s, rs_tree** tree_out) {
+    int rc = fork_init();
+    if (rc) return rc;
+    cudaStream_t aux = g_fork.aux;
+    auto fork = [&](rs_tree* t) -> int {
+        CK(cudaEventRecord(g_fork.prep, s));
+        CK(cudaStreamWaitEvent(aux, g_fork.prep, 0));
+        int r = fast_alloc(f, n_r, mode, 2ll * n_r + 4096, aux);
+        if (r) return r;
+        r = fast_bin(t, d_starts, d_ends, n_r, mode, o, f, aux);
+        if (r) return r;
+        CK(cudaEventRecord(g_fork.bin, aux));
+        return RS_OK;
+    };
+    ev_record(0, s);
+    rs_tree* t = nullptr;
+    rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, s, &t, fork);
+    if (rc) return rc;
+    CK(cudaStreamWaitEvent(s, g_fork.bin, 0));
+    rc = fast_trav(t, d_starts, d_ends, n_r, mode, o, f, false, s);
+    *tree_out = t;
+    return rc;
+}
+
 static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d_tris,
                              int64_t n_t, const float* d_starts, const float* d_ends, int64_t n_r,
                              int mode, int tree_kind, int max_coll, int max_stack, int32_t* d_flags,
                              int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
                              int64_t* n_hits, int64_t* bad, cudaStream_t s) {
     rs_tree* t = nullptr;
+    if (tree_kind == kTreeFast && !g_buffer_path && !g_binary_fast) {
+        FastOut o;
+        o.flags = d_flags;
+        o.c_ray = d_ray; o.c_dist = d_dist; o.c_tri = d_tri; o.c_pt = d_pt;
+        FastScratch f;
+        int rc = enqueue_fast_forked(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode, o, f,
+                                     s, &t);
+        RsStatus h{};
+        if (!rc) rc = read_status(f.st, s, &h);
+        if (f.blk) cudaFreeAsync(f.blk, s);
+        if (!rc && h.internal) rc = binary_query(t, d_starts, d_ends, n_r, mode, o, &h, s);
+        if (!rc) {
+            if (n_hits) *n_hits = (int64_t)h.hits;
+            rc = status_code(h, bad);
+        }
+        const int rc2 = t ? rs_free(t, s) : RS_OK;
+        return rc ? rc : rc2;
+    }
     ev_record(0, s);
     int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t);
     if (rc) return rc;
@@ -633,6 +750,18 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
                                 int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri,
                                 float* d_pt, RsStatus* h_status, cudaStream_t s) {
     rs_tree* t = nullptr;
+    if (tree_kind == kTreeFast && !g_buffer_path && !g_binary_fast) {
+        FastOut o;
+        o.flags = d_flags;
+        o.c_ray = d_ray; o.c_dist = d_dist; o.c_tri = d_tri; o.c_pt = d_pt;
+        FastScratch f;
+        int rc = enqueue_fast_forked(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode, o, f,
+                                     s, &t);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(h_status, f.st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(f.blk, s));
+        return rs_free(t, s);
+    }
     ev_record(0, s);
     int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t);
     if (rc) return rc;

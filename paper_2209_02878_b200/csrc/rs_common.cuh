@@ -56,7 +56,8 @@ struct RsHeader {
     unsigned long long smax[3];  //  ordered(max centroid)
     int root;
     int height;
-    int pad[2];
+    unsigned bmin[3];            // ~ordered32(min triangle-box coordinate) = root box
+    unsigned bmax[3];            //  ordered32(max triangle-box coordinate)
 };
 
 // Per-query device status (zeroed before a query).
@@ -87,6 +88,14 @@ __host__ __device__ __forceinline__ double from_ord(unsigned long long o) {
     __builtin_memcpy(&d, &u, 8);
     return d;
 #endif
+}
+
+__device__ __forceinline__ unsigned ord32(float f) {
+    const unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float from_ord32(unsigned o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
 }
 
 // ---- f32 box test: touching counts (geometry.py:69-79, _core.pyx:44-49) ---

@@ -153,7 +153,10 @@ struct SortedArgs {
     RsStatus* status;
 };
 size_t sorted_bins();
-void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s);
+bool sorted_wide();  // RS_SORTED_WIDE=1: 4-wide per-thread traversal (needs nodes4)
+// binning needs only the header's root box (available right after k_prep)
+void launch_binning(const SortedArgs& a, cudaStream_t s);
+void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t s);
 void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);
 size_t bary_compact_scratch(long long n_r);
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s);

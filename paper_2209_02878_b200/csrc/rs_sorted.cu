@@ -66,43 +66,34 @@ __device__ __forceinline__ unsigned spread_bits(unsigned v) {  // bit i -> bit 3
 
 // Root box + culling helper shared by both binning passes.
 struct RootInfo {
-    float lo[3], inv[3];
+    float lo[3], hi[3], inv[3];
 };
 
-__device__ __forceinline__ void root_info(const RsNode4* nodes4, int root, RootInfo& ri) {
-    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        float f[8];
-        ld_slot(&nodes4[root].s[j], f);
-        if (__float_as_int(f[6]) >= 0) {
-            lo[0] = fminf(lo[0], f[0]); hi[0] = fmaxf(hi[0], f[1]);
-            lo[1] = fminf(lo[1], f[2]); hi[1] = fmaxf(hi[1], f[3]);
-            lo[2] = fminf(lo[2], f[4]); hi[2] = fmaxf(hi[2], f[5]);
-        }
-    }
-    const float ext = fmaxf(fmaxf(hi[0] - lo[0], hi[1] - lo[1]), fmaxf(hi[2] - lo[2], 1e-30f));
+// The root box (union of all triangle boxes) comes from the build's k_prep,
+// so the binning can run concurrently with the rest of the build.
+__device__ __forceinline__ void root_info(const RsHeader* hdr, RootInfo& ri) {
+    float hi[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        ri.lo[k] = lo[k];
-        ri.inv[k] = ((float)(1 << kAxisBits) - 0.01f) / ext;
+        ri.lo[k] = from_ord32(~__ldg(&hdr->bmin[k]));
+        hi[k] = from_ord32(__ldg(&hdr->bmax[k]));
     }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ri.hi[k] = hi[k];
+    const float ext = fmaxf(fmaxf(hi[0] - ri.lo[0], hi[1] - ri.lo[1]), fmaxf(hi[2] - ri.lo[2], 1e-30f));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ri.inv[k] = ((float)(1 << kAxisBits) - 0.01f) / ext;
 }
 
-// Returns the bin of a live segment, or -1 when it overlaps no root child.
-__device__ __forceinline__ int seg_bin(const float s[3], const float e[3], const RsNode4* nodes4,
-                                       int root, const RootInfo& ri) {
+// Returns the bin of a live segment, or -1 when its box misses the root box
+// (no leaf box can overlap it: its result is the pre-zeroed default).
+__device__ __forceinline__ int seg_bin(const float s[3], const float e[3], const RootInfo& ri) {
     float b[6];
     b[0] = fminf(s[0], e[0]); b[1] = fmaxf(s[0], e[0]);
     b[2] = fminf(s[1], e[1]); b[3] = fmaxf(s[1], e[1]);
     b[4] = fminf(s[2], e[2]); b[5] = fmaxf(s[2], e[2]);
-    bool live = false;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        float f[8];
-        ld_slot(&nodes4[root].s[j], f);
-        live |= slot_hit(f, b);
-    }
+    const bool live = (b[0] <= ri.hi[0]) & (b[1] >= ri.lo[0]) & (b[2] <= ri.hi[1]) &
+                      (b[3] >= ri.lo[1]) & (b[4] <= ri.hi[2]) & (b[5] >= ri.lo[2]);
     if (!live) return -1;
     unsigned key = 0;
 #pragma unroll
@@ -152,16 +143,15 @@ __device__ __forceinline__ int load4(const float* __restrict__ S, const float* _
 
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
-    const int root = a.n_int > 0 ? __ldg(&a.hdr->root) : 0;
     RootInfo ri;
-    root_info(a.nodes4, root, ri);
+    root_info(a.hdr, ri);
     const long long nq = (a.n_r + 3) / 4;
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
         float s[4][3], e[4][3];
         const int cnt = load4<VEC>(a.starts, a.ends, q, a.n_r, s, e);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int bin = j < cnt ? seg_bin(s[j], e[j], a.nodes4, root, ri) : -1;
+            const int bin = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
             const unsigned act = __activemask();
             const unsigned peers = __match_any_sync(act, bin);
             if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
@@ -236,9 +226,8 @@ __global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
 
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
-    const int root = a.n_int > 0 ? __ldg(&a.hdr->root) : 0;
     RootInfo ri;
-    root_info(a.nodes4, root, ri);
+    root_info(a.hdr, ri);
     const long long nq = (a.n_r + 3) / 4;
     const int lane = threadIdx.x & 31;
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
@@ -246,7 +235,7 @@ __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
         const int cnt = load4<VEC>(a.starts, a.ends, q, a.n_r, s, e);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int bin = j < cnt ? seg_bin(s[j], e[j], a.nodes4, root, ri) : -1;
+            const int bin = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
             const unsigned act = __activemask();
             const unsigned peers = __match_any_sync(act, bin);
             const int leader = __ffs(peers) - 1;
@@ -400,11 +389,12 @@ __global__ void __launch_bounds__(kSortedThreads, kSortedMinBlocks) k_trav_sorte
         double bt = 0.0;
         int top = 0, node = root;
         bool ovf = false;
-        if (n_int == 0) {  // single triangle: the leaf's box is slot 0 of nodes4[0]
-            float f[8];
-            ld_slot(&a.nodes4[0].s[0], f);
-            const float b[6] = {b0, b1, b2, b3, b4, b5};
-            if (slot_hit(f, b)) leaf_exact<MODE>(leaves, 0, r0, r1, det, nh, btri, bt);
+        if (n_int == 0) {  // single triangle: the leaf is the root (_core.pyx:260-267)
+            const float4 p0 = __ldg(&leaves[0].p0), p1 = __ldg(&leaves[0].p1), p2 = __ldg(&leaves[0].p2);
+            const bool o = (b0 <= fmaxf(fmaxf(p0.x, p0.w), p1.z)) & (b1 >= fminf(fminf(p0.x, p0.w), p1.z)) &
+                           (b2 <= fmaxf(fmaxf(p0.y, p1.x), p1.w)) & (b3 >= fminf(fminf(p0.y, p1.x), p1.w)) &
+                           (b4 <= fmaxf(fmaxf(p0.z, p1.y), p2.x)) & (b5 >= fminf(fminf(p0.z, p1.y), p2.x));
+            if (o) leaf_exact<MODE>(leaves, 0, r0, r1, det, nh, btri, bt);
         } else {
             for (;;) {
                 float f0[8], f1[8];
@@ -450,15 +440,28 @@ __global__ void __launch_bounds__(kSortedThreads, kSortedMinBlocks) k_trav_sorte
 
 size_t sorted_bins() { return kBins; }
 
-void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
-    if (a.n_r <= 0) return;
-    count_launches(6);
+static int sm_total() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    return sms;
+}
+
+bool sorted_wide() {
+    static const bool wide = [] {
+        const char* e = getenv("RS_SORTED_WIDE");
+        return e && e[0] == '1';
+    }();
+    return wide;
+}
+
+void launch_binning(const SortedArgs& a, cudaStream_t s) {
+    if (a.n_r <= 0) return;
+    count_launches(5);
+    const int sms = sm_total();
     const bool vec = ((reinterpret_cast<uintptr_t>(a.starts) | reinterpret_cast<uintptr_t>(a.ends)) & 15) == 0;
     const long long want = (a.n_r + 1023) / 1024;
     const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
@@ -469,6 +472,12 @@ void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
     k_bin_scan<<<kScanTiles, 256, 0, s>>>(a);
     if (vec) k_bin_scatter<true><<<g, 256, 0, s>>>(a);
     else k_bin_scatter<false><<<g, 256, 0, s>>>(a);
+}
+
+void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
+    if (a.n_r <= 0) return;
+    count_launches(1);
+    const int sms = sm_total();
     static int occ[3] = {0, 0, 0};
     int& o = occ[mode];
     if (!o) {
@@ -482,10 +491,7 @@ void launch_sorted(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
     const unsigned gt = (unsigned)(wt < (long long)sms * o ? wt : (long long)sms * o);
     // binary nodes measured faster on coherent segments (C2: 0.64 vs 0.67 ms);
     // RS_SORTED_WIDE=1 selects the 4-wide per-thread traversal instead
-    static const bool bin_nodes = [] {
-        const char* e = getenv("RS_SORTED_WIDE");
-        return !(e && e[0] == '1');
-    }();
+    const bool bin_nodes = !sorted_wide();
     hot_kernel_mark(0, s);
     if (bin_nodes && !stats) {
         if (mode == kBoolean) k_trav_sorted_bin<kBoolean><<<gt, kSortedThreads, 0, s>>>(a);
