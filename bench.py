@@ -290,6 +290,9 @@ def main():
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
         mesh_p = rs.Mesh.from_arrays(pin(mesh_h.vertices), pin(mesh_h.triangles))
         seg_p = rs.SegmentBatch.from_arrays(pin(seg_h.starts), pin(seg_h.ends))
+        if os.environ.get("RS_E2E_CHUNK"):  # pipeline chunk experiments
+            import dataclasses
+            config = dataclasses.replace(config, chunk_rays=int(os.environ["RS_E2E_CHUNK"]))
         for _ in range(2):
             r = rs.run_batch(mesh_p, seg_p, config)
         ts = []
@@ -339,6 +342,11 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if os.environ.get("RS_DEBUG_STATUS"):
+        st = (C.c_ulonglong * 8)()
+        lib.rs_last_status(st)
+        line["debug_status"] = dict(zip(["bad", "internal", "hits", "tile_counter", "visits", "mts",
+                                         "cand_count", "pad"], [int(x) for x in st]))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference(cfg, 2, 1, sc=sc)
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "Mrays/s", "cores": info["cores"],

@@ -155,6 +155,18 @@ RS_API int rs_last_timings(float *build_ms, float *query_ms, float *hot_kernel_m
 /* Cumulative number of kernels this library has launched. */
 RS_API long long rs_kernel_launches(void);
 
+/* Tuning knobs of the fast-tree query (A/B experiments and tests that pin a
+ * traversal variant): "trav" (0 auto, 1 per-thread binary, 2 per-thread
+ * 4-wide, 3 tile), "tile_density", "tile_balance", "tile_area",
+ * "bin_occupancy".  A negative value only reads; the previous value is
+ * returned in *old_value.  Results never depend on these. */
+RS_API int rs_set_option(const char *name, long long value, long long *old_value);
+
+/* Diagnostics: the 8 device status words (bad, internal, hits, tile_counter,
+ * visits, mts, cand_count, pad) of the calling thread's last graph-replayed
+ * rs_run_batch_device. */
+RS_API int rs_last_status(unsigned long long *out8);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,7 @@ missing or no CUDA device is present, every compute call raises.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import re
 from pathlib import Path
@@ -43,6 +44,8 @@ _SIGS = {
     "rs_set_timing": (i32, [i32]),
     "rs_last_timings": (i32, [p, p, p]),
     "rs_kernel_launches": (C.c_longlong, []),
+    "rs_last_status": (i32, [p]),
+    "rs_set_option": (i32, [C.c_char_p, C.c_longlong, p]),
 }
 
 _lib = None
@@ -67,6 +70,17 @@ def lib() -> C.CDLL:
             fn.argtypes = args
         _lib = dll
     return _lib
+
+
+@contextlib.contextmanager
+def option(name: str, value: int):
+    """Temporarily set a fast-path tuning knob (rs_set_option)."""
+    old = C.c_longlong()
+    check(lib().rs_set_option(name.encode(), int(value), C.byref(old)))
+    try:
+        yield
+    finally:
+        lib().rs_set_option(name.encode(), old.value, None)
 
 
 def last_error() -> str:

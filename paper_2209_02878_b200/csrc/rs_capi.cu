@@ -174,11 +174,13 @@ int alloc_tree(int64_t n, int kind, cudaStream_t s, rs_tree** out) {
 
 // nodes4 (the 4-wide collapse) is read only by the A/B traversal variants
 bool need_nodes4() {
-    static const bool need = [] {
+    static const bool buffer = [] {
         const char* e = getenv("RS_FAST_PATH");
-        return (e && e[0] == 'b') || rs::sorted_wide();
+        return e && e[0] == 'b';
     }();
-    return need;
+    long long trav = 0;
+    rs::sorted_option("trav", -1, &trav);
+    return buffer || trav == 2;
 }
 
 // after_prep (optional) runs on the host right after k_prep is enqueued on
@@ -275,8 +277,8 @@ int status_code(const RsStatus& h, int64_t* bad_segment) {
 // Per-thread cached pipeline resources for rs_run_batch_host.
 struct Pipe {
     int device = -1;
-    cudaStream_t copy = nullptr, copy2 = nullptr;  // starts / ends H2D on two DMA queues
-    cudaEvent_t ev_in[2], ev_in2[2], ev_q[2], ev_out[2];
+    cudaStream_t copy = nullptr, copy2 = nullptr;  // H2D (both endpoint arrays) / D2H
+    cudaEvent_t ev_in[2], ev_in2[2], ev_q[2], ev_out[2], ev_blk;
 };
 thread_local Pipe g_pipe;
 
@@ -292,6 +294,7 @@ int pipe_init() {
         CK(cudaEventCreateWithFlags(&g_pipe.ev_q[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&g_pipe.ev_out[k], cudaEventDisableTiming));
     }
+    CK(cudaEventCreateWithFlags(&g_pipe.ev_blk, cudaEventDisableTiming));
     g_pipe.device = dev;
     return RS_OK;
 }
@@ -405,7 +408,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         total += align256(8ull * n_r) + align256(4ull * n_r) + align256(8ull * cap) +
                  align256(bary_compact_scratch(n_r));
     if (g_buffer_path) total += align256(4 * trav_gstack_ints());
-    total += 3 * align256(4 * sorted_bins()) + align256(4 * 64) + align256(32ull * n_r);
+    total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r);
     CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
@@ -422,7 +425,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     if (g_buffer_path) f.gstack = c.take<int>(trav_gstack_ints());
     f.bins = c.take<unsigned>(2 * sorted_bins());  // counters + look-back words (zeroed together)
     f.cursor = c.take<unsigned>(sorted_bins());
-    f.n_live = c.take<unsigned>(64);
+    f.n_live = c.take<unsigned>(64 + 4 * 32);
     f.rec = c.take<float4>(2ull * n_r);
     f.cap = cap;
     return RS_OK;
@@ -431,7 +434,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
 static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r,
                               const FastOut& o, FastScratch& f) {
     return SortedArgs{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r,
-                      f.bins, f.cursor, f.n_live, f.bins + sorted_bins(), f.rec, o.flags,
+                      f.bins, f.cursor, f.n_live, reinterpret_cast<float*>(f.n_live + 64), f.bins + sorted_bins(), f.rec, o.flags,
                       f.best_t, f.best_tri, f.st};
 }
 
@@ -801,7 +804,7 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
 struct GraphKey {
     const void* p[9];
     int64_t n_v, n_t, n_r;
-    int mode, kind, mc, ms, timing;
+    int mode, kind, mc, ms, timing, opt_gen;
     bool operator<(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) < 0; }
 };
 struct GraphEntry {
@@ -810,6 +813,8 @@ struct GraphEntry {
     unsigned long long stamp = 0;
     long long kernels = 0;         // kernel nodes in the graph (for rs_kernel_launches)
 };
+static thread_local RsStatus g_last_status{};
+static std::atomic<int> g_opt_gen{0};  // bumped by rs_set_option: captured graphs bake the options in
 static std::mutex g_graph_mu;
 static std::map<GraphKey, GraphEntry> g_graphs;
 static unsigned long long g_graph_clock = 0;
@@ -847,6 +852,7 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         key.n_v = n_v; key.n_t = n_t; key.n_r = n_r;
         key.mode = mode; key.kind = tree_kind; key.mc = max_coll; key.ms = max_stack;
         key.timing = g_timing ? 1 : 0;
+        key.opt_gen = g_opt_gen.load();
         GraphEntry* ge = nullptr;
         {
             std::lock_guard<std::mutex> lk(g_graph_mu);
@@ -893,6 +899,7 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
             rs::g_launches.fetch_add(ge->kernels);
             CK(cudaStreamSynchronize(s));
             const RsStatus h = *ge->h_status;
+            g_last_status = h;
             if (!h.internal) {
                 if (n_hits) *n_hits = (int64_t)h.hits;
                 rc = status_code(h, bad);
@@ -932,6 +939,22 @@ RS_API int rs_last_timings(float* build_ms, float* query_ms, float* hot_ms) {
 }
 
 RS_API long long rs_kernel_launches(void) { return g_launches.load(); }
+
+// Diagnostics: the device status words of the calling thread's last
+// graph-replayed rs_run_batch_device (bad, internal, hits, tile_counter,
+// visits, mts, cand_count, pad); builds with -DRS_TILE_STATS fill the
+// traversal counters.
+RS_API int rs_set_option(const char* name, long long value, long long* old_value) {
+    if (!name) return fail(RS_INVALID_ARG, "null option name");
+    if (rs::sorted_option(name, value, old_value)) return fail(RS_INVALID_ARG, "unknown option %s", name);
+    g_opt_gen.fetch_add(1);
+    return RS_OK;
+}
+
+RS_API int rs_last_status(unsigned long long* out8) {
+    std::memcpy(out8, &g_last_status, sizeof(RsStatus));
+    return RS_OK;
+}
 
 }  // extern "C"
 
@@ -996,7 +1019,16 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     }
     char* tiles = reinterpret_cast<char*>(c.take<char>(align256(compact_scratch_bytes(chunk_rays)) * nchunks));
     RsStatus* st = c.take<RsStatus>(nchunks);
+    // Streams: s computes (build, then one query per chunk), h2d = g_pipe.copy
+    // uploads the chunks (PCIe H2D is the bound of this path: the inputs are
+    // 24 B per segment), d2h = g_pipe.copy2 returns each chunk's flags as soon
+    // as its query ends.  The uploads start right after the allocation, so
+    // the mesh upload and the build overlap chunk 0's transfer.
+    cudaStream_t h2d = cp, d2h = g_pipe.copy2;
     CK(cudaMemsetAsync(tiles, 0, tiles_b + st_b, s));
+    CK(cudaEventRecord(g_pipe.ev_blk, s));
+    CK(cudaStreamWaitEvent(h2d, g_pipe.ev_blk, 0));
+    CK(cudaStreamWaitEvent(d2h, g_pipe.ev_blk, 0));
     CK(cudaMemcpyAsync(dV, h_verts, 12ull * n_v, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dT, h_tris, 12ull * n_t, cudaMemcpyHostToDevice, s));
     rs_tree* t = nullptr;
@@ -1013,27 +1045,17 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
             rc = fast_alloc(fs[b], chunk_rays, mode, 2 * chunk_rays + 4096, s);
             if (rc) return rc;
         }
-    // The copy stream must see the memset/mesh copies ordered before chunk 0.
-    CK(cudaEventRecord(g_pipe.ev_q[1], s));
-    CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[1], 0));
-    CK(cudaStreamWaitEvent(g_pipe.copy2, g_pipe.ev_q[1], 0));
     unsigned long long running = 0;  // barycentric rows already placed
     for (int64_t k = 0; k < nchunks; ++k) {
         const int b = (int)(k & 1);
         const int64_t lo = k * chunk_rays;
         const int64_t cnt = (lo + chunk_rays <= n_r) ? chunk_rays : n_r - lo;
-        if (k >= 2) {  // buffer b free again
-            CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));
-            CK(cudaStreamWaitEvent(g_pipe.copy2, g_pipe.ev_q[b], 0));
-        }
-        CK(cudaMemcpyAsync(din[b][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, cp));
-        CK(cudaMemcpyAsync(din[b][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice,
-                           g_pipe.copy2));
-        CK(cudaEventRecord(g_pipe.ev_in[b], cp));
-        CK(cudaEventRecord(g_pipe.ev_in2[b], g_pipe.copy2));
+        if (k >= 2) CK(cudaStreamWaitEvent(h2d, g_pipe.ev_q[b], 0));  // input buffer b free again
+        CK(cudaMemcpyAsync(din[b][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
+        CK(cudaMemcpyAsync(din[b][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
+        CK(cudaEventRecord(g_pipe.ev_in[b], h2d));
         CK(cudaStreamWaitEvent(s, g_pipe.ev_in[b], 0));
-        CK(cudaStreamWaitEvent(s, g_pipe.ev_in2[b], 0));
-        if (k >= 2 && !bary) CK(cudaStreamWaitEvent(s, g_pipe.ev_out[b], 0));
+        if (k >= 2 && !bary) CK(cudaStreamWaitEvent(s, g_pipe.ev_out[b], 0));  // flags b read back
         if (fast) {
             fs[b].st = st + k;
             FastOut o;
@@ -1045,41 +1067,36 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
             }
             rc = fast_launch(t, din[b][0], din[b][1], cnt, mode, o, fs[b], false, s);
             if (rc) return rc;
-            CK(cudaEventRecord(g_pipe.ev_q[b], s));
-            if (!bary) {
-                CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));
-                CK(cudaMemcpyAsync(h_flags + lo, dflag[b], 4ull * cnt, cudaMemcpyDeviceToHost, cp));
-                CK(cudaEventRecord(g_pipe.ev_out[b], cp));
-            }
-            continue;
-        }
-        QueryArgs a = make_args(t, din[b][0], din[b][1], cnt, max_coll, max_stack, st + k);
-        a.ray_offset = lo;
-        if (bary) {
-            // each chunk compacts into its own region; rows are concatenated on the host
-            a.c_ray = dray + lo;
-            a.c_dist = ddist + lo;
-            a.c_tri = dtri + lo;
-            a.c_point = dpt + 3 * lo;
-            a.tile_status = reinterpret_cast<unsigned long long*>(
-                tiles + align256(compact_scratch_bytes(chunk_rays)) * k);
         } else {
-            a.detected = dflag[b];
-            a.counts = dflag[b];
+            QueryArgs a = make_args(t, din[b][0], din[b][1], cnt, max_coll, max_stack, st + k);
+            a.ray_offset = lo;
+            if (bary) {
+                // each chunk compacts into its own region; rows are concatenated on the host
+                a.c_ray = dray + lo;
+                a.c_dist = ddist + lo;
+                a.c_tri = dtri + lo;
+                a.c_point = dpt + 3 * lo;
+                a.tile_status = reinterpret_cast<unsigned long long*>(
+                    tiles + align256(compact_scratch_bytes(chunk_rays)) * k);
+            } else {
+                a.detected = dflag[b];
+                a.counts = dflag[b];
+            }
+            if (launch_query(a, mode, ref != 0, bary, kstack_for(ref != 0, max_stack), false, s)) {
+                rs_free(t, stream);
+                cudaFreeAsync(blk, s);
+                return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
+            }
+            CK(cudaGetLastError());
         }
-        if (launch_query(a, mode, ref != 0, bary, kstack_for(ref != 0, max_stack), false, s)) {
-            rs_free(t, stream);
-            cudaFreeAsync(blk, s);
-            return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
-        }
-        CK(cudaGetLastError());
         CK(cudaEventRecord(g_pipe.ev_q[b], s));
         if (!bary) {
-            CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[b], 0));
-            CK(cudaMemcpyAsync(h_flags + lo, dflag[b], 4ull * cnt, cudaMemcpyDeviceToHost, cp));
-            CK(cudaEventRecord(g_pipe.ev_out[b], cp));
+            CK(cudaStreamWaitEvent(d2h, g_pipe.ev_q[b], 0));
+            CK(cudaMemcpyAsync(h_flags + lo, dflag[b], 4ull * cnt, cudaMemcpyDeviceToHost, d2h));
+            CK(cudaEventRecord(g_pipe.ev_out[b], d2h));
         }
     }
+    cp = d2h;
     // statuses of every chunk; barycentric row counts come back with them
     RsStatus* hst = new RsStatus[nchunks];
     CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[(nchunks - 1) & 1], 0));

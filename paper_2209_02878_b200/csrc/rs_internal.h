@@ -145,18 +145,26 @@ struct SortedArgs {
     unsigned* bins;      // sorted_bins() counters (zeroed)
     unsigned* cursor;    // sorted_bins() scatter cursors
     unsigned* n_live;    // live segment count (written by the scan)
+    float* seg_stats;    // k_seg_sample: per-CTA (sum of box sides x/y/z, live count)
     unsigned* tile_sum;  // sorted_bins()/1024 per-tile counts (zeroed) -> tile offsets
     float4* rec;         // n_r x 32-B records (start, id, end)
     int* flags;                  // boolean / count output (pre-zeroed)
     unsigned long long* best_t;  // barycentric (pre-set ~0)
     int* best_tri;               // barycentric (pre-set -1)
     RsStatus* status;
+    unsigned bin_occupancy;  // binning: target live segments per bin (set at launch)
+    unsigned tile_area;  // tile traversal: target triangles' worth of records per tile (set at launch)
+    unsigned tile_balance;      // tile traversal: at least this many tiles per CTA
+    unsigned tile_min_density;  // tile traversal only above this many records per triangle
 };
 size_t sorted_bins();
 bool sorted_wide();  // RS_SORTED_WIDE=1: 4-wide per-thread traversal (needs nodes4)
 // binning needs only the header's root box (available right after k_prep)
 void launch_binning(const SortedArgs& a, cudaStream_t s);
 void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t s);
+// Tuning knob by name (trav, tile_density, tile_balance, tile_area,
+// bin_occupancy); value < 0 (or 0 for counts) only reads.  -1: unknown name.
+int sorted_option(const char* name, long long value, long long* old);
 void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);
 size_t bary_compact_scratch(long long n_r);
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s);

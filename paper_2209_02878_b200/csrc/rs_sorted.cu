@@ -28,12 +28,14 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 namespace rs {
 
 constexpr unsigned kFullMask = 0xffffffffu;
-constexpr int kAxisBits = 7;                 // bins per axis = 128
-constexpr int kBinBits = 3 * kAxisBits;
+constexpr int kBinBits = 21;                 // up to 2M spatial bins
+constexpr int kSampleCtas = 32;              // k_seg_sample grid
+constexpr int kSampleThreads = 128;
 constexpr int kBins = 1 << kBinBits;
 constexpr int kScanShift = 10;
 constexpr int kScanTile = 1 << kScanShift;
@@ -57,32 +59,104 @@ __device__ __forceinline__ bool slot_hit(const float f[8], const float b[6]) {
            (b[3] >= f[2]) & (b[4] <= f[5]) & (b[5] >= f[4]);
 }
 
-__device__ __forceinline__ unsigned spread_bits(unsigned v) {  // bit i -> bit 3i
-    unsigned r = 0;
-#pragma unroll
-    for (int i = 0; i < kAxisBits; ++i) r |= ((v >> i) & 1u) << (3 * i);
-    return r;
+__device__ __forceinline__ unsigned spread3(unsigned v) {  // bit i -> bit 3i (i < 10)
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__device__ __forceinline__ unsigned spread2(unsigned v) {  // bit i -> bit 2i (i < 16)
+    v &= 0xffffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
 }
 
-// Root box + culling helper shared by both binning passes.
+// Root box + bin geometry shared by both binning passes.  The 21 key bits
+// are shared out so that cells are as close to cubes as the root box allows
+// (greedy: the next bit halves the currently longest cell side): a flat
+// terrain gets fine xy cells and few z cells instead of 128 per axis.
+// Axes are ranked by bit count (A >= B >= C); the key interleaves all three
+// over C's bits, then A and B, then A alone (a Morton order with unequal
+// axis resolutions).
 struct RootInfo {
-    float lo[3], hi[3], inv[3];
+    float lo[3], hi[3], scale[3];
+    int qmax[3];
+    int pa, pb, pc;  // axes by bit count, descending
+    int bb, bc;      // bits of B and C
 };
 
 // The root box (union of all triangle boxes) comes from the build's k_prep,
 // so the binning can run concurrently with the rest of the build.
-__device__ __forceinline__ void root_info(const RsHeader* hdr, RootInfo& ri) {
-    float hi[3];
+__device__ __forceinline__ void root_info_compute(const RsHeader* hdr, const SortedArgs& a,
+                                                  RootInfo& ri) {
+    float e0, e1, e2;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         ri.lo[k] = from_ord32(~__ldg(&hdr->bmin[k]));
-        hi[k] = from_ord32(__ldg(&hdr->bmax[k]));
+        ri.hi[k] = from_ord32(__ldg(&hdr->bmax[k]));
     }
+    e0 = fmaxf(ri.hi[0] - ri.lo[0], 0.f);
+    e1 = fmaxf(ri.hi[1] - ri.lo[1], 0.f);
+    e2 = fmaxf(ri.hi[2] - ri.lo[2], 0.f);
+    float st[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < kSampleCtas; ++c)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) ri.hi[k] = hi[k];
-    const float ext = fmaxf(fmaxf(hi[0] - ri.lo[0], hi[1] - ri.lo[1]), fmaxf(hi[2] - ri.lo[2], 1e-30f));
-#pragma unroll
-    for (int k = 0; k < 3; ++k) ri.inv[k] = ((float)(1 << kAxisBits) - 0.01f) / ext;
+        for (int k = 0; k < 4; ++k) st[k] += a.seg_stats[4 * c + k];
+    // a cell side below the typical segment-box side along that axis buys
+    // no coherence (neighbouring boxes overlap anyway): such an axis only
+    // gets bits once every other axis is that fine too
+    const float f0 = st[3] > 0.f ? st[0] / st[3] : 0.f;
+    const float f1 = st[3] > 0.f ? st[1] / st[3] : 0.f;
+    const float f2 = st[3] > 0.f ? st[2] / st[3] : 0.f;
+    // total bits: about a.bin_occupancy live segments per bin, so the bins'
+    // open output lines stay L2-resident during the scatter
+    const double live = (double)a.n_r * (st[3] / (float)(kSampleCtas * kSampleThreads));
+    int nbits = 0;
+    while (nbits < kBinBits && (double)(1u << (nbits + 1)) * a.bin_occupancy <= live) ++nbits;
+    nbits = nbits < 8 ? 8 : nbits;
+    float c0 = e0, c1 = e1, c2 = e2;
+    int b0 = 0, b1 = 0, b2 = 0;
+    for (int i = 0; i < nbits; ++i) {
+        const float g0 = c0 > f0 ? c0 : 0.f, g1 = c1 > f1 ? c1 : 0.f, g2 = c2 > f2 ? c2 : 0.f;
+        const bool any = (g0 > 0.f) | (g1 > 0.f) | (g2 > 0.f);
+        const float h0 = any ? g0 : c0, h1 = any ? g1 : c1, h2 = any ? g2 : c2;
+        if (h0 >= h1 && h0 >= h2) { ++b0; c0 *= 0.5f; }
+        else if (h1 >= h2) { ++b1; c1 *= 0.5f; }
+        else { ++b2; c2 *= 0.5f; }
+    }
+    ri.qmax[0] = (1 << b0) - 1; ri.qmax[1] = (1 << b1) - 1; ri.qmax[2] = (1 << b2) - 1;
+    ri.scale[0] = e0 > 0.f ? (float)(1 << b0) / e0 : 0.f;
+    ri.scale[1] = e1 > 0.f ? (float)(1 << b1) / e1 : 0.f;
+    ri.scale[2] = e2 > 0.f ? (float)(1 << b2) / e2 : 0.f;
+    // rank the axes by bit count (ties: lower axis first)
+    const int pa = (b0 >= b1 && b0 >= b2) ? 0 : (b1 >= b2 ? 1 : 2);
+    int pc;
+    if (pa == 0) pc = b2 < b1 ? 2 : 1;
+    else if (pa == 1) pc = b2 < b0 ? 2 : 0;
+    else pc = b1 < b0 ? 1 : 0;
+    ri.pa = pa;
+    ri.pc = pc;
+    ri.pb = 3 - pa - pc;
+    const int bits[3] = {b0, b1, b2};
+    ri.bb = bits[ri.pb];
+    ri.bc = bits[pc];
+}
+
+// One thread derives the bin geometry; the CTA reads it from shared memory.
+__device__ __forceinline__ void root_info(const SortedArgs& a, RootInfo& ri) {
+    __shared__ RootInfo s_ri;
+    if (threadIdx.x == 0) root_info_compute(a.hdr, a, s_ri);
+    __syncthreads();
+    ri = s_ri;
+}
+
+__device__ __forceinline__ unsigned pick3(const unsigned q[3], int k) {
+    return k == 0 ? q[0] : (k == 1 ? q[1] : q[2]);
 }
 
 // Returns the bin of a live segment, or -1 when its box misses the root box
@@ -95,13 +169,19 @@ __device__ __forceinline__ int seg_bin(const float s[3], const float e[3], const
     const bool live = (b[0] <= ri.hi[0]) & (b[1] >= ri.lo[0]) & (b[2] <= ri.hi[1]) &
                       (b[3] >= ri.lo[1]) & (b[4] <= ri.hi[2]) & (b[5] >= ri.lo[2]);
     if (!live) return -1;
-    unsigned key = 0;
+    unsigned q[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const float c = 0.5f * (b[2 * k] + b[2 * k + 1]);
-        const float q = fminf(fmaxf((c - ri.lo[k]) * ri.inv[k], 0.f), (float)((1 << kAxisBits) - 1));
-        key |= spread_bits((unsigned)q) << k;
+        const float f = fminf(fmaxf((c - ri.lo[k]) * ri.scale[k], 0.f), (float)ri.qmax[k]);
+        q[k] = (unsigned)f;
     }
+    const unsigned qa = pick3(q, ri.pa), qb = pick3(q, ri.pb), qc = pick3(q, ri.pc);
+    const unsigned mc = (1u << ri.bc) - 1u;
+    const unsigned mb = (1u << (ri.bb - ri.bc)) - 1u;
+    unsigned key = spread3(qa & mc) | (spread3(qb & mc) << 1) | (spread3(qc) << 2);
+    key |= (spread2((qa >> ri.bc) & mb) | (spread2((qb >> ri.bc) & mb) << 1)) << (3 * ri.bc);
+    key |= (qa >> ri.bb) << (2 * ri.bb + ri.bc);
     return (int)key;
 }
 
@@ -141,10 +221,58 @@ __device__ __forceinline__ int load4(const float* __restrict__ S, const float* _
     return cnt;
 }
 
+// Sample statistics over a fixed strided sample of kSampleCtas x 128
+// segments: per CTA, the summed box sides of the sampled segments that
+// overlap the root box and their count.  root_info_compute sums the CTA
+// partials in a fixed order (deterministic) and derives the bin geometry.
+__global__ void __launch_bounds__(kSampleThreads) k_seg_sample(SortedArgs a) {
+    __shared__ float red[4][kSampleThreads / 32];
+    float lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = from_ord32(~__ldg(&a.hdr->bmin[k]));
+        hi[k] = from_ord32(__ldg(&a.hdr->bmax[k]));
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const long long n_s = (long long)kSampleCtas * kSampleThreads;
+    const long long stride = a.n_r / n_s > 0 ? a.n_r / n_s : 1;
+    const long long i = ((long long)blockIdx.x * kSampleThreads + threadIdx.x) * stride;
+    if (i < a.n_r) {
+        float b[6];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float p = __ldg(a.starts + 3 * i + k), q = __ldg(a.ends + 3 * i + k);
+            b[2 * k] = fminf(p, q);
+            b[2 * k + 1] = fmaxf(p, q);
+        }
+        const bool live = (b[0] <= hi[0]) & (b[1] >= lo[0]) & (b[2] <= hi[1]) & (b[3] >= lo[1]) &
+                          (b[4] <= hi[2]) & (b[5] >= lo[2]);
+        if (live) {
+            acc[0] = b[1] - b[0];
+            acc[1] = b[3] - b[2];
+            acc[2] = b[5] - b[4];
+            acc[3] = 1.f;
+        }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float v = acc[k];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+        if (lane == 0) red[k][w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        float v = 0.f;
+        for (int j = 0; j < kSampleThreads / 32; ++j) v += red[threadIdx.x][j];
+        a.seg_stats[4 * blockIdx.x + threadIdx.x] = v;
+    }
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
     RootInfo ri;
-    root_info(a.hdr, ri);
+    root_info(a, ri);
     const long long nq = (a.n_r + 3) / 4;
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
         float s[4][3], e[4][3];
@@ -227,7 +355,7 @@ __global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
     RootInfo ri;
-    root_info(a.hdr, ri);
+    root_info(a, ri);
     const long long nq = (a.n_r + 3) / 4;
     const int lane = threadIdx.x & 31;
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
@@ -364,75 +492,411 @@ __device__ __forceinline__ void leaf_exact(const RsLeaf* __restrict__ leaves, in
     }
 }
 
-// Binary-node traversal (default): the coherent record order over the 64-B
-// RsNode records (two 256-bit loads per visit).
+// One segment's stack traversal of the binary tree (RsNode records, two
+// 256-bit loads per visit) with the exact test at the leaves
+// (_core.pyx:255-322 semantics, order-free accumulation).
+template <int MODE>
+__device__ __forceinline__ void trav_one(const RsSlot* __restrict__ nodes,
+                                         const RsLeaf* __restrict__ leaves, int n_int, int root,
+                                         float4 r0, float4 r1, int& det, int& nh, int& btri,
+                                         double& bt, bool& ovf) {
+    int stack[kSortedStack];
+    const float b0 = fminf(r0.x, r1.x), b1 = fmaxf(r0.x, r1.x);
+    const float b2 = fminf(r0.y, r1.y), b3 = fmaxf(r0.y, r1.y);
+    const float b4 = fminf(r0.z, r1.z), b5 = fmaxf(r0.z, r1.z);
+    if (n_int == 0) {  // single triangle: the leaf is the root (_core.pyx:260-267)
+        const float4 p0 = __ldg(&leaves[0].p0), p1 = __ldg(&leaves[0].p1), p2 = __ldg(&leaves[0].p2);
+        const bool o = (b0 <= fmaxf(fmaxf(p0.x, p0.w), p1.z)) & (b1 >= fminf(fminf(p0.x, p0.w), p1.z)) &
+                       (b2 <= fmaxf(fmaxf(p0.y, p1.x), p1.w)) & (b3 >= fminf(fminf(p0.y, p1.x), p1.w)) &
+                       (b4 <= fmaxf(fmaxf(p0.z, p1.y), p2.x)) & (b5 >= fminf(fminf(p0.z, p1.y), p2.x));
+        if (o) leaf_exact<MODE>(leaves, 0, r0, r1, det, nh, btri, bt);
+        return;
+    }
+    int top = 0, node = root;
+    for (;;) {
+        float f0[8], f1[8];
+        ld_slot(nodes + 2 * node, f0);
+        ld_slot(nodes + 2 * node + 1, f1);
+        // RsNode: [l.x0 l.x1 l.y0 l.y1 l.z0 l.z1 r.x0 r.x1] [r.y0 r.y1 r.z0 r.z1 lref rref - -]
+        const int ca = __float_as_int(f1[4]), cb = __float_as_int(f1[5]);
+        const bool oa = (b0 <= f0[1]) & (b1 >= f0[0]) & (b2 <= f0[3]) & (b3 >= f0[2]) &
+                        (b4 <= f0[5]) & (b5 >= f0[4]);
+        const bool ob = (b0 <= f0[7]) & (b1 >= f0[6]) & (b2 <= f1[1]) & (b3 >= f1[0]) &
+                        (b4 <= f1[3]) & (b5 >= f1[2]);
+        const bool la = ca >= n_int, lb = cb >= n_int;
+        if (oa & la) leaf_exact<MODE>(leaves, ca - n_int, r0, r1, det, nh, btri, bt);
+        if (ob & lb) leaf_exact<MODE>(leaves, cb - n_int, r0, r1, det, nh, btri, bt);
+        if (MODE == kBoolean && det) break;
+        const bool ta = oa & !la, tb = ob & !lb;
+        if (ta & tb) {
+            if (top < kSortedStack) stack[top++] = cb;
+            else ovf = true;
+        }
+        if (ta | tb) {
+            node = ta ? ca : cb;
+        } else if (top > 0) {
+            node = stack[--top];
+        } else {
+            break;
+        }
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void write_result(const SortedArgs& a, int id, int det, int nh,
+                                             int btri, double bt) {
+    if (MODE == kBoolean) {
+        if (det) a.flags[id] = 1;
+    } else if (MODE == kCount) {
+        if (nh) a.flags[id] = nh;
+    } else if (btri >= 0) {
+        a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
+        a.best_tri[id] = btri;
+    }
+}
+
+// Binary-node traversal, one thread per record in the coherent record order.
 template <int MODE>
 __global__ void __launch_bounds__(kSortedThreads, kSortedMinBlocks) k_trav_sorted_bin(SortedArgs a) {
     const unsigned n_live = *a.n_live;
     const int n_int = a.n_int;
     const int root = n_int > 0 ? __ldg(&a.hdr->root) : 0;
     const RsSlot* const nodes = reinterpret_cast<const RsSlot*>(a.nodes);
-    const RsLeaf* const leaves = a.leaves;
-    const float4* const rec = a.rec;
-    int stack[kSortedStack];
     const unsigned per_cta = ((n_live + gridDim.x - 1) / gridDim.x + kSortedThreads - 1) /
                              kSortedThreads * kSortedThreads;
     const unsigned beg = blockIdx.x * per_cta;
     const unsigned end = beg + per_cta < n_live ? beg + per_cta : n_live;
     for (unsigned idx = beg + threadIdx.x; idx < end; idx += kSortedThreads) {
-        const float4 r0 = rec[2 * idx], r1 = rec[2 * idx + 1];
-        const int id = __float_as_int(r0.w);
-        const float b0 = fminf(r0.x, r1.x), b1 = fmaxf(r0.x, r1.x);
-        const float b2 = fminf(r0.y, r1.y), b3 = fmaxf(r0.y, r1.y);
-        const float b4 = fminf(r0.z, r1.z), b5 = fmaxf(r0.z, r1.z);
+        const float4 r0 = a.rec[2 * idx], r1 = a.rec[2 * idx + 1];
         int det = 0, nh = 0, btri = -1;
         double bt = 0.0;
-        int top = 0, node = root;
         bool ovf = false;
-        if (n_int == 0) {  // single triangle: the leaf is the root (_core.pyx:260-267)
-            const float4 p0 = __ldg(&leaves[0].p0), p1 = __ldg(&leaves[0].p1), p2 = __ldg(&leaves[0].p2);
-            const bool o = (b0 <= fmaxf(fmaxf(p0.x, p0.w), p1.z)) & (b1 >= fminf(fminf(p0.x, p0.w), p1.z)) &
-                           (b2 <= fmaxf(fmaxf(p0.y, p1.x), p1.w)) & (b3 >= fminf(fminf(p0.y, p1.x), p1.w)) &
-                           (b4 <= fmaxf(fmaxf(p0.z, p1.y), p2.x)) & (b5 >= fminf(fminf(p0.z, p1.y), p2.x));
-            if (o) leaf_exact<MODE>(leaves, 0, r0, r1, det, nh, btri, bt);
-        } else {
-            for (;;) {
+        trav_one<MODE>(nodes, a.leaves, n_int, root, r0, r1, det, nh, btri, bt, ovf);
+        if (ovf) atomicAdd(&a.status->internal, 1ull);
+        write_result<MODE>(a, __float_as_int(r0.w), det, nh, btri, bt);
+    }
+}
+
+// ---- tile traversal (default) ---------------------------------------------
+//
+// The records are in spatial-bin order, so a contiguous run of them (a tile)
+// covers a small region.  One CTA per tile:
+//   1. union box U of the tile's segment boxes (block reduction);
+//   2. cooperative breadth-first walk of the tree with U: every leaf whose
+//      exact box overlaps U goes to a shared-memory candidate list L.  Any
+//      leaf overlapping a segment's box overlaps U (the segment box is inside
+//      U and every internal box contains its subtree's boxes), so L holds
+//      every candidate of every segment of the tile;
+//   3. per warp of 32 records: the warp's union box W filters L (one ballot
+//      per 32 entries); each lane then runs the exact f32 box test of its own
+//      segment against the surviving entries (broadcast shared-memory reads)
+//      and the f64 Moller-Trumbore test on its overlaps.
+// The top of the tree is walked once per tile instead of once per segment,
+// and the per-segment loop has no stack and no dependent global loads.
+// A tile whose walk exceeds the shared-memory capacities (huge segments,
+// random soups) falls back to trav_one for its records.
+constexpr int kTileThreads = 128;
+#ifndef RS_TILE_MIN_BLOCKS
+#define RS_TILE_MIN_BLOCKS 8
+#endif
+constexpr int kTileMinBlocks = RS_TILE_MIN_BLOCKS;
+constexpr int kTileLCap = 512;  // leaf candidates per tile
+constexpr int kTileFCap = 256;  // walk frontier per level
+constexpr int kCutDepth = 6;    // the walk starts from the tree's depth-6 cut
+constexpr int kCutCap = 1 << kCutDepth;
+constexpr int kLaneCand = 8;    // per-lane candidate slots between exact-test passes
+
+struct TileSmem {
+    float4 lxy[kTileLCap];  // leaf box x0 x1 y0 y1
+    float2 lz[kTileLCap];   // z0 z1
+    int lid[kTileLCap];     // leaf index (Morton order)
+    int front[2][kTileFCap];
+    float4 cxy[kCutCap];    // the cut: entry boxes and refs (built once per CTA)
+    float2 cz[kCutCap];
+    int cref[kCutCap];
+    unsigned short cand[kTileThreads / 32][kLaneCand][32];
+    float part[kTileThreads / 32][6];
+    int nf[3];
+    int nl;
+    int ovf;
+    int ncut;
+    unsigned tile;
+};
+
+__device__ __forceinline__ float wred_min(float v) {
+    float r;
+    asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
+__device__ __forceinline__ float wred_max(float v) {
+    float r;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
+
+__device__ __forceinline__ bool box_ov(const float q[6], float4 xy, float2 z) {
+    return (q[0] <= xy.y) & (q[1] >= xy.x) & (q[2] <= xy.w) & (q[3] >= xy.z) & (q[4] <= z.y) &
+           (q[5] >= z.x);
+}
+
+// Out-of-line fallback (keeps the tile loop's registers free).
+template <int MODE>
+__device__ __noinline__ void trav_one_call(const SortedArgs& a, const RsSlot* nodes, int root,
+                                           float4 r0, float4 r1, int& det, int& nh, int& btri,
+                                           double& bt) {
+    bool ovf = false;
+    trav_one<MODE>(nodes, a.leaves, a.n_int, root, r0, r1, det, nh, btri, bt, ovf);
+    if (ovf) atomicAdd(&a.status->internal, 1ull);
+}
+
+// The depth-kCutDepth cut of the tree (every node at that depth, plus the
+// leaves above it), with each entry's exact box taken from its parent's
+// record.  Warp 0 builds it once per CTA; every tile's walk starts from it.
+__device__ __forceinline__ void build_cut(TileSmem& sm, const RsSlot* nodes, int n_int, int root) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    // level 0: the root's two children
+    int n = 0;
+    if (lane == 0) {
+        float f0[8], f1[8];
+        ld_slot(nodes + 2 * root, f0);
+        ld_slot(nodes + 2 * root + 1, f1);
+        sm.cxy[0] = make_float4(f0[0], f0[1], f0[2], f0[3]);
+        sm.cz[0] = make_float2(f0[4], f0[5]);
+        sm.cref[0] = __float_as_int(f1[4]);
+        sm.cxy[1] = make_float4(f0[6], f0[7], f1[0], f1[1]);
+        sm.cz[1] = make_float2(f1[2], f1[3]);
+        sm.cref[1] = __float_as_int(f1[5]);
+    }
+    n = 2;
+    __syncwarp();
+    for (int d = 1; d < kCutDepth; ++d) {
+        // expand every internal entry into its two children (in place: entry
+        // i's children go to slots i and n + (rank of i among internals))
+        float4 xy[2];
+        float2 z[2];
+        int ref = -1, c0 = -1, c1 = -1;
+        bool internal = false;
+        if (lane < n) {
+            ref = sm.cref[lane];
+            internal = ref < n_int;
+            if (internal) {
                 float f0[8], f1[8];
-                ld_slot(nodes + 2 * node, f0);
-                ld_slot(nodes + 2 * node + 1, f1);
-                // RsNode: [l.x0 l.x1 l.y0 l.y1 l.z0 l.z1 r.x0 r.x1] [r.y0 r.y1 r.z0 r.z1 lref rref - -]
-                const int ca = __float_as_int(f1[4]), cb = __float_as_int(f1[5]);
-                const bool oa = (b0 <= f0[1]) & (b1 >= f0[0]) & (b2 <= f0[3]) & (b3 >= f0[2]) &
-                                (b4 <= f0[5]) & (b5 >= f0[4]);
-                const bool ob = (b0 <= f0[7]) & (b1 >= f0[6]) & (b2 <= f1[1]) & (b3 >= f1[0]) &
-                                (b4 <= f1[3]) & (b5 >= f1[2]);
-                const bool la = ca >= n_int, lb = cb >= n_int;
-                if (oa & la) leaf_exact<MODE>(leaves, ca - n_int, r0, r1, det, nh, btri, bt);
-                if (ob & lb) leaf_exact<MODE>(leaves, cb - n_int, r0, r1, det, nh, btri, bt);
-                if (MODE == kBoolean && det) break;
-                const bool ta = oa & !la, tb = ob & !lb;
-                if (ta & tb) {
-                    if (top < kSortedStack) stack[top++] = cb;
-                    else ovf = true;
-                }
-                if (ta | tb) {
-                    node = ta ? ca : cb;
-                } else if (top > 0) {
-                    node = stack[--top];
+                ld_slot(nodes + 2 * ref, f0);
+                ld_slot(nodes + 2 * ref + 1, f1);
+                xy[0] = make_float4(f0[0], f0[1], f0[2], f0[3]);
+                z[0] = make_float2(f0[4], f0[5]);
+                c0 = __float_as_int(f1[4]);
+                xy[1] = make_float4(f0[6], f0[7], f1[0], f1[1]);
+                z[1] = make_float2(f1[2], f1[3]);
+                c1 = __float_as_int(f1[5]);
+            }
+        }
+        const unsigned m = __ballot_sync(kFullMask, internal);
+        __syncwarp();
+        if (internal) {
+            const int extra = n + __popc(m & ((1u << lane) - 1u));
+            sm.cxy[lane] = xy[0]; sm.cz[lane] = z[0]; sm.cref[lane] = c0;
+            sm.cxy[extra] = xy[1]; sm.cz[extra] = z[1]; sm.cref[extra] = c1;
+        }
+        n += __popc(m);
+        __syncwarp();
+    }
+    if (lane == 0) sm.ncut = n;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(SortedArgs a) {
+    __shared__ TileSmem sm;
+    const unsigned n_live = *a.n_live;
+    const int n_int = a.n_int;
+    const int root = __ldg(&a.hdr->root);
+    const RsSlot* const nodes = reinterpret_cast<const RsSlot*>(a.nodes);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // tile size: about a.tile_area triangles' worth of records, but at least
+    // a.tile_balance tiles per CTA; a multiple of the CTA size
+    unsigned T = (unsigned)((unsigned long long)a.tile_area * n_live / (unsigned)(n_int + 1));
+    const unsigned per = a.tile_balance * gridDim.x;
+    const unsigned bal = (n_live + per - 1) / per;
+    T = T < bal ? T : bal;
+    T = (T + kTileThreads - 1) / kTileThreads * kTileThreads;
+    T = T < kTileThreads ? kTileThreads : (T > 16384 ? 16384 : T);
+    const unsigned n_tiles = (n_live + T - 1) / T;
+    build_cut(sm, nodes, n_int, root);
+    if (tid == 0) sm.tile = atomicAdd(reinterpret_cast<unsigned*>(&a.status->tile_counter), 1u);
+    __syncthreads();
+    const int ncut = sm.ncut;
+    for (;;) {
+        const unsigned tile = sm.tile;
+        if (tile >= n_tiles) break;
+        const unsigned beg = tile * T;
+        const unsigned end = beg + T < n_live ? beg + T : n_live;
+        // 1. union box U of the tile's segment boxes
+        float u[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
+        for (unsigned idx = beg + tid; idx < end; idx += kTileThreads) {
+            const float4 r0 = a.rec[2 * idx], r1 = a.rec[2 * idx + 1];
+            u[0] = fminf(u[0], fminf(r0.x, r1.x)); u[1] = fmaxf(u[1], fmaxf(r0.x, r1.x));
+            u[2] = fminf(u[2], fminf(r0.y, r1.y)); u[3] = fmaxf(u[3], fmaxf(r0.y, r1.y));
+            u[4] = fminf(u[4], fminf(r0.z, r1.z)); u[5] = fmaxf(u[5], fmaxf(r0.z, r1.z));
+        }
+#pragma unroll
+        for (int k = 0; k < 6; k += 2) {
+            u[k] = wred_min(u[k]);
+            u[k + 1] = wred_max(u[k + 1]);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) sm.part[warp][k] = u[k];
+        }
+        if (tid == 0) {
+            sm.nf[0] = 0; sm.nf[1] = 0; sm.nf[2] = 0;
+            sm.nl = 0;
+            sm.ovf = 0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kTileThreads / 32; ++w)
+#pragma unroll
+            for (int k = 0; k < 6; k += 2) {
+                if (w == 0) { u[k] = sm.part[0][k]; u[k + 1] = sm.part[0][k + 1]; }
+                else { u[k] = fminf(u[k], sm.part[w][k]); u[k + 1] = fmaxf(u[k + 1], sm.part[w][k + 1]); }
+            }
+        // 2. breadth-first walk with U, from the cut
+        if (tid < ncut) {
+            const int ref = sm.cref[tid];
+            if (box_ov(u, sm.cxy[tid], sm.cz[tid])) {
+                if (ref >= n_int) {
+                    const int k = atomicAdd(&sm.nl, 1);
+                    sm.lxy[k] = sm.cxy[tid];
+                    sm.lz[k] = sm.cz[tid];
+                    sm.lid[k] = ref - n_int;
                 } else {
-                    break;
+                    sm.front[0][atomicAdd(&sm.nf[0], 1)] = ref;
                 }
             }
         }
-        if (ovf) atomicAdd(&a.status->internal, 1ull);
-        if (MODE == kBoolean) {
-            if (det) a.flags[id] = 1;
-        } else if (MODE == kCount) {
-            if (nh) a.flags[id] = nh;
-        } else if (btri >= 0) {
-            a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
-            a.best_tri[id] = btri;
+        __syncthreads();
+        for (int level = 0;; ++level) {
+            const int n = sm.nf[level % 3];
+            if (n == 0 || sm.ovf) break;
+            const int* cur = sm.front[level & 1];
+            int* nxt = sm.front[(level + 1) & 1];
+            int* nnf = &sm.nf[(level + 1) % 3];
+            if (tid == 0) sm.nf[(level + 2) % 3] = 0;
+            for (int i = tid; i < n; i += kTileThreads) {
+                const int node = cur[i];
+                float f0[8], f1[8];
+                ld_slot(nodes + 2 * node, f0);
+                ld_slot(nodes + 2 * node + 1, f1);
+                const int ca = __float_as_int(f1[4]), cb = __float_as_int(f1[5]);
+                const bool oa = (u[0] <= f0[1]) & (u[1] >= f0[0]) & (u[2] <= f0[3]) & (u[3] >= f0[2]) &
+                                (u[4] <= f0[5]) & (u[5] >= f0[4]);
+                const bool ob = (u[0] <= f0[7]) & (u[1] >= f0[6]) & (u[2] <= f1[1]) & (u[3] >= f1[0]) &
+                                (u[4] <= f1[3]) & (u[5] >= f1[2]);
+                if (oa) {
+                    if (ca >= n_int) {
+                        const int k = atomicAdd(&sm.nl, 1);
+                        if (k < kTileLCap) {
+                            sm.lxy[k] = make_float4(f0[0], f0[1], f0[2], f0[3]);
+                            sm.lz[k] = make_float2(f0[4], f0[5]);
+                            sm.lid[k] = ca - n_int;
+                        } else {
+                            sm.ovf = 1;
+                        }
+                    } else {
+                        const int k = atomicAdd(nnf, 1);
+                        if (k < kTileFCap) nxt[k] = ca;
+                        else sm.ovf = 1;
+                    }
+                }
+                if (ob) {
+                    if (cb >= n_int) {
+                        const int k = atomicAdd(&sm.nl, 1);
+                        if (k < kTileLCap) {
+                            sm.lxy[k] = make_float4(f0[6], f0[7], f1[0], f1[1]);
+                            sm.lz[k] = make_float2(f1[2], f1[3]);
+                            sm.lid[k] = cb - n_int;
+                        } else {
+                            sm.ovf = 1;
+                        }
+                    } else {
+                        const int k = atomicAdd(nnf, 1);
+                        if (k < kTileFCap) nxt[k] = cb;
+                        else sm.ovf = 1;
+                    }
+                }
+            }
+            __syncthreads();
         }
+        const bool fallback = sm.ovf != 0;
+        const int nl = sm.nl;
+#ifdef RS_TILE_STATS
+        if (tid == 0) {
+            atomicAdd(&a.status->visits, (unsigned long long)nl);
+            if (fallback) atomicAdd(&a.status->cand_count, 1ull);
+        }
+#endif
+        // 3. segments, one warp per 32 consecutive records
+        for (unsigned base = beg + warp * 32; base < end; base += kTileThreads) {
+            const unsigned idx = base + lane;
+            const bool valid = idx < end;
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+            if (valid) { r0 = a.rec[2 * idx]; r1 = a.rec[2 * idx + 1]; }
+            int det = 0, nh = 0, btri = -1;
+            double bt = 0.0;
+            if (fallback) {
+                if (valid) trav_one_call<MODE>(a, nodes, root, r0, r1, det, nh, btri, bt);
+            } else {
+                float b[6];
+                b[0] = fminf(r0.x, r1.x); b[1] = fmaxf(r0.x, r1.x);
+                b[2] = fminf(r0.y, r1.y); b[3] = fmaxf(r0.y, r1.y);
+                b[4] = fminf(r0.z, r1.z); b[5] = fmaxf(r0.z, r1.z);
+                float w[6];
+#pragma unroll
+                for (int k = 0; k < 6; k += 2) {
+                    w[k] = wred_min(valid ? b[k] : INFINITY);
+                    w[k + 1] = wred_max(valid ? b[k + 1] : -INFINITY);
+                }
+                // candidates: L filtered by the warp box, then by the lane's
+                // own box; the exact tests run in passes over the per-lane
+                // slots so the warp executes each pass once
+                bool live = valid;
+                int nc = 0;
+                unsigned short(*slots)[32] = sm.cand[warp];
+                auto pass = [&]() {
+                    const int most = __reduce_max_sync(kFullMask, nc);
+                    for (int i = 0; i < most; ++i) {
+                        if (i < nc && live) {
+#ifdef RS_TILE_STATS
+                            atomicAdd(&a.status->mts, 1ull);
+#endif
+                            leaf_exact<MODE>(a.leaves, sm.lid[slots[i][lane]], r0, r1, det, nh, btri, bt);
+                            if (MODE == kBoolean && det) live = false;
+                        }
+                    }
+                    nc = 0;
+                };
+                for (int cb = 0; cb < nl; cb += 32) {
+                    const int j = cb + lane;
+                    const bool hit = j < nl && box_ov(w, sm.lxy[j], sm.lz[j]);
+                    unsigned m = __ballot_sync(kFullMask, hit);
+                    while (m) {
+                        const int k = cb + __ffs(m) - 1;
+                        m &= m - 1;
+#ifdef RS_TILE_STATS
+                        if (lane == 0) atomicAdd(&a.status->pad, 1ull);
+#endif
+                        if (live && box_ov(b, sm.lxy[k], sm.lz[k])) slots[nc++][lane] = (unsigned short)k;
+                        if (__any_sync(kFullMask, nc == kLaneCand)) pass();
+                    }
+                }
+                pass();
+            }
+            if (valid) write_result<MODE>(a, __float_as_int(r0.w), det, nh, btri, bt);
+        }
+        __syncthreads();  // the next tile reuses the shared lists
+        if (tid == 0) sm.tile = atomicAdd(reinterpret_cast<unsigned*>(&a.status->tile_counter), 1u);
+        __syncthreads();
     }
 }
 
@@ -458,10 +922,15 @@ bool sorted_wide() {
     return wide;
 }
 
-void launch_binning(const SortedArgs& a, cudaStream_t s) {
+static unsigned bin_occupancy();
+
+void launch_binning(const SortedArgs& a0, cudaStream_t s) {
+    SortedArgs a = a0;
+    a.bin_occupancy = bin_occupancy();
     if (a.n_r <= 0) return;
-    count_launches(5);
+    count_launches(6);
     const int sms = sm_total();
+    k_seg_sample<<<kSampleCtas, kSampleThreads, 0, s>>>(a);
     const bool vec = ((reinterpret_cast<uintptr_t>(a.starts) | reinterpret_cast<uintptr_t>(a.ends)) & 15) == 0;
     const long long want = (a.n_r + 1023) / 1024;
     const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
@@ -474,10 +943,87 @@ void launch_binning(const SortedArgs& a, cudaStream_t s) {
     else k_bin_scatter<false><<<g, 256, 0, s>>>(a);
 }
 
-void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t s) {
-    if (a.n_r <= 0) return;
+// Tuning knobs of the sorted path (rs_set_option; initial values from the
+// environment).  trav: 0 auto (tile when dense enough), 1 per-thread binary,
+// 2 per-thread 4-wide, 3 tile always.
+struct SortedOpts {
+    int trav = 0;
+    unsigned tile_density = 16;  // auto: tiles when segments >= this x triangles
+    unsigned tile_balance = 8;   // at least this many tiles per CTA
+    unsigned tile_area = 48;     // about this many triangles' worth of records per tile
+    unsigned bin_occ = 16;       // target live segments per spatial bin
+};
+static SortedOpts& opts() {
+    static SortedOpts o = [] {
+        SortedOpts d;
+        auto num = [](const char* name, long long def) {
+            const char* e = getenv(name);
+            return e && *e ? atoll(e) : def;
+        };
+        const char* t = getenv("RS_TRAV");
+        if (t && t[0] == 'b') d.trav = 1;
+        else if ((t && t[0] == 'w') || sorted_wide()) d.trav = 2;
+        else if (t && t[0] == 't') d.trav = 3;
+        d.tile_density = (unsigned)num("RS_TILE_DENSITY", d.tile_density);
+        d.tile_balance = (unsigned)num("RS_TILE_BALANCE", d.tile_balance);
+        d.tile_area = (unsigned)num("RS_TILE_AREA", d.tile_area);
+        d.bin_occ = (unsigned)num("RS_BIN_OCC", d.bin_occ);
+        return d;
+    }();
+    return o;
+}
+
+int sorted_option(const char* name, long long value, long long* old) {
+    SortedOpts& o = opts();
+    long long prev;
+    if (!strcmp(name, "trav")) { prev = o.trav; if (value >= 0) o.trav = (int)value; }
+    else if (!strcmp(name, "tile_density")) { prev = o.tile_density; if (value >= 0) o.tile_density = (unsigned)value; }
+    else if (!strcmp(name, "tile_balance")) { prev = o.tile_balance; if (value > 0) o.tile_balance = (unsigned)value; }
+    else if (!strcmp(name, "tile_area")) { prev = o.tile_area; if (value > 0) o.tile_area = (unsigned)value; }
+    else if (!strcmp(name, "bin_occupancy")) { prev = o.bin_occ; if (value > 0) o.bin_occ = (unsigned)value; }
+    else return -1;
+    if (old) *old = prev;
+    return 0;
+}
+
+static int trav_variant() { return opts().trav; }
+static unsigned tile_min_density() { return opts().tile_density; }
+static unsigned tile_balance() { return opts().tile_balance; }
+static unsigned bin_occupancy() { return opts().bin_occ; }
+static unsigned tile_area() { return opts().tile_area; }
+
+template <int MODE>
+static void launch_tile(const SortedArgs& a, int sms, cudaStream_t s) {
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trav_tile<MODE>, kTileThreads, 0);
+        if (occ < 1) occ = 1;
+    }
+    k_trav_tile<MODE><<<sms * occ, kTileThreads, 0, s>>>(a);
+}
+
+void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t s) {
+    if (a0.n_r <= 0) return;
+    SortedArgs a = a0;
+    a.tile_area = tile_area();
+    a.tile_min_density = tile_min_density();
+    a.tile_balance = tile_balance();
     count_launches(1);
     const int sms = sm_total();
+    int variant = trav_variant();
+    // tiles pay off only with many segments per triangle (a tile's walk is
+    // amortised over its records); a single triangle has no tree to walk
+    if (variant == 0)
+        variant = a.n_r < (long long)a.tile_min_density * (a.n_int + 1) ? 1 : 3;
+    if (a.n_int == 0) variant = 1;
+    hot_kernel_mark(0, s);
+    if (variant == 3 && !stats) {
+        if (mode == kBoolean) launch_tile<kBoolean>(a, sms, s);
+        else if (mode == kCount) launch_tile<kCount>(a, sms, s);
+        else launch_tile<kBarycentric>(a, sms, s);
+        hot_kernel_mark(1, s);
+        return;
+    }
     static int occ[3] = {0, 0, 0};
     int& o = occ[mode];
     if (!o) {
@@ -489,11 +1035,7 @@ void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t 
     }
     const long long wt = (a.n_r + kSortedThreads - 1) / kSortedThreads;
     const unsigned gt = (unsigned)(wt < (long long)sms * o ? wt : (long long)sms * o);
-    // binary nodes measured faster on coherent segments (C2: 0.64 vs 0.67 ms);
-    // RS_SORTED_WIDE=1 selects the 4-wide per-thread traversal instead
-    const bool bin_nodes = !sorted_wide();
-    hot_kernel_mark(0, s);
-    if (bin_nodes && !stats) {
+    if (variant == 1 && !stats) {
         if (mode == kBoolean) k_trav_sorted_bin<kBoolean><<<gt, kSortedThreads, 0, s>>>(a);
         else if (mode == kCount) k_trav_sorted_bin<kCount><<<gt, kSortedThreads, 0, s>>>(a);
         else k_trav_sorted_bin<kBarycentric><<<gt, kSortedThreads, 0, s>>>(a);

@@ -5,6 +5,8 @@ Bar: integer/index fields bit-exact; distance/point
 bit-exact as well (f64 Moller-Trumbore in the reference op order, no FMA).
 """
 
+import contextlib
+
 import numpy as np
 import pytest
 
@@ -13,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 import paper_2209_02878_b200 as rs  # noqa: E402
 from paper_2209_02878_b200._backend import b200  # noqa: E402
+from paper_2209_02878_b200 import _lib  # noqa: E402
 from golden_io import (MODES, OVERFLOWS, SCENES, SOUPS, TREE_FIELDS, TREE_SIZES,  # noqa: E402
                        assert_result_fields, expected, load)
 from oracle import oracle as O  # noqa: E402
@@ -140,6 +143,64 @@ def test_layered(cap, mode):
     mesh, batch = mesh_batch(fx)
     got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, max_collisions=cap))
     assert_result_fields(result_dict(got), expected(fx, f"cap{cap}", mode), f"layered cap{cap}")
+
+
+# Fast-tree traversal variants (rs_set_option "trav"): the tile walk with its
+# shared candidate lists, the per-thread binary and 4-wide walks.  Results
+# must not depend on the variant, the tile size, the spatial-bin resolution
+# or the tile fallback (candidate-list overflow -> per-record walk).
+TRAV = {"tile": 3, "binary": 1, "wide": 2}
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+@pytest.mark.parametrize("variant", list(TRAV))
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", SCENES + tuple(f"soup:{s}" for s in SOUPS) + ("layered",))
+def test_traversal_variants_bitwise(name, mode, variant, device):
+    fx = load(name if name == "layered" else
+              (f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}"))
+    mesh, batch = mesh_batch(fx, device)
+    want = expected(fx, "cap32" if name == "layered" else "batch", mode)
+    with _lib.option("trav", TRAV[variant]):
+        got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
+    assert_result_fields(result_dict(got), want, f"{name} {mode} {variant}")
+
+
+@pytest.mark.parametrize("knobs", [
+    {"tile_balance": 1, "tile_area": 1},            # one-CTA-size tiles
+    {"tile_balance": 1, "tile_area": 1 << 20},      # huge tiles: candidate-list overflow
+    {"tile_balance": 64, "tile_area": 4},
+    {"bin_occupancy": 1},                           # finest bins
+    {"bin_occupancy": 1 << 20},                     # 256 bins
+], ids=["small", "huge", "many", "finebins", "coarsebins"])
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
+def test_tile_knobs_bitwise(name, mode, knobs):
+    fx = load(name if name == "layered" else
+              (f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}"))
+    mesh, batch = mesh_batch(fx, True)
+    want = expected(fx, "cap32" if name == "layered" else "batch", mode)
+    with contextlib.ExitStack() as stack:
+        stack.enter_context(_lib.option("trav", TRAV["tile"]))
+        for k, v in knobs.items():
+            stack.enter_context(_lib.option(k, v))
+        got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
+    assert_result_fields(result_dict(got), want, f"{name} {mode} {knobs}")
+
+
+@pytest.mark.parametrize("seed,n_tri,n_seg", [(11, 64, 20000), (12, 700, 30000), (13, 3000, 60000)])
+@pytest.mark.parametrize("mode", MODES)
+def test_tile_random_soup_vs_oracle(seed, n_tri, n_seg, mode):
+    """Dense random soups (short segments, many per triangle) through the
+    tile walk, against the C oracle."""
+    V, T, s, _ = _random_soup(seed, n_tri, n_seg)
+    e = s + np.random.default_rng(seed + 100).uniform(-1.5, 1.5, size=s.shape).astype(np.float32)
+    want = O.run_batch(V, T, s, e, mode=mode, max_stack=10**6)
+    for variant in ("tile", "binary"):
+        with _lib.option("trav", TRAV[variant]):
+            got = rs.run_batch(rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e),
+                               rs.EngineConfig(mode=mode, tree="fast"))
+        assert_result_fields(result_dict(got), want, f"dense soup {seed} {mode} {variant}")
 
 
 @pytest.mark.parametrize("mode", MODES)

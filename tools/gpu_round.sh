@@ -24,13 +24,26 @@ for w in $WHAT; do
                    RS_SIMPLE_QUERY=1 RS_BINARY_FAST=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_simple.json" 2>> "$OUT/bench.err";;
     bench_buffer) RS_FAST_PATH=buffer timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_buffer.json" 2>> "$OUT/bench.err";;
     bench_sbin) RS_SORTED_BINARY=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_sbin.json" 2>> "$OUT/bench.err";;
-    bench_mb) for mb in 8 10; do RS_LIB=paper_2209_02878_b200/lib/libraysurf_b200_mb$mb.so timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_mb$mb.json" 2>> "$OUT/bench.err"; done;;
+    bench_mb) for mb in ${RS_MBS:-6}; do for c in ${RS_CFGS:-c2 c3 c4}; do RS_LIB=paper_2209_02878_b200/lib/libraysurf_b200_mb$mb.so timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_mb$mb.json" 2>> "$OUT/bench.err"; done; done;;
+    bench_mb_old) for mb in 8 10; do RS_LIB=paper_2209_02878_b200/lib/libraysurf_b200_mb$mb.so timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_mb$mb.json" 2>> "$OUT/bench.err"; done;;
     bench_nograph) RS_NO_GRAPH=1 timeout 600 python bench.py --no-cpu-baseline --no-e2e > "$OUT/bench_nograph.json" 2>> "$OUT/bench.err";;
     benchq) timeout 600 python bench.py --no-cpu-baseline > "$OUT/bench.json" 2>> "$OUT/bench.err";;
     stats) timeout 300 python tools/stats.py c2 > "$OUT/stats_c2.json" 2>&1;;
     ncuq) timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_query|k_trav|k_exact|k_bin' -s 6 -c 5 \
         -o "$OUT/query" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_full.log" 2>&1;;
     bench_c3) timeout 600 python bench.py --config c3 --no-cpu-baseline --steps 20 > "$OUT/bench_c3.json" 2>> "$OUT/bench.err";;
+    bench_var) for v in ${RS_VARS:-bin tile}; do for c in ${RS_CFGS:-c2 c3 c4 c5}; do RS_TRAV=$v timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_$v.json" 2>> "$OUT/bench.err"; done; done;;
+    bench_area) for ar in ${RS_AREAS:-16 32 48 96}; do for c in ${RS_CFGS:-c2 c4 c5}; do RS_TILE_AREA=$ar timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_a$ar.json" 2>> "$OUT/bench.err"; done; done;;
+    bench_env) # RS_ENVS="A=1,B=2 A=3" : one bench per env set (commas -> spaces)
+      for ev in $RS_ENVS; do for c in ${RS_CFGS:-c2}; do tag=$(echo "$ev" | sed 's|paper_2209_02878_b200/lib/||g' | tr ',=/' '_-_'); env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_$tag.json" 2>> "$OUT/bench.err"; done; done;;
+    ncut) timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_trav' -s 3 -c 1 \
+        -o "$OUT/trav_${RS_NCU_CFG:-c2}" python bench.py --config ${RS_NCU_CFG:-c2} --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_trav.log" 2>&1;;
+    e2e_env) for ev in ${RS_ENVS:-RS_NONE=1}; do for c in ${RS_CFGS:-c2}; do tag=$(echo "$ev" | sed 's|paper_2209_02878_b200/lib/||g' | tr ',=/' '_-_'); env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --steps 20 > "$OUT/e2e_${c}_$tag.json" 2>> "$OUT/bench.err"; done; done;;
+    klist) # per-kernel serialized times for each env set in RS_ENVS (or default), config RS_CFGS
+      for ev in ${RS_ENVS:-RS_NONE=1}; do for c in ${RS_CFGS:-c2}; do tag=$(echo "$ev" | sed 's|paper_2209_02878_b200/lib/||g' | tr ',=/' '_-_');
+        env $(echo "$ev" | tr ',' ' ') timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+          --log-file "$OUT/kl_${c}_$tag.csv" python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>> "$OUT/bench.err";
+        python tools/launch_table.py "$OUT/kl_${c}_$tag.csv" 18 > "$OUT/kl_${c}_$tag.txt"; done; done;;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
