@@ -451,7 +451,7 @@ static int fast_bin(const rs_tree* t, const float* d_s, const float* d_e, int64_
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
         CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
     }
-    CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 4 * (sorted_bins() / 1024), s));
+    CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 4 * (2 * (sorted_bins() / 1024) + 64), s));  // counters, look-back words, ticket
     launch_binning(sorted_args(t, d_s, d_e, n_r, o, f), s);
     return RS_OK;
 }

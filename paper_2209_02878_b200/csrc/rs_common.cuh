@@ -107,15 +107,14 @@ __device__ __forceinline__ bool overlap6(const float q[6], float x0, float x1, f
 // ---- f64 Moller-Trumbore in the reference op order (geometry.py:82-137,
 // _core.pyx:67-114).  Explicit _rn intrinsics: no FMA contraction, so the
 // result is bit-identical to the -ffp-contract=off CPU reference. ----------
-__device__ __forceinline__ bool mt_hit(float ax_, float ay_, float az_, float bx, float by,
-                                       float bz, float cx, float cy, float cz, double sx,
-                                       double sy, double sz, double dx, double dy, double dz,
-                                       double* t_out) {
-    const double ax = ax_, ay = ay_, az = az_;
-    const double e1x = __dsub_rn((double)bx, ax), e1y = __dsub_rn((double)by, ay),
-                 e1z = __dsub_rn((double)bz, az);
-    const double e2x = __dsub_rn((double)cx, ax), e2y = __dsub_rn((double)cy, ay),
-                 e2z = __dsub_rn((double)cz, az);
+// mt_hit_pre takes the triangle's first vertex and both edges already in f64
+// (e1 = b - a, e2 = c - a, each one rounded f64 subtraction of f32 inputs,
+// exactly as the reference forms them), so a caller testing one triangle
+// against many segments forms them once.
+__device__ __forceinline__ bool mt_hit_pre(double ax, double ay, double az, double e1x,
+                                           double e1y, double e1z, double e2x, double e2y,
+                                           double e2z, double sx, double sy, double sz, double dx,
+                                           double dy, double dz, double* t_out) {
     const double px = __dsub_rn(__dmul_rn(dy, e2z), __dmul_rn(dz, e2y));
     const double py = __dsub_rn(__dmul_rn(dz, e2x), __dmul_rn(dx, e2z));
     const double pz = __dsub_rn(__dmul_rn(dx, e2y), __dmul_rn(dy, e2x));
@@ -139,6 +138,18 @@ __device__ __forceinline__ bool mt_hit(float ax_, float ay_, float az_, float bx
     if (t < 0.0 || t > 1.0) return false;
     *t_out = t;
     return true;
+}
+
+__device__ __forceinline__ bool mt_hit(float ax_, float ay_, float az_, float bx, float by,
+                                       float bz, float cx, float cy, float cz, double sx,
+                                       double sy, double sz, double dx, double dy, double dz,
+                                       double* t_out) {
+    const double ax = ax_, ay = ay_, az = az_;
+    const double e1x = __dsub_rn((double)bx, ax), e1y = __dsub_rn((double)by, ay),
+                 e1z = __dsub_rn((double)bz, az);
+    const double e2x = __dsub_rn((double)cx, ax), e2y = __dsub_rn((double)cy, ay),
+                 e2z = __dsub_rn((double)cz, az);
+    return mt_hit_pre(ax, ay, az, e1x, e1y, e1z, e2x, e2y, e2z, sx, sy, sz, dx, dy, dz, t_out);
 }
 
 // _core.pyx:330-348: point = s + t*d (f64), distance = f32(sqrt(|p - s|^2)).

@@ -59,6 +59,14 @@ __device__ __forceinline__ bool slot_hit(const float f[8], const float b[6]) {
            (b[3] >= f[2]) & (b[4] <= f[5]) & (b[5] >= f[4]);
 }
 
+// One 32-B record (start, id, end) as a single 256-bit store: one full
+// sector per record instead of two half-sector writes.
+__device__ __forceinline__ void st_rec(float4* dst, const float s[3], int id, const float e[3]) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "f"(s[0]), "f"(s[1]),
+                 "f"(s[2]), "f"(__int_as_float(id)), "f"(e[0]), "f"(e[1]), "f"(e[2]), "f"(0.f)
+                 : "memory");
+}
+
 __device__ __forceinline__ unsigned spread3(unsigned v) {  // bit i -> bit 3i (i < 10)
     v &= 0x3ffu;
     v = (v | (v << 16)) & 0x030000ffu;
@@ -88,6 +96,7 @@ struct RootInfo {
     int qmax[3];
     int pa, pb, pc;  // axes by bit count, descending
     int bb, bc;      // bits of B and C
+    int nbits;       // key bits: keys < 2^nbits
 };
 
 // The root box (union of all triangle boxes) comes from the build's k_prep,
@@ -119,6 +128,7 @@ __device__ __forceinline__ void root_info_compute(const RsHeader* hdr, const Sor
     int nbits = 0;
     while (nbits < kBinBits && (double)(1u << (nbits + 1)) * a.bin_occupancy <= live) ++nbits;
     nbits = nbits < 8 ? 8 : nbits;
+    ri.nbits = nbits;
     float c0 = e0, c1 = e1, c2 = e2;
     int b0 = 0, b1 = 0, b2 = 0;
     for (int i = 0; i < nbits; ++i) {
@@ -269,21 +279,31 @@ __global__ void __launch_bounds__(kSampleThreads) k_seg_sample(SortedArgs a) {
     }
 }
 
+// Histogram pass.  Inputs arrive in caller order, so a warp's bins rarely
+// coincide: plain fire-and-forget reductions, with warp aggregation only
+// when neighbouring lanes share a bin (pre-sorted inputs).
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
     RootInfo ri;
     root_info(a, ri);
     const long long nq = (a.n_r + 3) / 4;
+    const int lane = threadIdx.x & 31;
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
         float s[4][3], e[4][3];
         const int cnt = load4<VEC>(a.starts, a.ends, q, a.n_r, s, e);
+        int bin[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bin[j] = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
+        const unsigned act = __activemask();
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int bin = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
-            const unsigned act = __activemask();
-            const unsigned peers = __match_any_sync(act, bin);
-            if (bin >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
-                atomicAdd(a.bins + bin, __popc(peers));
+            const int up = __shfl_up_sync(act, bin[j], 1);
+            if (__any_sync(act, lane > 0 && bin[j] >= 0 && up == bin[j])) {
+                const unsigned peers = __match_any_sync(act, bin[j]);
+                if (bin[j] >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(a.bins + bin[j], __popc(peers));
+            } else if (bin[j] >= 0) {
+                atomicAdd(a.bins + bin[j], 1u);
+            }
         }
     }
 }
@@ -352,6 +372,50 @@ __global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
     *reinterpret_cast<uint4*>(a.cursor + base) = o;
 }
 
+// Scatter pass: the same bins; each live segment's 32-B record goes to its
+// bin's next slot.  The four cursor claims of a thread are issued together
+// (their round trips overlap) before any record is written.
+// Single-pass exclusive scan of the active bins (keys < 2^nbits): one CTA
+// per 1024-bin tile in ticket order, decoupled look-back across tiles; the
+// last active tile publishes the live count.  Tiles beyond the active range
+// exit at once.
+constexpr int kScanTicket = 2 * kScanTiles;  // word offset of the ticket in tile_sum
+__global__ void __launch_bounds__(256) k_bin_scan1(SortedArgs a) {
+    __shared__ unsigned wtot[8];
+    __shared__ int s_tile, s_active;
+    __shared__ unsigned s_excl;
+    if (threadIdx.x == 0) {
+        RootInfo ri;
+        root_info_compute(a.hdr, a, ri);
+        const int active = (1 << ri.nbits) > kScanTile ? (1 << ri.nbits) / kScanTile : 1;
+        s_active = active;
+        s_tile = (int)atomicAdd(a.tile_sum + kScanTicket, 1u);
+    }
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= s_active) return;
+    const int base = tile * kScanTile + threadIdx.x * 4;
+    const uint4 v = *reinterpret_cast<const uint4*>(a.bins + base);
+    unsigned total;
+    const unsigned local = block_excl_scan_256(v.x + v.y + v.z + v.w, wtot, &total);
+    if (threadIdx.x < 32) {
+        const unsigned long long excl =
+            lookback_warp(reinterpret_cast<unsigned long long*>(a.tile_sum), tile, total);
+        if (threadIdx.x == 0) {
+            s_excl = (unsigned)excl;
+            if (tile == s_active - 1) *a.n_live = (unsigned)(excl + total);
+        }
+    }
+    __syncthreads();
+    unsigned run = s_excl + local;
+    uint4 o;
+    o.x = run; run += v.x;
+    o.y = run; run += v.y;
+    o.z = run; run += v.z;
+    o.w = run;
+    *reinterpret_cast<uint4*>(a.cursor + base) = o;
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
     RootInfo ri;
@@ -361,22 +425,206 @@ __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
     for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
         float s[4][3], e[4][3];
         const int cnt = load4<VEC>(a.starts, a.ends, q, a.n_r, s, e);
+        int bin[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bin[j] = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
+        const unsigned act = __activemask();
+        bool dup = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int bin = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
-            const unsigned act = __activemask();
-            const unsigned peers = __match_any_sync(act, bin);
-            const int leader = __ffs(peers) - 1;
-            unsigned pos = 0;
-            if (bin >= 0 && leader == lane) pos = atomicAdd(a.cursor + bin, __popc(peers));
-            pos = __shfl_sync(peers, pos, leader);
-            if (bin < 0) continue;
-            pos += __popc(peers & ((1u << lane) - 1u));
-            const long long id = 4 * q + j;
-            a.rec[2 * pos] = make_float4(s[j][0], s[j][1], s[j][2], __int_as_float((int)id));
-            a.rec[2 * pos + 1] = make_float4(e[j][0], e[j][1], e[j][2], 0.f);
+            const int up = __shfl_up_sync(act, bin[j], 1);
+            dup |= lane > 0 && bin[j] >= 0 && up == bin[j];
+        }
+        unsigned pos[4];
+        if (__any_sync(act, dup)) {
+            // neighbouring lanes share bins: one claim per distinct bin
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const unsigned peers = __match_any_sync(act, bin[j]);
+                const int leader = __ffs(peers) - 1;
+                unsigned p = 0;
+                if (bin[j] >= 0 && leader == lane) p = atomicAdd(a.cursor + bin[j], __popc(peers));
+                pos[j] = __shfl_sync(peers, p, leader) + __popc(peers & ((1u << lane) - 1u));
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pos[j] = bin[j] >= 0 ? atomicAdd(a.cursor + bin[j], 1u) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (bin[j] < 0) continue;
+            st_rec(a.rec + 2 * pos[j], s[j], (int)(4 * q + j), e[j]);
         }
     }
+}
+
+// ---- binning passes over TMA bulk copies ------------------------------------
+//
+// The two binning passes stream 24 B per segment and do ~100 instructions of
+// key arithmetic per segment.  With plain loads a thread's loads sit idle
+// while it computes, so the passes reached about half of HBM bandwidth.  Here
+// each CTA keeps two 1024-segment stages in shared memory, filled by the TMA
+// engine (cp.async.bulk global->shared, completion on an mbarrier) one chunk
+// ahead of the compute, so the DRAM stream never waits for the key math.
+constexpr int kStreamSegs = 1024;
+constexpr int kStreamThreads = 256;
+constexpr unsigned kStreamStageBytes = 2u * kStreamSegs * 12u;  // starts + ends
+constexpr size_t kStreamSmem = 2 * kStreamStageBytes + 64;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "RS_MBAR_WAIT%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra RS_MBAR_WAIT%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Calls body(s, e, cnt, q) for every group of four consecutive segments
+// (q = group index), with the full 1024-segment chunks streamed through
+// shared memory and the ragged tail read directly.
+template <class Body>
+__device__ __forceinline__ void stream_segments(const SortedArgs& a, Body&& body) {
+    extern __shared__ __align__(128) unsigned char stream_smem[];
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(stream_smem + 2 * kStreamStageBytes);
+    const long long nfull = a.n_r / kStreamSegs;
+    const long long first = blockIdx.x;
+    const long long step = gridDim.x;
+    auto stage = [&](int st) { return reinterpret_cast<float*>(stream_smem + st * kStreamStageBytes); };
+    auto issue = [&](long long c, int st) {
+        const size_t off = (size_t)c * kStreamSegs * 3;
+        mbar_expect_tx(&bar[st], kStreamStageBytes);
+        bulk_g2s(stage(st), a.starts + off, kStreamSegs * 12u, &bar[st]);
+        bulk_g2s(stage(st) + kStreamSegs * 3, a.ends + off, kStreamSegs * 12u, &bar[st]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (first < nfull) issue(first, 0);
+        if (first + step < nfull) issue(first + step, 1);
+    }
+    int it = 0;
+    for (long long c = first; c < nfull; c += step, ++it) {
+        const int st = it & 1;
+        mbar_wait(&bar[st], (unsigned)((it >> 1) & 1));
+        const float* S = stage(st);
+        const float* E = stage(st) + kStreamSegs * 3;
+        const int t = threadIdx.x;
+        float s[4][3], e[4][3];
+        const float4* s4 = reinterpret_cast<const float4*>(S + 12 * t);
+        const float4* e4 = reinterpret_cast<const float4*>(E + 12 * t);
+        float fs[12], fe[12];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float4 x = s4[k], y = e4[k];
+            fs[4 * k] = x.x; fs[4 * k + 1] = x.y; fs[4 * k + 2] = x.z; fs[4 * k + 3] = x.w;
+            fe[4 * k] = y.x; fe[4 * k + 1] = y.y; fe[4 * k + 2] = y.z; fe[4 * k + 3] = y.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                s[j][k] = fs[3 * j + k];
+                e[j][k] = fe[3 * j + k];
+            }
+        __syncthreads();  // every thread has its data in registers: the stage may refill
+        if (threadIdx.x == 0 && c + 2 * step < nfull) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(c + 2 * step, st);
+        }
+        body(s, e, 4, c * (kStreamSegs / 4) + t);
+    }
+    // ragged tail (< one chunk): the last CTA reads it directly
+    if (blockIdx.x == gridDim.x - 1) {
+        const long long nq = (a.n_r + 3) / 4;
+        for (long long q = nfull * (kStreamSegs / 4) + threadIdx.x; q < nq; q += kStreamThreads) {
+            float s[4][3], e[4][3];
+            const int cnt = load4<false>(a.starts, a.ends, q, a.n_r, s, e);
+            body(s, e, cnt, q);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kStreamThreads) k_bin_count_tma(SortedArgs a) {
+    RootInfo ri;
+    root_info(a, ri);
+    const int lane = threadIdx.x & 31;
+    stream_segments(a, [&](float (&s)[4][3], float (&e)[4][3], int cnt, long long) {
+        int bin[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bin[j] = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
+        const unsigned act = __activemask();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int up = __shfl_up_sync(act, bin[j], 1);
+            if (__any_sync(act, lane > 0 && bin[j] >= 0 && up == bin[j])) {
+                const unsigned peers = __match_any_sync(act, bin[j]);
+                if (bin[j] >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(a.bins + bin[j], __popc(peers));
+            } else if (bin[j] >= 0) {
+                atomicAdd(a.bins + bin[j], 1u);
+            }
+        }
+    });
+}
+
+__global__ void __launch_bounds__(kStreamThreads) k_bin_scatter_tma(SortedArgs a) {
+    RootInfo ri;
+    root_info(a, ri);
+    const int lane = threadIdx.x & 31;
+    stream_segments(a, [&](float (&s)[4][3], float (&e)[4][3], int cnt, long long q) {
+        int bin[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bin[j] = j < cnt ? seg_bin(s[j], e[j], ri) : -1;
+        const unsigned act = __activemask();
+        bool dup = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int up = __shfl_up_sync(act, bin[j], 1);
+            dup |= lane > 0 && bin[j] >= 0 && up == bin[j];
+        }
+        unsigned pos[4];
+        if (__any_sync(act, dup)) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const unsigned peers = __match_any_sync(act, bin[j]);
+                const int leader = __ffs(peers) - 1;
+                unsigned p = 0;
+                if (bin[j] >= 0 && leader == lane) p = atomicAdd(a.cursor + bin[j], __popc(peers));
+                pos[j] = __shfl_sync(peers, p, leader) + __popc(peers & ((1u << lane) - 1u));
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pos[j] = bin[j] >= 0 ? atomicAdd(a.cursor + bin[j], 1u) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (bin[j] < 0) continue;
+            st_rec(a.rec + 2 * pos[j], s[j], (int)(4 * q + j), e[j]);
+        }
+    });
 }
 
 template <int MODE, bool STATS>
@@ -604,7 +852,17 @@ constexpr int kTileLCap = 512;  // leaf candidates per tile
 constexpr int kTileFCap = 256;  // walk frontier per level
 constexpr int kCutDepth = 6;    // the walk starts from the tree's depth-6 cut
 constexpr int kCutCap = 1 << kCutDepth;
-constexpr int kLaneCand = 8;    // per-lane candidate slots between exact-test passes
+constexpr int kWCap = 16;       // warp candidates prepared per round
+
+// One warp's prepared candidates: the triangle's first vertex and edges in
+// f64 (formed once per warp instead of once per exact test), its exact box
+// and original id.
+struct WarpCand {
+    double a[3][kWCap], e1[3][kWCap], e2[3][kWCap];
+    float4 xy[kWCap];
+    float2 z[kWCap];
+    int tid[kWCap];
+};
 
 struct TileSmem {
     float4 lxy[kTileLCap];  // leaf box x0 x1 y0 y1
@@ -614,7 +872,8 @@ struct TileSmem {
     float4 cxy[kCutCap];    // the cut: entry boxes and refs (built once per CTA)
     float2 cz[kCutCap];
     int cref[kCutCap];
-    unsigned short cand[kTileThreads / 32][kLaneCand][32];
+    WarpCand wc[kTileThreads / 32];
+    unsigned char slot[kTileThreads / 32][kWCap][32];  // per-lane candidate lists
     float part[kTileThreads / 32][6];
     int nf[3];
     int nl;
@@ -857,40 +1116,73 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
                     w[k] = wred_min(valid ? b[k] : INFINITY);
                     w[k + 1] = wred_max(valid ? b[k + 1] : -INFINITY);
                 }
-                // candidates: L filtered by the warp box, then by the lane's
-                // own box; the exact tests run in passes over the per-lane
-                // slots so the warp executes each pass once
+                // candidates: L filtered by the warp box W; each round
+                // prepares up to kWCap of them (one lane each: f64 vertex and
+                // edges into shared memory), then every lane keeps the ones
+                // its own box overlaps and the exact tests run in passes over
+                // the per-lane lists, so the warp executes each pass once
                 bool live = valid;
-                int nc = 0;
-                unsigned short(*slots)[32] = sm.cand[warp];
-                auto pass = [&]() {
-                    const int most = __reduce_max_sync(kFullMask, nc);
-                    for (int i = 0; i < most; ++i) {
-                        if (i < nc && live) {
-#ifdef RS_TILE_STATS
-                            atomicAdd(&a.status->mts, 1ull);
-#endif
-                            leaf_exact<MODE>(a.leaves, sm.lid[slots[i][lane]], r0, r1, det, nh, btri, bt);
-                            if (MODE == kBoolean && det) live = false;
-                        }
-                    }
-                    nc = 0;
-                };
+                WarpCand& wc = sm.wc[warp];
+                unsigned char(*slots)[32] = sm.slot[warp];
                 for (int cb = 0; cb < nl; cb += 32) {
                     const int j = cb + lane;
                     const bool hit = j < nl && box_ov(w, sm.lxy[j], sm.lz[j]);
-                    unsigned m = __ballot_sync(kFullMask, hit);
-                    while (m) {
-                        const int k = cb + __ffs(m) - 1;
-                        m &= m - 1;
-#ifdef RS_TILE_STATS
-                        if (lane == 0) atomicAdd(&a.status->pad, 1ull);
-#endif
-                        if (live && box_ov(b, sm.lxy[k], sm.lz[k])) slots[nc++][lane] = (unsigned short)k;
-                        if (__any_sync(kFullMask, nc == kLaneCand)) pass();
+                    const unsigned m = __ballot_sync(kFullMask, hit);
+                    const int nm = __popc(m);
+                    const int rank = __popc(m & ((1u << lane) - 1u));
+                    for (int base = 0; base < nm; base += kWCap) {
+                        const int nw = nm - base < kWCap ? nm - base : kWCap;
+                        if (hit && rank >= base && rank < base + kWCap) {
+                            const int e = rank - base;
+                            const RsLeaf* L = a.leaves + sm.lid[j];
+                            const float4 p0 = __ldg(&L->p0), p1 = __ldg(&L->p1), p2 = __ldg(&L->p2);
+                            const double ax = p0.x, ay = p0.y, az = p0.z;
+                            wc.a[0][e] = ax;
+                            wc.a[1][e] = ay;
+                            wc.a[2][e] = az;
+                            wc.e1[0][e] = __dsub_rn((double)p0.w, ax);
+                            wc.e1[1][e] = __dsub_rn((double)p1.x, ay);
+                            wc.e1[2][e] = __dsub_rn((double)p1.y, az);
+                            wc.e2[0][e] = __dsub_rn((double)p1.z, ax);
+                            wc.e2[1][e] = __dsub_rn((double)p1.w, ay);
+                            wc.e2[2][e] = __dsub_rn((double)p2.x, az);
+                            wc.xy[e] = sm.lxy[j];
+                            wc.z[e] = sm.lz[j];
+                            wc.tid[e] = __float_as_int(p2.y);
+                        }
+                        __syncwarp();
+                        int nc = 0;
+                        if (live)
+                            for (int i = 0; i < nw; ++i)
+                                if (box_ov(b, wc.xy[i], wc.z[i])) slots[nc++][lane] = (unsigned char)i;
+                        const int most = __reduce_max_sync(kFullMask, nc);
+                        for (int i = 0; i < most; ++i) {
+                            if (i < nc && live) {
+                                const int e = slots[i][lane];
+                                const double sx = r0.x, sy = r0.y, sz = r0.z;
+                                const double dx = __dsub_rn((double)r1.x, sx),
+                                             dy = __dsub_rn((double)r1.y, sy),
+                                             dz = __dsub_rn((double)r1.z, sz);
+                                double t;
+                                if (mt_hit_pre(wc.a[0][e], wc.a[1][e], wc.a[2][e], wc.e1[0][e],
+                                               wc.e1[1][e], wc.e1[2][e], wc.e2[0][e], wc.e2[1][e],
+                                               wc.e2[2][e], sx, sy, sz, dx, dy, dz, &t)) {
+                                    const int tid = wc.tid[e];
+                                    det = 1;
+                                    ++nh;
+                                    if (MODE == kBarycentric &&
+                                        (btri < 0 || t < bt || (t == bt && tid < btri))) {
+                                        bt = t;
+                                        btri = tid;
+                                    }
+                                    if (MODE == kBoolean) live = false;
+                                }
+                            }
+                        }
+                        __syncwarp();
                     }
+                    if (MODE == kBoolean && !__any_sync(kFullMask, live)) break;
                 }
-                pass();
             }
             if (valid) write_result<MODE>(a, __float_as_int(r0.w), det, nh, btri, bt);
         }
@@ -922,27 +1214,6 @@ bool sorted_wide() {
     return wide;
 }
 
-static unsigned bin_occupancy();
-
-void launch_binning(const SortedArgs& a0, cudaStream_t s) {
-    SortedArgs a = a0;
-    a.bin_occupancy = bin_occupancy();
-    if (a.n_r <= 0) return;
-    count_launches(6);
-    const int sms = sm_total();
-    k_seg_sample<<<kSampleCtas, kSampleThreads, 0, s>>>(a);
-    const bool vec = ((reinterpret_cast<uintptr_t>(a.starts) | reinterpret_cast<uintptr_t>(a.ends)) & 15) == 0;
-    const long long want = (a.n_r + 1023) / 1024;
-    const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
-    if (vec) k_bin_count<true><<<g, 256, 0, s>>>(a);
-    else k_bin_count<false><<<g, 256, 0, s>>>(a);
-    k_tile_reduce<<<kScanTiles, 256, 0, s>>>(a);
-    k_tile_scan<<<1, 256, 0, s>>>(a);
-    k_bin_scan<<<kScanTiles, 256, 0, s>>>(a);
-    if (vec) k_bin_scatter<true><<<g, 256, 0, s>>>(a);
-    else k_bin_scatter<false><<<g, 256, 0, s>>>(a);
-}
-
 // Tuning knobs of the sorted path (rs_set_option; initial values from the
 // environment).  trav: 0 auto (tile when dense enough), 1 per-thread binary,
 // 2 per-thread 4-wide, 3 tile always.
@@ -952,6 +1223,7 @@ struct SortedOpts {
     unsigned tile_balance = 8;   // at least this many tiles per CTA
     unsigned tile_area = 48;     // about this many triangles' worth of records per tile
     unsigned bin_occ = 16;       // target live segments per spatial bin
+    int bin_tma = 1;             // binning passes stream through TMA bulk copies
 };
 static SortedOpts& opts() {
     static SortedOpts o = [] {
@@ -968,6 +1240,7 @@ static SortedOpts& opts() {
         d.tile_balance = (unsigned)num("RS_TILE_BALANCE", d.tile_balance);
         d.tile_area = (unsigned)num("RS_TILE_AREA", d.tile_area);
         d.bin_occ = (unsigned)num("RS_BIN_OCC", d.bin_occ);
+        d.bin_tma = (int)num("RS_BIN_TMA", d.bin_tma);
         return d;
     }();
     return o;
@@ -981,6 +1254,7 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "tile_balance")) { prev = o.tile_balance; if (value > 0) o.tile_balance = (unsigned)value; }
     else if (!strcmp(name, "tile_area")) { prev = o.tile_area; if (value > 0) o.tile_area = (unsigned)value; }
     else if (!strcmp(name, "bin_occupancy")) { prev = o.bin_occ; if (value > 0) o.bin_occ = (unsigned)value; }
+    else if (!strcmp(name, "bin_tma")) { prev = o.bin_tma; if (value >= 0) o.bin_tma = (int)value; }
     else return -1;
     if (old) *old = prev;
     return 0;
@@ -991,6 +1265,43 @@ static unsigned tile_min_density() { return opts().tile_density; }
 static unsigned tile_balance() { return opts().tile_balance; }
 static unsigned bin_occupancy() { return opts().bin_occ; }
 static unsigned tile_area() { return opts().tile_area; }
+
+void launch_binning(const SortedArgs& a0, cudaStream_t s) {
+    SortedArgs a = a0;
+    a.bin_occupancy = bin_occupancy();
+    if (a.n_r <= 0) return;
+    count_launches(4);
+    const int sms = sm_total();
+    k_seg_sample<<<kSampleCtas, kSampleThreads, 0, s>>>(a);
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.starts) | reinterpret_cast<uintptr_t>(a.ends)) & 15) == 0;
+    if (vec && opts().bin_tma && a.n_r >= kStreamSegs) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_bin_count_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem);
+            cudaFuncSetAttribute(k_bin_scatter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem);
+            attr = true;
+        }
+        const long long chunks = a.n_r / kStreamSegs;
+        const unsigned g = (unsigned)(chunks < sms * 4ll ? chunks : sms * 4ll);
+        k_bin_count_tma<<<g, kStreamThreads, kStreamSmem, s>>>(a);
+        k_bin_scan1<<<kScanTiles, 256, 0, s>>>(a);
+        if (opts().bin_tma & 2) {
+            k_bin_scatter_tma<<<g, kStreamThreads, kStreamSmem, s>>>(a);
+        } else {
+            const long long want = (a.n_r + 1023) / 1024;
+            const unsigned g2 = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
+            k_bin_scatter<true><<<g2, 256, 0, s>>>(a);
+        }
+        return;
+    }
+    const long long want = (a.n_r + 1023) / 1024;
+    const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
+    if (vec) k_bin_count<true><<<g, 256, 0, s>>>(a);
+    else k_bin_count<false><<<g, 256, 0, s>>>(a);
+    k_bin_scan1<<<kScanTiles, 256, 0, s>>>(a);
+    if (vec) k_bin_scatter<true><<<g, 256, 0, s>>>(a);
+    else k_bin_scatter<false><<<g, 256, 0, s>>>(a);
+}
 
 template <int MODE>
 static void launch_tile(const SortedArgs& a, int sms, cudaStream_t s) {

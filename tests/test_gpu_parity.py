@@ -172,7 +172,8 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"tile_balance": 64, "tile_area": 4},
     {"bin_occupancy": 1},                           # finest bins
     {"bin_occupancy": 1 << 20},                     # 256 bins
-], ids=["small", "huge", "many", "finebins", "coarsebins"])
+    {"bin_tma": 0},                                 # binning with plain loads
+], ids=["small", "huge", "many", "finebins", "coarsebins", "notma"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
 def test_tile_knobs_bitwise(name, mode, knobs):

@@ -35,7 +35,10 @@ for w in $WHAT; do
     bench_var) for v in ${RS_VARS:-bin tile}; do for c in ${RS_CFGS:-c2 c3 c4 c5}; do RS_TRAV=$v timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_$v.json" 2>> "$OUT/bench.err"; done; done;;
     bench_area) for ar in ${RS_AREAS:-16 32 48 96}; do for c in ${RS_CFGS:-c2 c4 c5}; do RS_TILE_AREA=$ar timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_a$ar.json" 2>> "$OUT/bench.err"; done; done;;
     bench_env) # RS_ENVS="A=1,B=2 A=3" : one bench per env set (commas -> spaces)
-      for ev in $RS_ENVS; do for c in ${RS_CFGS:-c2}; do tag=$(echo "$ev" | sed 's|paper_2209_02878_b200/lib/||g' | tr ',=/' '_-_'); env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_$tag.json" 2>> "$OUT/bench.err"; done; done;;
+      for ev in ${RS_ENVS:-RS_NONE=1}; do for c in ${RS_CFGS:-c2}; do tag=$(echo "$ev" | sed 's|paper_2209_02878_b200/lib/||g' | tr ',=/' '_-_'); env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 20 > "$OUT/bench_${c}_$tag.json" 2>> "$OUT/bench.err"; done; done;;
+    ncuk) # full capture of kernels matching RS_NCU_K (regex) in one step of config RS_NCU_CFG
+      timeout 600 ncu --set full --clock-control none --import-source on -k regex:"${RS_NCU_K:-k_bin}" -s ${RS_NCU_SKIP:-10} -c ${RS_NCU_C:-3} \
+        -o "$OUT/k_${RS_NCU_CFG:-c2}" python bench.py --config ${RS_NCU_CFG:-c2} --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_k.log" 2>&1;;
     ncut) timeout 600 ncu --set full --clock-control none --import-source on -k regex:'k_trav' -s 3 -c 1 \
         -o "$OUT/trav_${RS_NCU_CFG:-c2}" python bench.py --config ${RS_NCU_CFG:-c2} --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_trav.log" 2>&1;;
     e2e_env) for ev in ${RS_ENVS:-RS_NONE=1}; do for c in ${RS_CFGS:-c2}; do tag=$(echo "$ev" | sed 's|paper_2209_02878_b200/lib/||g' | tr ',=/' '_-_'); env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --steps 20 > "$OUT/e2e_${c}_$tag.json" 2>> "$OUT/bench.err"; done; done;;
