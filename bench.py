@@ -274,6 +274,7 @@ def main():
         t_end = clocks.mark()
         time.sleep(0.05)
     launches = lib.rs_kernel_launches() - launches0
+    hot_kernel = lib.rs_hot_kernel().decode()
     if world > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
@@ -335,7 +336,7 @@ def main():
                      "traversal_kernel": round(h_ms, 4)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "k_trav_sorted_bin", "peak_kind": peak_kind,
+                     "kernel": hot_kernel, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_segment": b_ray},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(t_start, t_end + 0.02),

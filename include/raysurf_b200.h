@@ -162,6 +162,10 @@ RS_API long long rs_kernel_launches(void);
  * returned in *old_value.  Results never depend on these. */
 RS_API int rs_set_option(const char *name, long long value, long long *old_value);
 
+/* Name of the traversal kernel the fast path chose on its last launch (the
+ * dominant kernel bench.py's roofline is quoted on). */
+RS_API const char *rs_hot_kernel(void);
+
 /* Diagnostics: the 8 device status words (bad, internal, hits, tile_counter,
  * visits, mts, cand_count, pad) of the calling thread's last graph-replayed
  * rs_run_batch_device. */

@@ -46,6 +46,7 @@ _SIGS = {
     "rs_kernel_launches": (C.c_longlong, []),
     "rs_last_status": (i32, [p]),
     "rs_set_option": (i32, [C.c_char_p, C.c_longlong, p]),
+    "rs_hot_kernel": (C.c_char_p, []),
 }
 
 _lib = None

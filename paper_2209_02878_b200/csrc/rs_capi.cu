@@ -178,9 +178,10 @@ bool need_nodes4() {
         const char* e = getenv("RS_FAST_PATH");
         return e && e[0] == 'b';
     }();
-    long long trav = 0;
+    long long trav = 0, wide = 0;
     rs::sorted_option("trav", -1, &trav);
-    return buffer || trav == 2;
+    rs::sorted_option("tile_wide", -1, &wide);
+    return buffer || trav == 2 || (wide && trav != 1);
 }
 
 // after_prep (optional) runs on the host right after k_prep is enqueued on
@@ -388,6 +389,7 @@ struct FastScratch {
     int* gstack = nullptr;
     unsigned *bins = nullptr, *cursor = nullptr, *n_live = nullptr;
     float4* rec = nullptr;
+    unsigned long long* seg_key = nullptr;
 };
 
 // RS_FAST_PATH=buffer: pair traversal -> collision buffer -> exact pass
@@ -408,7 +410,8 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         total += align256(8ull * n_r) + align256(4ull * n_r) + align256(8ull * cap) +
                  align256(bary_compact_scratch(n_r));
     if (g_buffer_path) total += align256(4 * trav_gstack_ints());
-    total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r);
+    total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r) +
+             align256(8ull * n_r);
     CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
@@ -427,6 +430,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     f.cursor = c.take<unsigned>(sorted_bins());
     f.n_live = c.take<unsigned>(64 + 4 * 32);
     f.rec = c.take<float4>(2ull * n_r);
+    f.seg_key = c.take<unsigned long long>(n_r);
     f.cap = cap;
     return RS_OK;
 }
@@ -434,7 +438,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
 static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r,
                               const FastOut& o, FastScratch& f) {
     return SortedArgs{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r,
-                      f.bins, f.cursor, f.n_live, reinterpret_cast<float*>(f.n_live + 64), f.bins + sorted_bins(), f.rec, o.flags,
+                      f.bins, f.cursor, f.n_live, reinterpret_cast<float*>(f.n_live + 64), f.bins + sorted_bins(), f.rec, f.seg_key, o.flags,
                       f.best_t, f.best_tri, f.st};
 }
 
@@ -950,6 +954,8 @@ RS_API int rs_set_option(const char* name, long long value, long long* old_value
     g_opt_gen.fetch_add(1);
     return RS_OK;
 }
+
+RS_API const char* rs_hot_kernel(void) { return rs::hot_kernel_name(); }
 
 RS_API int rs_last_status(unsigned long long* out8) {
     std::memcpy(out8, &g_last_status, sizeof(RsStatus));

@@ -148,13 +148,16 @@ struct SortedArgs {
     float* seg_stats;    // k_seg_sample: per-CTA (sum of box sides x/y/z, live count)
     unsigned* tile_sum;  // sorted_bins()/1024 per-tile counts (zeroed) -> tile offsets
     float4* rec;         // n_r x 32-B records (start, id, end)
+    unsigned long long* seg_key;  // n_r: bin << 32 | rank within bin (~0: dead), from the histogram pass
     int* flags;                  // boolean / count output (pre-zeroed)
     unsigned long long* best_t;  // barycentric (pre-set ~0)
     int* best_tri;               // barycentric (pre-set -1)
     RsStatus* status;
     unsigned bin_occupancy;  // binning: target live segments per bin (set at launch)
+    int rec_ids;             // rec holds 4-B segment ids instead of 32-B records (set at launch)
     unsigned tile_area;  // tile traversal: target triangles' worth of records per tile (set at launch)
     unsigned tile_balance;      // tile traversal: at least this many tiles per CTA
+    unsigned warp_chunks;       // warp tiles: 32-record chunks per warp unit
     unsigned tile_min_density;  // tile traversal only above this many records per triangle
 };
 size_t sorted_bins();
@@ -165,6 +168,8 @@ void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t 
 // Tuning knob by name (trav, tile_density, tile_balance, tile_area,
 // bin_occupancy); value < 0 (or 0 for counts) only reads.  -1: unknown name.
 int sorted_option(const char* name, long long value, long long* old);
+// Name of the traversal kernel the last launch_sorted_trav chose.
+const char* hot_kernel_name();
 void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);
 size_t bary_compact_scratch(long long n_r);
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s);

@@ -149,7 +149,7 @@ def test_layered(cap, mode):
 # shared candidate lists, the per-thread binary and 4-wide walks.  Results
 # must not depend on the variant, the tile size, the spatial-bin resolution
 # or the tile fallback (candidate-list overflow -> per-record walk).
-TRAV = {"tile": 3, "binary": 1, "wide": 2}
+TRAV = {"tile": 3, "warptile": 4, "binary": 1, "wide": 2}
 
 
 @pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
@@ -173,7 +173,13 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"bin_occupancy": 1},                           # finest bins
     {"bin_occupancy": 1 << 20},                     # 256 bins
     {"bin_tma": 0},                                 # binning with plain loads
-], ids=["small", "huge", "many", "finebins", "coarsebins", "notma"])
+    {"bin_tma": 3},                                 # both binning passes over TMA
+    {"bin_rank": 1},                                # slots from the histogram pass
+    {"rec_ids": 0},                                 # 32-B records instead of ids
+    {"tile_wide": 1},                               # tile walk over 4-wide nodes
+    {"trav": 4, "warp_chunks": 1},                  # warp tiles of one chunk
+    {"trav": 4, "warp_chunks": 64},                 # warp tiles overflowing their lists
+], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
 def test_tile_knobs_bitwise(name, mode, knobs):
@@ -183,7 +189,7 @@ def test_tile_knobs_bitwise(name, mode, knobs):
     want = expected(fx, "cap32" if name == "layered" else "batch", mode)
     with contextlib.ExitStack() as stack:
         stack.enter_context(_lib.option("trav", TRAV["tile"]))
-        for k, v in knobs.items():
+        for k, v in sorted(knobs.items(), key=lambda kv: kv[0] != "trav"):
             stack.enter_context(_lib.option(k, v))
         got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
     assert_result_fields(result_dict(got), want, f"{name} {mode} {knobs}")
@@ -197,7 +203,7 @@ def test_tile_random_soup_vs_oracle(seed, n_tri, n_seg, mode):
     V, T, s, _ = _random_soup(seed, n_tri, n_seg)
     e = s + np.random.default_rng(seed + 100).uniform(-1.5, 1.5, size=s.shape).astype(np.float32)
     want = O.run_batch(V, T, s, e, mode=mode, max_stack=10**6)
-    for variant in ("tile", "binary"):
+    for variant in ("tile", "warptile", "binary"):
         with _lib.option("trav", TRAV[variant]):
             got = rs.run_batch(rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e),
                                rs.EngineConfig(mode=mode, tree="fast"))
