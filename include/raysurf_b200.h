@@ -117,6 +117,14 @@ RS_API int rs_query_stats(const rs_tree *tree, const float *d_starts, const floa
                    int mode, int max_collisions, int max_stack, int ref_semantics,
                    int64_t *internal_visits, int64_t *exact_tests, void *stream);
 
+/* sort_segments_by_morton (reference engine.py:125-147) on device: writes
+ * the segments in Z-order of their f64 midpoints (per-axis 21-bit
+ * quantisation over the midpoints' support, 63-bit interleave, stable by
+ * (code, index)) and perm[k] = original index of sorted slot k (int64, as
+ * the reference's np.lexsort result).  Stream-ordered; does not synchronise. */
+RS_API int rs_sort_segments(const float *d_starts, const float *d_ends, int64_t n,
+                            float *d_out_starts, float *d_out_ends, int64_t *d_perm, void *stream);
+
 /* All-pairs baseline (no BVH), device arrays, dense outputs as rs_query. */
 RS_API int rs_baseline(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
                 const float *d_starts, const float *d_ends, int64_t n_r, int mode,

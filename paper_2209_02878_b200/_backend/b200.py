@@ -172,17 +172,12 @@ def _device_tree_for(mesh, tree: BvhTree) -> DeviceTree:
     if isinstance(dt, DeviceTree):
         return dt
     # a tree built elsewhere (e.g. by the reference's own backend): rebuild it
-    # on device from its Morton order; the climb reproduces it exactly.
-    from .. import morton
-
-    v = np.asarray(mesh.vertices, np.float64)
-    t = np.asarray(mesh.triangles)
-    cent = (v[t[:, 0]] + v[t[:, 1]] + v[t[:, 2]]) / 3.0
-    codes = morton.encode(morton.quantize(cent))
-    order = np.lexsort((np.arange(codes.shape[0]), codes))
-    if not np.array_equal(order.astype(np.int32), np.asarray(tree.sorted_triangle_ids)):
+    # on device from the mesh (device keys + sort, reference kind); the climb
+    # reproduces it exactly when it came from this mesh's Morton order.
+    dt = DeviceTree(mesh, kind="reference")
+    if not np.array_equal(np.asarray(dt.download().sorted_triangle_ids),
+                          np.asarray(tree.sorted_triangle_ids)):
         raise ValueError("tree was not built from this mesh's Morton order")
-    dt = DeviceTree(mesh, sorted_codes=codes[order], sorted_ids=order.astype(np.int32))
     tree.device = dt
     return dt
 

@@ -47,6 +47,7 @@ _SIGS = {
     "rs_last_status": (i32, [p]),
     "rs_set_option": (i32, [C.c_char_p, C.c_longlong, p]),
     "rs_hot_kernel": (C.c_char_p, []),
+    "rs_sort_segments": (i32, [p, p, i64, p, p, p, p]),
 }
 
 _lib = None

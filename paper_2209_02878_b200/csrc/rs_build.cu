@@ -150,6 +150,63 @@ __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ cent, i
     vals[j] = j;
 }
 
+// -------------------------------------------------- segment Morton order ---
+// sort_segments_by_morton (engine.py:125-147): f64 midpoints (s + e) / 2,
+// their support, the reference's per-axis 21-bit quantisation and 63-bit
+// interleave (k_keys, reference kind), a stable sort by (code, index).
+
+__global__ void __launch_bounds__(256) k_mid_prep(const float* __restrict__ S,
+                                                  const float* __restrict__ E, int n, double* mid,
+                                                  RsHeader* hdr) {
+    __shared__ double red[8][6];
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double m = __ddiv_rn(__dadd_rn((double)S[3ll * j + k], (double)E[3ll * j + k]), 2.0);
+            mid[3ll * j + k] = m;
+            lo[k] = fmin(lo[k], m);
+            hi[k] = fmax(hi[k], m);
+        }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = warp_min(lo[k]);
+        hi[k] = warp_max(hi[k]);
+    }
+    if (l == 0)
+        for (int k = 0; k < 3; ++k) {
+            red[w][k] = lo[k];
+            red[w][3 + k] = hi[k];
+        }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int k = threadIdx.x;
+        double v = red[0][k];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) v = k < 3 ? fmin(v, red[i][k]) : fmax(v, red[i][k]);
+        if (isfinite(v)) {
+            if (k < 3) atomicMax(&hdr->smin[k], ~ord_of(v));
+            else atomicMax(&hdr->smax[k - 3], ord_of(v));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gather_segments(const int* __restrict__ order,
+                                                         const float* __restrict__ S,
+                                                         const float* __restrict__ E, int n,
+                                                         float* So, float* Eo, long long* perm) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int i = order[j];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        So[3ll * j + k] = S[3ll * i + k];
+        Eo[3ll * j + k] = E[3ll * i + k];
+    }
+    perm[j] = i;
+}
+
 // ------------------------------------------------------------ radix sort ---
 
 constexpr int kSortThreads = 256;
@@ -497,6 +554,30 @@ void launch_sort(unsigned long long* keys, int* vals, unsigned long long* keys_a
         unsigned long long* tk = ki; ki = ko; ko = tk;
         int* tv = vi; vi = vo; vo = tv;
     }
+}
+
+void launch_sort_segments(const float* S, const float* E, int n, float* So, float* Eo,
+                          long long* perm, void* scratch, cudaStream_t s) {
+    char* p = reinterpret_cast<char*>(scratch);
+    auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) & ~size_t(255); return r; };
+    RsHeader* hdr = reinterpret_cast<RsHeader*>(take(sizeof(RsHeader)));
+    double* mid = reinterpret_cast<double*>(take(24ull * n));
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(take(8ull * n));
+    unsigned long long* keys2 = reinterpret_cast<unsigned long long*>(take(8ull * n));
+    int* vals = reinterpret_cast<int*>(take(4ull * n));
+    int* vals2 = reinterpret_cast<int*>(take(4ull * n));
+    void* sort_scratch = take(sort_scratch_bytes(n, 8));
+    cudaMemsetAsync(hdr, 0, sizeof(RsHeader), s);
+    count_launches(3);
+    k_mid_prep<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(S, E, n, mid, hdr);
+    k_keys<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(mid, n, hdr, kTreeReference, keys, vals);
+    launch_sort(keys, vals, keys2, vals2, n, 8, sort_scratch, s);  // 8 passes: result in (keys, vals)
+    k_gather_segments<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(vals, S, E, n, So, Eo, perm);
+}
+
+size_t sort_segments_scratch_bytes(int n) {
+    auto r = [](size_t b) { return (b + 255) & ~size_t(255); };
+    return r(sizeof(RsHeader)) + r(24ull * n) + 2 * r(8ull * n) + 2 * r(4ull * n) + r(sort_scratch_bytes(n, 8));
 }
 
 void launch_climb(const float* V, const int* T, int n, const unsigned long long* codes,

@@ -648,6 +648,21 @@ int rs_query_stats(const rs_tree* t, const float* d_starts, const float* d_ends,
     return rc;
 }
 
+int rs_sort_segments(const float* d_starts, const float* d_ends, int64_t n, float* d_out_starts,
+                     float* d_out_ends, int64_t* d_perm, void* stream) {
+    if (n < 0 || n > 2147483647ll) return fail(RS_INVALID_ARG, "bad segment count");
+    if (n == 0) return RS_OK;
+    if (!(d_starts && d_ends && d_out_starts && d_out_ends && d_perm)) return fail(RS_INVALID_ARG, "null pointer");
+    cudaStream_t s = S(stream);
+    char* blk = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), sort_segments_scratch_bytes((int)n), s));
+    launch_sort_segments(d_starts, d_ends, (int)n, d_out_starts, d_out_ends,
+                         reinterpret_cast<long long*>(d_perm), blk, s);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(blk, s));
+    return RS_OK;
+}
+
 int rs_baseline(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
                 const float* d_starts, const float* d_ends, int64_t n_r, int mode,
                 int32_t* d_detected, int32_t* d_counts, int32_t* d_tri, float* d_dist,

@@ -37,6 +37,11 @@ void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
 size_t sort_scratch_bytes(int n, int passes);
 void launch_sort(unsigned long long* keys, int* vals, unsigned long long* keys_alt,
                  int* vals_alt, int n, int passes, void* scratch, cudaStream_t s);
+// sort_segments_by_morton on device (engine.py:125-147): So/Eo = the
+// segments in Z-order of their f64 midpoints, perm[k] = original index.
+size_t sort_segments_scratch_bytes(int n);
+void launch_sort_segments(const float* S, const float* E, int n, float* So, float* Eo,
+                          long long* perm, void* scratch, cudaStream_t s);
 void launch_climb(const float* V, const int* T, int n, const unsigned long long* codes,
                   const int* ids, const TreeArrays& ta, RsNode* nodes, RsLeaf* leaves,
                   RsHeader* hdr, cudaStream_t s);

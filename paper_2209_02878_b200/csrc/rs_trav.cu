@@ -457,48 +457,65 @@ constexpr int kCompactItems = 16;
 constexpr int kCompactTile = kCompactThreads * kCompactItems;
 
 __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a) {
-    __shared__ unsigned s_warp[kCompactThreads / 32];
+    // Striped tile: in round k, thread t owns segment base + k*256 + t, so
+    // every load and every output row of a round is coalesced across the
+    // warp.  A segment's rank = hits in earlier rounds of the tile + hits of
+    // lower threads in its round (ballots + a warp-sum scan per round).
+    __shared__ unsigned s_round[kCompactItems][kCompactThreads / 32];
     __shared__ unsigned long long s_prefix;
     __shared__ int s_tile;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1ull);
     __syncthreads();
     const long long tile = s_tile;
-    // thread t owns segments [base + t*16, base + t*16 + 16): contiguous rows
-    const long long i0 = tile * kCompactTile + (long long)threadIdx.x * kCompactItems;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const unsigned lt = (1u << l) - 1u;
+    const long long base = tile * kCompactTile;
     int tri[kCompactItems];
-    unsigned cnt = 0;
+    unsigned inwarp[kCompactItems];
 #pragma unroll
     for (int k = 0; k < kCompactItems; ++k) {
-        tri[k] = i0 + k < a.n_r ? a.best_tri[i0 + k] : -1;
-        cnt += tri[k] >= 0;
+        const long long i = base + k * kCompactThreads + threadIdx.x;
+        tri[k] = i < a.n_r ? a.best_tri[i] : -1;
+        const unsigned m = __ballot_sync(kFull, tri[k] >= 0);
+        inwarp[k] = __popc(m & lt);
+        if (l == 0) s_round[k][w] = __popc(m);
     }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    unsigned x = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(kFull, x, o);
-        if (l >= o) x += y;
-    }
-    if (l == 31) s_warp[w] = x;
     __syncthreads();
+    // warp 0: exclusive offsets of every (round, warp) cell in tile order
     if (w == 0) {
-        unsigned agg = 0, mine = 0;
-        for (int k = 0; k < kCompactThreads / 32; ++k) {
-            if (k == l) mine = agg;
-            agg += s_warp[k];
+        constexpr int kCells = kCompactItems * (kCompactThreads / 32);  // 128
+        unsigned v[kCells / 32], run = 0;
+#pragma unroll
+        for (int j = 0; j < kCells / 32; ++j) {
+            v[j] = (&s_round[0][0])[l * (kCells / 32) + j];
+            run += v[j];
         }
-        __syncwarp();
-        if (l < kCompactThreads / 32) s_warp[l] = mine;
+        unsigned x = run;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(kFull, x, o);
+            if (l >= o) x += y;
+        }
+        const unsigned agg = __shfl_sync(kFull, x, 31);
+        unsigned off = x - run;
+#pragma unroll
+        for (int j = 0; j < kCells / 32; ++j) {
+            const unsigned c = v[j];
+            (&s_round[0][0])[l * (kCells / 32) + j] = off;
+            off += c;
+        }
         const unsigned long long excl = lookback_warp(a.tile_status, tile, agg);
         if (l == 0) {
             s_prefix = excl;
-            if ((tile + 1) * kCompactTile >= a.n_r) *a.n_hits = excl + agg;
+            if (base + kCompactTile >= a.n_r) *a.n_hits = excl + agg;
         }
     }
     __syncthreads();
-    unsigned long long pos = s_prefix + s_warp[w] + x - cnt;
+    const unsigned long long tb = s_prefix;
+#pragma unroll
     for (int k = 0; k < kCompactItems; ++k) {
         if (tri[k] < 0) continue;
-        const long long i = i0 + k;
+        const long long i = base + k * kCompactThreads + threadIdx.x;
+        const unsigned long long pos = tb + s_round[k][w] + inwarp[k];
         const unsigned long long key = a.best_t[i];
         const double t = key == 0ull ? 0.0 : __longlong_as_double((long long)key);
         const float* s = a.starts + 3 * i;
@@ -513,11 +530,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
         a.point[3 * pos] = px;
         a.point[3 * pos + 1] = py;
         a.point[3 * pos + 2] = pz;
-        ++pos;
     }
 }
 
-// Dense barycentric rows from (best_t, best_tri) (plugin protocol path).
 __global__ void __launch_bounds__(256) k_bary_dense(CompactArgs a, int* detected, int* tri_out,
                                                     float* dist, float* points) {
     const long long i = blockIdx.x * 256ll + threadIdx.x;

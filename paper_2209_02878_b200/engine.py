@@ -160,24 +160,28 @@ def compute_segment_boxes(segments: SegmentBatch) -> np.ndarray:
 
 
 def sort_segments_by_morton(segments: SegmentBatch):
-    """Z-order of segment midpoints (engine.py:125-147): returns the permuted
-    batch and perm (perm[k] = original index of sorted slot k)."""
-    from . import morton
+    """Z-order of segment midpoints (engine.py:125-147), computed on the GPU
+    (rs_sort_segments): returns the permuted batch and perm (perm[k] =
+    original index of sorted slot k; int64 numpy for host batches, an int64
+    CUDA tensor for device batches)."""
+    import torch
 
     n = segments.count
     if n == 0:
         return segments, np.empty(0, dtype=np.int64)
     host = not segments.on_device
-    s = np.asarray(segments.starts if host else segments.starts.cpu())
-    e = np.asarray(segments.ends if host else segments.ends.cpu())
-    mid = (s.astype(np.float64) + e.astype(np.float64)) / 2.0
-    perm = morton.order_points(mid)
     if host:
-        return SegmentBatch(np.ascontiguousarray(s[perm]), np.ascontiguousarray(e[perm])), perm
-    import torch
-
-    p = torch.from_numpy(perm).to(segments.starts.device)
-    return SegmentBatch(segments.starts[p].contiguous(), segments.ends[p].contiguous()), perm
+        s = torch.from_numpy(np.ascontiguousarray(segments.starts)).cuda()
+        e = torch.from_numpy(np.ascontiguousarray(segments.ends)).cuda()
+    else:
+        s, e = segments.starts, segments.ends
+    so, eo = torch.empty_like(s), torch.empty_like(e)
+    perm = torch.empty(n, dtype=torch.int64, device=s.device)
+    _lib.check(_lib.lib().rs_sort_segments(_ptr(s), _ptr(e), n, _ptr(so), _ptr(eo), _ptr(perm),
+                                           _stream()))
+    if host:
+        return SegmentBatch(so.cpu().numpy(), eo.cpu().numpy()), perm.cpu().numpy()
+    return SegmentBatch(so, eo), perm
 
 
 # --------------------------------------------------------------- internals --
@@ -237,7 +241,7 @@ def _unpermute(rs: ResultSet, perm) -> ResultSet:
             import torch
 
             out = torch.empty_like(vals)
-            out[torch.from_numpy(perm).to(vals.device)] = vals
+            out[perm if torch.is_tensor(perm) else torch.from_numpy(perm).to(vals.device)] = vals
         else:
             out = np.empty_like(vals)
             out[perm] = vals
@@ -247,7 +251,7 @@ def _unpermute(rs: ResultSet, perm) -> ResultSet:
     if is_device_array(ri):
         import torch
 
-        pt = torch.from_numpy(perm).to(ri.device)
+        pt = perm if torch.is_tensor(perm) else torch.from_numpy(perm).to(ri.device)
         orig = pt[ri.long()]
         order = torch.argsort(orig)
         rs.ray_index = orig[order].to(torch.int32)

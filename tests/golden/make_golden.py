@@ -20,6 +20,7 @@ them):
   soup_*.npz    random-soup inputs (tests/helpers.py random_mesh/segments)
                 with results and max_stack overflow indices
   tree_*.npz    trees for random meshes (test_backends.py:46-84 sizes)
+  sortperm.npz  sort_segments_by_morton permutations (engine.py:125-147)
 """
 
 from __future__ import annotations
@@ -198,8 +199,30 @@ def layered_case(rs):
     print("wrote layered")
 
 
+def sortperm_case(rs):
+    """engine.sort_segments_by_morton (engine.py:125-147) on three batches:
+    the permutation and the permuted endpoints."""
+    from raysurf.engine import sort_segments_by_morton
+
+    d = {}
+    for name in ("scene_c1", "scene_s19", "soup_17", "layered"):
+        with np.load(OUT / f"{name}.npz") as z:
+            batch = rs.SegmentBatch.from_arrays(z["starts"], z["ends"])
+        sb, perm = sort_segments_by_morton(batch)
+        d[f"{name}_starts"] = batch.starts
+        d[f"{name}_ends"] = batch.ends
+        d[f"{name}_perm"] = perm
+        d[f"{name}_sorted_starts"] = sb.starts
+        d[f"{name}_sorted_ends"] = sb.ends
+    np.savez_compressed(OUT / "sortperm.npz", **d)
+    print("wrote sortperm")
+
+
 def main():
     rs = _import_reference()
+    if sys.argv[1:] == ["sortperm"]:
+        sortperm_case(rs)
+        return
     from raysurf import morton
 
     # morton known answers straight from the reference (test_morton.py:33-74)
@@ -223,6 +246,7 @@ def main():
     for n in (1, 2, 3, 7, 8, 100, 5000):                        # test_backends.py:46-56
         tree_case(rs, n, n)
     layered_case(rs)
+    sortperm_case(rs)
 
 
 if __name__ == "__main__":

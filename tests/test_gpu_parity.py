@@ -273,6 +273,30 @@ def test_edge_cases():
         assert r.num_crossing() == 0
 
 
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+@pytest.mark.parametrize("name", ("scene_c1", "scene_s19", "soup_17", "layered"))
+def test_sort_segments_by_morton_matches_reference(name, device):
+    """rs_sort_segments (device keys + stable radix sort) gives the
+    reference's permutation and permuted endpoints bit for bit."""
+    fx = load("sortperm")
+    s, e = fx[f"{name}_starts"], fx[f"{name}_ends"]
+    if device:
+        s, e = torch.from_numpy(s).cuda(), torch.from_numpy(e).cuda()
+    sb, perm = rs.sort_segments_by_morton(rs.SegmentBatch.from_arrays(s, e))
+    assert np.array_equal(_np(perm), fx[f"{name}_perm"])
+    assert np.array_equal(_np(sb.starts), fx[f"{name}_sorted_starts"])
+    assert np.array_equal(_np(sb.ends), fx[f"{name}_sorted_ends"])
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+@pytest.mark.parametrize("mode", MODES)
+def test_sort_rays_device_invariance(mode, device):
+    fx = load("scene_s19")
+    mesh, batch = mesh_batch(fx, device)
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, sort_rays=True))
+    assert_result_fields(result_dict(got), expected(fx, "batch", mode), f"sort_rays {mode}")
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_sort_rays_invariance(mode):
     fx = load("scene_s19")
