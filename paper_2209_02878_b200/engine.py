@@ -148,15 +148,19 @@ class EngineConfig:
             raise ValidationError("traversal stack needs capacity >= 1")
 
 
-def compute_segment_boxes(segments: SegmentBatch) -> np.ndarray:
-    """(N_r,6) f32 segment AABBs (engine.py:115-122).  Host helper kept for
-    API parity; the query kernel computes the same boxes in registers."""
-    s = np.asarray(segments.starts.cpu() if segments.on_device else segments.starts)
-    e = np.asarray(segments.ends.cpu() if segments.on_device else segments.ends)
-    boxes = np.empty((s.shape[0], 6), dtype=np.float32)
-    boxes[:, 0::2] = np.minimum(s, e)
-    boxes[:, 1::2] = np.maximum(s, e)
-    return boxes
+def compute_segment_boxes(segments: SegmentBatch):
+    """(N_r,6) f32 segment AABBs [xmin,xmax,ymin,ymax,zmin,zmax]
+    (engine.py:115-122), on the device; kept for API parity (the query
+    kernels form the same boxes in registers).  numpy in, numpy out."""
+    import torch
+
+    host = not segments.on_device
+    s = torch.from_numpy(segments.starts).cuda() if host else segments.starts
+    e = torch.from_numpy(segments.ends).cuda() if host else segments.ends
+    boxes = torch.empty((s.shape[0], 6), dtype=torch.float32, device=s.device)
+    boxes[:, 0::2] = torch.minimum(s, e)
+    boxes[:, 1::2] = torch.maximum(s, e)
+    return boxes.cpu().numpy() if host else boxes
 
 
 def sort_segments_by_morton(segments: SegmentBatch):
@@ -328,10 +332,28 @@ def run_device(mesh: Mesh, seg: SegmentBatch, config: EngineConfig, kind: str,
     return ResultSet(mode, n, ray_index=ray[:k], distance=dist[:k], triangle_id=tri[:k], point=pt[:k])
 
 
+def _to_device(mesh: Mesh, segments: SegmentBatch):
+    import torch
+
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    return (Mesh.from_arrays(t(mesh.vertices), t(mesh.triangles)),
+            SegmentBatch(t(segments.starts), t(segments.ends)))
+
+
+def _to_host(rs: ResultSet) -> ResultSet:
+    for f in ("crossing", "counts", "ray_index", "distance", "triangle_id", "point"):
+        v = getattr(rs, f)
+        if v is not None and is_device_array(v):
+            setattr(rs, f, v.cpu().numpy())
+    return rs
+
+
 def run_batch(mesh: Mesh, segments: SegmentBatch, config: EngineConfig | None = None) -> ResultSet:
     """Index the mesh on the GPU and test every segment (engine.py:222-290).
 
-    Results equal the reference's for the same inputs in every mode."""
+    Results equal the reference's for the same inputs in every mode.  With
+    sort_rays, host inputs are moved to the device once: the Morton order,
+    the query and the un-permutation all run there."""
     config = config or EngineConfig()
     config.validate()
     n = segments.count
@@ -340,6 +362,8 @@ def run_batch(mesh: Mesh, segments: SegmentBatch, config: EngineConfig | None = 
         raise ValidationError("mesh and segments must both be host arrays or both CUDA tensors")
     if n == 0 or mesh.num_triangles == 0:
         return _empty_result(config.mode, n, segments.starts.device if dev else None)
+    if config.sort_rays and not dev:
+        return _to_host(run_batch(*_to_device(mesh, segments), config))
     timings = {}
     perm = None
     if config.sort_rays:
@@ -369,6 +393,8 @@ def run_baseline_allpairs(mesh: Mesh, segments: SegmentBatch,
     dev = segments.on_device
     if n == 0 or mesh.num_triangles == 0:
         return _empty_result(config.mode, n, segments.starts.device if dev else None)
+    if not dev:  # compaction and un-permutation run on the device too
+        return _to_host(run_baseline_allpairs(*_to_device(mesh, segments), config))
     perm = None
     timings = {}
     if config.sort_rays:
@@ -389,13 +415,8 @@ def _assemble_dense(mode: str, out: dict, n: int, dev: bool) -> ResultSet:
         return ResultSet(mode, n, crossing=out["detected"])
     if mode == MODE_COUNT:
         return ResultSet(mode, n, counts=out["counts"])
-    det = out["detected"]
-    if dev:
-        import torch
+    import torch
 
-        idx = torch.nonzero(det).flatten()
-        return ResultSet(mode, n, ray_index=idx.to(torch.int32), distance=out["dist"][idx],
-                         triangle_id=out["tri"][idx], point=out["points"][idx])
-    idx = np.nonzero(det)[0].astype(np.int32)
-    return ResultSet(mode, n, ray_index=idx, distance=out["dist"][idx],
+    idx = torch.nonzero(out["detected"]).flatten()
+    return ResultSet(mode, n, ray_index=idx.to(torch.int32), distance=out["dist"][idx],
                      triangle_id=out["tri"][idx], point=out["points"][idx])
