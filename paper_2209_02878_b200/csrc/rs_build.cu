@@ -33,21 +33,25 @@ __device__ __forceinline__ double warp_max(double v) {
 
 __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
                                               const int* __restrict__ T, int n, double* cent,
-                                              RsHeader* hdr, TreeArrays ta, int do_centroids) {
+                                              RsHeader* hdr, TreeArrays ta, int do_centroids,
+                                              int lean) {
     __shared__ double red[8][6];
     __shared__ float fred[8][6];
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     float blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        // _reset_tree (lbvh.py:181-189) for internal slot j
-        reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[0] = make_float2(0.f, 0.f);
-        reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[1] = make_float2(0.f, 0.f);
-        reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[2] = make_float2(0.f, 0.f);
-        ta.child_l[j] = kEmpty;
-        ta.child_r[j] = kEmpty;
-        ta.range_l[j] = -1;
-        ta.range_r[j] = -1;
-        ta.int_tri[j] = -1;
+        // _reset_tree (lbvh.py:181-189) for internal slot j; a lean build
+        // (query-only tree, never downloaded) keeps just the visit counters
+        if (!lean) {
+            reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[0] = make_float2(0.f, 0.f);
+            reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[1] = make_float2(0.f, 0.f);
+            reinterpret_cast<float2*>(ta.int_bounds + 6ll * j)[2] = make_float2(0.f, 0.f);
+            ta.child_l[j] = kEmpty;
+            ta.child_r[j] = kEmpty;
+            ta.range_l[j] = -1;
+            ta.range_r[j] = -1;
+            ta.int_tri[j] = -1;
+        }
         ta.visit[j] = 0;
         const int ia = T[3ll * j], ib = T[3ll * j + 1], ic = T[3ll * j + 2];
 #pragma unroll
@@ -304,29 +308,69 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
             me.store((2ull << 62) | tot, cuda::memory_order_release);
         } else {
             me.store((1ull << 62) | tot, cuda::memory_order_release);
+            // look back 8 predecessors per round (independent loads in
+            // flight), summing aggregates until an inclusive prefix
+            constexpr int kLB = 8;
             for (int j = tile - 1; j >= 0;) {
-                cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> prev(
-                    status[(long long)j * 256 + d]);
-                const unsigned long long v = prev.load(cuda::memory_order_acquire);
-                const unsigned flag = (unsigned)(v >> 62);
-                if (flag == 0) continue;
-                excl += v & ((1ull << 62) - 1);
-                if (flag == 2) break;
-                --j;
+                unsigned long long v[kLB];
+#pragma unroll
+                for (int k = 0; k < kLB; ++k)
+                    v[k] = j - k >= 0 ? reinterpret_cast<volatile unsigned long long*>(status)[(long long)(j - k) * 256 + d]
+                                      : (2ull << 62);
+                int k = 0;
+                bool done = false;
+                for (; k < kLB; ++k) {
+                    const unsigned flag = (unsigned)(v[k] >> 62);
+                    if (flag == 0) break;  // not published yet: re-read from here
+                    excl += v[k] & ((1ull << 62) - 1);
+                    if (flag == 2) { done = true; break; }
+                }
+                if (done) break;
+                j -= k;
             }
+            __threadfence();
             me.store((2ull << 62) | (excl + tot), cuda::memory_order_release);
         }
         // exclusive global digit base: keys with smaller digits + tiles before us
         gbase[d] = (unsigned long long)dig_excl + excl;
+    }
+    // local reorder: stage the tile's keys in digit order in shared memory,
+    // then write each digit's run out contiguously (coalesced stores instead
+    // of one scattered 8-B + 4-B store per key)
+    __shared__ unsigned dig_local[256];
+    __shared__ unsigned long long s_key[kSortTile];
+    __shared__ int s_val[kSortTile];
+    {
+        // exclusive scan over digits of the tile's per-digit totals
+        unsigned x = tot;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        if (l == 31) wsum[w] = x;
+        __syncthreads();
+        unsigned before = 0;
+        for (int i = 0; i < w; ++i) before += wsum[i];
+        dig_local[d] = before + x - tot;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
         const int dd = dig[k];
         if (dd < 0) continue;
-        const unsigned long long pos = gbase[dd] + warp_cnt[w][dd] + rank[k];
-        kout[pos] = key[k];
-        vout[pos] = val[k];
+        const unsigned lp = dig_local[dd] + warp_cnt[w][dd] + rank[k];
+        s_key[lp] = key[k];
+        s_val[lp] = val[k];
+    }
+    __syncthreads();
+    const long long tile_base = (long long)tile * kSortTile;
+    const int cnt = n - tile_base < kSortTile ? (int)(n - tile_base) : kSortTile;
+    for (int j = threadIdx.x; j < cnt; j += kSortThreads) {
+        const unsigned long long kk = s_key[j];
+        const int dd = (int)((kk >> shift) & 255u);
+        const unsigned long long pos = gbase[dd] + (unsigned long long)(j - (int)dig_local[dd]);
+        kout[pos] = kk;
+        vout[pos] = s_val[j];
     }
 }
 
@@ -510,9 +554,10 @@ static int grid_for(long long n, int block, int cap) {
 }
 
 void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hdr,
-                 const TreeArrays& ta, bool centroids, cudaStream_t s) {
+                 const TreeArrays& ta, bool centroids, cudaStream_t s, bool lean) {
     count_launches(1);
-    k_prep<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(V, T, n, cent, hdr, ta, centroids ? 1 : 0);
+    k_prep<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(V, T, n, cent, hdr, ta, centroids ? 1 : 0,
+                                                     lean ? 1 : 0);
 }
 
 void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
@@ -585,6 +630,94 @@ void launch_climb(const float* V, const int* T, int n, const unsigned long long*
                   RsHeader* hdr, cudaStream_t s) {
     count_launches(1);
     k_climb<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(V, T, n, codes, ids, ta, nodes, leaves, hdr);
+}
+
+// ------------------------------------------------------------ lean climb ---
+// The same Apetrei climb (same parent choice, so the same tree) for trees
+// that are only queried: each arriving child writes its half of the
+// parent's 64-B RsNode (its exact box, its ref, its end of the parent's
+// range in d.z / d.w) before the acq_rel visit counter; the second arriver
+// reads the whole record back.  No reference SoA arrays, heights or parent
+// links: about half the climb's memory traffic.
+__global__ void __launch_bounds__(256) k_climb_lean(const float* __restrict__ V,
+                                                    const int* __restrict__ T, int n,
+                                                    const unsigned long long* __restrict__ codes,
+                                                    const int* __restrict__ ids, int* visit,
+                                                    RsNode* nodes, RsLeaf* leaves, RsHeader* hdr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int n_int = n - 1;
+    const int tid = ids[i];
+    const int ia = T[3ll * tid], ib = T[3ll * tid + 1], ic = T[3ll * tid + 2];
+    float a[3], b[3], c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a[k] = V[3ll * ia + k];
+        b[k] = V[3ll * ib + k];
+        c[k] = V[3ll * ic + k];
+    }
+    float box[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // mesh.py:74-75
+        box[2 * k] = fminf(fminf(a[k], b[k]), c[k]);
+        box[2 * k + 1] = fmaxf(fmaxf(a[k], b[k]), c[k]);
+    }
+    RsLeaf lf;
+    lf.p0 = make_float4(a[0], a[1], a[2], b[0]);
+    lf.p1 = make_float4(b[1], b[2], c[0], c[1]);
+    lf.p2 = make_float4(c[2], __int_as_float(tid), 0.f, 0.f);
+    leaves[i] = lf;
+    if (n == 1) {
+        hdr->root = n_int;
+        return;
+    }
+    int left = i, right = i, node = n_int + i;
+    for (;;) {
+        if (left == 0 && right == n - 1) {
+            hdr->root = node;
+            return;
+        }
+        int parent;
+        float* rec;
+        if (left == 0 || (right != n - 1 && delta_less(codes, ids, right, left - 1))) {
+            parent = right;  // we are the left child
+            rec = reinterpret_cast<float*>(nodes + parent);
+            reinterpret_cast<float4*>(rec)[0] = make_float4(box[0], box[1], box[2], box[3]);
+            reinterpret_cast<float2*>(rec)[2] = make_float2(box[4], box[5]);
+            reinterpret_cast<int*>(rec)[12] = node;
+            reinterpret_cast<int*>(rec)[14] = left;
+        } else {
+            parent = left - 1;  // we are the right child
+            rec = reinterpret_cast<float*>(nodes + parent);
+            reinterpret_cast<float2*>(rec)[3] = make_float2(box[0], box[1]);
+            reinterpret_cast<float4*>(rec)[2] = make_float4(box[2], box[3], box[4], box[5]);
+            reinterpret_cast<int*>(rec)[13] = node;
+            reinterpret_cast<int*>(rec)[15] = right;
+        }
+        cuda::atomic_ref<int, cuda::thread_scope_device> vis(visit[parent]);
+        if (vis.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // first arriver stops
+        const float4 q0 = __ldcg(reinterpret_cast<const float4*>(rec));
+        const float4 q1 = __ldcg(reinterpret_cast<const float4*>(rec) + 1);
+        const float4 q2 = __ldcg(reinterpret_cast<const float4*>(rec) + 2);
+        const int4 q3 = __ldcg(reinterpret_cast<const int4*>(rec) + 3);
+        // _core.pyx:181-183: parent box = (min, max) of the children's
+        box[0] = q0.x < q1.z ? q0.x : q1.z;
+        box[1] = q0.y > q1.w ? q0.y : q1.w;
+        box[2] = q0.z < q2.x ? q0.z : q2.x;
+        box[3] = q0.w > q2.y ? q0.w : q2.y;
+        box[4] = q1.x < q2.z ? q1.x : q2.z;
+        box[5] = q1.y > q2.w ? q1.y : q2.w;
+        left = q3.z;
+        right = q3.w;
+        node = parent;
+    }
+}
+
+void launch_climb_lean(const float* V, const int* T, int n, const unsigned long long* codes,
+                       const int* ids, int* visit, RsNode* nodes, RsLeaf* leaves, RsHeader* hdr,
+                       cudaStream_t s) {
+    count_launches(1);
+    k_climb_lean<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(V, T, n, codes, ids, visit, nodes, leaves, hdr);
 }
 
 }  // namespace rs

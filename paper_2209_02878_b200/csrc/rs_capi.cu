@@ -184,12 +184,19 @@ bool need_nodes4() {
     return buffer || trav == 2 || (wide && trav != 1);
 }
 
+// RS_LEAN_BUILD=0: query-only fast trees keep the full reference SoA (A/B).
+static const bool g_lean_build = [] {
+    const char* e = getenv("RS_LEAN_BUILD");
+    return !(e && e[0] == '0');
+}();
+
 // after_prep (optional) runs on the host right after k_prep is enqueued on
 // `s`: the fast query forks its binning onto a second stream there, since it
 // needs only the root box k_prep computes.
 int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
                const uint64_t* sorted_codes, const int* sorted_ids, cudaStream_t s,
-               rs_tree** out, const std::function<int(rs_tree*)>& after_prep = nullptr) {
+               rs_tree** out, const std::function<int(rs_tree*)>& after_prep = nullptr,
+               bool lean = false) {
     int rc = check_mesh(n_v, n_t);
     if (rc) return rc;
     if (kind != kTreeReference && kind != kTreeFast)
@@ -217,14 +224,18 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
         int* vals = c.take<int>(n);
         int* vals2 = c.take<int>(n);
         void* sort_scratch = c.take<char>(sb);
-        launch_prep(V, T, n, cent, t->hdr, t->ta, true, s);
+        // lean: a fast tree only this call queries (never downloaded, no
+        // 4-wide collapse): records only
+        lean = lean && kind == kTreeFast && !need_nodes4() && g_lean_build;
+        launch_prep(V, T, n, cent, t->hdr, t->ta, true, s, lean);
         if (after_prep) {
             rc = after_prep(t);
             if (rc) return rc;
         }
         launch_keys(cent, n, t->hdr, kind, keys, vals, s);
         launch_sort(keys, vals, keys2, vals2, n, passes, sort_scratch, s);
-        launch_climb(V, T, n, keys, vals, t->ta, t->nodes, t->leaves, t->hdr, s);
+        if (lean) launch_climb_lean(V, T, n, keys, vals, t->ta.visit, t->nodes, t->leaves, t->hdr, s);
+        else launch_climb(V, T, n, keys, vals, t->ta, t->nodes, t->leaves, t->hdr, s);
         if (kind == kTreeFast && need_nodes4()) launch_collapse(n, t->ta, t->nodes, t->nodes4, t->hdr, s);
         CK(cudaFreeAsync(scratch, s));
     }
@@ -716,7 +727,7 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
     };
     ev_record(0, s);
     rs_tree* t = nullptr;
-    rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, s, &t, fork);
+    rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, s, &t, fork, true);
     if (rc) return rc;
     CK(cudaStreamWaitEvent(s, g_fork.bin, 0));
     rc = fast_trav(t, d_starts, d_ends, n_r, mode, o, f, false, s);
@@ -749,7 +760,7 @@ static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d
         return rc ? rc : rc2;
     }
     ev_record(0, s);
-    int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t);
+    int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
     if (rc) return rc;
     const int ref = tree_kind == kTreeReference;
     if (mode == kBarycentric)
@@ -785,7 +796,7 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
         return rs_free(t, s);
     }
     ev_record(0, s);
-    int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t);
+    int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
     if (rc) return rc;
     if (tree_kind == kTreeFast && !g_binary_fast) {
         FastOut o;
@@ -1053,7 +1064,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     CK(cudaMemcpyAsync(dV, h_verts, 12ull * n_v, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dT, h_tris, 12ull * n_t, cudaMemcpyHostToDevice, s));
     rs_tree* t = nullptr;
-    rc = build_impl(dV, n_v, dT, n_t, tree_kind, nullptr, nullptr, s, &t);
+    rc = build_impl(dV, n_v, dT, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
     if (rc) {
         cudaFreeAsync(blk, s);
         return rc;

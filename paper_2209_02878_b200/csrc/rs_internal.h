@@ -31,7 +31,11 @@ struct TreeArrays {
 };
 
 void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hdr,
-                 const TreeArrays& ta, bool centroids, cudaStream_t s);
+                 const TreeArrays& ta, bool centroids, cudaStream_t s, bool lean = false);
+// Query-only climb: RsNode/RsLeaf records and the root, no SoA fields.
+void launch_climb_lean(const float* V, const int* T, int n, const unsigned long long* codes,
+                       const int* ids, int* visit, RsNode* nodes, RsLeaf* leaves, RsHeader* hdr,
+                       cudaStream_t s);
 void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
                  unsigned long long* keys, int* vals, cudaStream_t s);
 size_t sort_scratch_bytes(int n, int passes);

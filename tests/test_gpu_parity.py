@@ -195,6 +195,28 @@ def test_tile_knobs_bitwise(name, mode, knobs):
     assert_result_fields(result_dict(got), want, f"{name} {mode} {knobs}")
 
 
+def test_lean_build_matches_full_build():
+    """run_batch builds query-only trees with the lean climb (RsNode records
+    only); the same mesh through the full climb (rs_build, downloadable)
+    must give identical results on every variant."""
+    sc = rs.generate_scene(3000, 60_000, 0.5, seed=5)
+    dm = rs.Mesh.from_arrays(torch.from_numpy(sc.mesh.vertices).cuda(),
+                             torch.from_numpy(sc.mesh.triangles).cuda())
+    db = rs.SegmentBatch.from_arrays(torch.from_numpy(sc.segments.starts).cuda(),
+                                     torch.from_numpy(sc.segments.ends).cuda())
+    for mode in MODES:
+        lean = result_dict(rs.run_batch(dm, db, rs.EngineConfig(mode=mode, tree="fast")))
+        dt = b200.DeviceTree(sc.mesh, kind="fast")
+        full = dt.query_dense(sc.segments.starts, sc.segments.ends, mode, 32, 64, ref_semantics=False)
+        det = _np(full["detected"] if mode != "count" else full["counts"])
+        if mode == "boolean":
+            assert np.array_equal(lean["crossing"], det)
+        elif mode == "count":
+            assert np.array_equal(lean["counts"], det)
+        else:
+            assert np.array_equal(lean["ray_index"], np.nonzero(det)[0])
+
+
 @pytest.mark.parametrize("seed,n_tri,n_seg", [(11, 64, 20000), (12, 700, 30000), (13, 3000, 60000)])
 @pytest.mark.parametrize("mode", MODES)
 def test_tile_random_soup_vs_oracle(seed, n_tri, n_seg, mode):
