@@ -184,6 +184,13 @@ bool need_nodes4() {
     return buffer || trav == 2 || (wide && trav != 1);
 }
 
+// RS_ZERO_COPY=1: the compaction writes barycentric rows straight into mapped
+// pinned host outputs (A/B: 3% slower than the lagged per-chunk copies).
+static const bool g_zero_copy = [] {
+    const char* e = getenv("RS_ZERO_COPY");
+    return e && e[0] == '1';
+}();
+
 // RS_LEAN_BUILD=0: query-only fast trees keep the full reference SoA (A/B).
 static const bool g_lean_build = [] {
     const char* e = getenv("RS_LEAN_BUILD");
@@ -291,6 +298,8 @@ struct Pipe {
     int device = -1;
     cudaStream_t copy = nullptr, copy2 = nullptr;  // H2D (both endpoint arrays) / D2H
     cudaEvent_t ev_in[2], ev_in2[2], ev_q[2], ev_out[2], ev_blk;
+    RsStatus* hst = nullptr;  // pinned per-chunk statuses (barycentric row counts)
+    int64_t hst_cap = 0;
 };
 thread_local Pipe g_pipe;
 
@@ -386,6 +395,7 @@ struct FastOut {
     int32_t *c_ray = nullptr, *c_tri = nullptr;
     float *c_dist = nullptr, *c_pt = nullptr;
     long long ray_offset = 0;
+    unsigned long long* row_base = nullptr;  // compact rows: running row count across chunks
 };
 
 struct FastScratch {
@@ -478,7 +488,7 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
     launch_sorted_trav(sorted_args(t, d_s, d_e, n_r, o, f), mode, stats, s);
     if (mode == kBarycentric) {
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
-                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset};
+                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base};
         if (o.c_ray) launch_bary_compact(ca, s);
         else launch_bary_dense(ca, o.det, o.tri, o.dist, o.pts, s);
     }
@@ -511,7 +521,7 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
     launch_exact(ea, mode, stats, s);
     if (bary) {
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
-                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset};
+                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base};
         if (o.c_ray) launch_bary_compact(ca, s);
         else launch_bary_dense(ca, o.det, o.tri, o.dist, o.pts, s);
     }
@@ -1020,11 +1030,29 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     chunk_rays = ((chunk_rays + 127) / 128) * 128;
     const int64_t nchunks = (n_r + chunk_rays - 1) / chunk_rays;
     const bool bary = mode == kBarycentric;
+    const bool fast_tree = tree_kind == kTreeFast && !g_binary_fast;
+    // Barycentric rows into pinned host outputs: each chunk's compaction
+    // writes its rows straight into the caller's (mapped) host arrays at the
+    // running row count, so the D2H overlaps the remaining uploads instead
+    // of one copy after the last chunk.  Pageable outputs: device rows + copy.
+    int32_t *zray = nullptr, *ztri = nullptr;
+    float *zdist = nullptr, *zpt = nullptr;
+    bool zc = false;
+    if (bary && fast_tree && g_zero_copy && !g_buffer_path) {
+        void *a = nullptr, *b = nullptr, *cc = nullptr, *d = nullptr;
+        zc = cudaHostGetDevicePointer(&a, h_ray, 0) == cudaSuccess &&
+             cudaHostGetDevicePointer(&b, h_dist, 0) == cudaSuccess &&
+             cudaHostGetDevicePointer(&cc, h_tri, 0) == cudaSuccess &&
+             cudaHostGetDevicePointer(&d, h_pt, 0) == cudaSuccess;
+        cudaGetLastError();
+        zray = static_cast<int32_t*>(a); zdist = static_cast<float*>(b);
+        ztri = static_cast<int32_t*>(cc); zpt = static_cast<float*>(d);
+    }
 
     // one device block: mesh, 2x chunk inputs, outputs, status, tile status
     const size_t mesh_b = align256(12ull * n_v) + align256(12ull * n_t);
     const size_t in_b = 2 * 2 * align256(12ull * chunk_rays);
-    const size_t out_b = bary ? 4 * align256(12ull * n_r) : 2 * align256(4ull * chunk_rays);
+    const size_t out_b = bary ? (zc ? 256 : 4 * align256(12ull * n_r)) : 2 * align256(4ull * chunk_rays);
     const size_t tiles_b = align256(compact_scratch_bytes(chunk_rays)) * (size_t)nchunks;
     const size_t st_b = align256(sizeof(RsStatus) * (size_t)nchunks);
     char* blk = nullptr;
@@ -1040,7 +1068,10 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     int32_t* dflag[2] = {nullptr, nullptr};
     int32_t *dray = nullptr, *dtri = nullptr;
     float *ddist = nullptr, *dpt = nullptr;
-    if (bary) {
+    unsigned long long* d_rows = nullptr;
+    if (bary && zc) {
+        d_rows = c.take<unsigned long long>(1);
+    } else if (bary) {
         dray = c.take<int32_t>(n_r);
         ddist = c.take<float>(n_r);
         dtri = c.take<int32_t>(n_r);
@@ -1058,6 +1089,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     // the mesh upload and the build overlap chunk 0's transfer.
     cudaStream_t h2d = cp, d2h = g_pipe.copy2;
     CK(cudaMemsetAsync(tiles, 0, tiles_b + st_b, s));
+    if (d_rows) CK(cudaMemsetAsync(d_rows, 0, sizeof(unsigned long long), s));
     CK(cudaEventRecord(g_pipe.ev_blk, s));
     CK(cudaStreamWaitEvent(h2d, g_pipe.ev_blk, 0));
     CK(cudaStreamWaitEvent(d2h, g_pipe.ev_blk, 0));
@@ -1078,6 +1110,30 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
             if (rc) return rc;
         }
     unsigned long long running = 0;  // barycentric rows already placed
+    // Barycentric rows (device-compacted per chunk) come back one chunk
+    // behind: once chunk j's status has landed in pinned memory the host
+    // knows its row count and queues the row copies at the running offset,
+    // while the device already works on chunk j+1.
+    const bool lagged = bary && !zc && !g_buffer_path;
+    if (lagged && g_pipe.hst_cap < nchunks) {
+        if (g_pipe.hst) cudaFreeHost(g_pipe.hst);
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&g_pipe.hst), sizeof(RsStatus) * nchunks,
+                         cudaHostAllocDefault));
+        g_pipe.hst_cap = nchunks;
+    }
+    auto retire = [&](int64_t j) -> int {
+        CK(cudaEventSynchronize(g_pipe.ev_out[j & 1]));
+        const size_t m = (size_t)g_pipe.hst[j].hits;
+        const int64_t lo = j * chunk_rays;
+        if (m && !g_pipe.hst[j].bad && !g_pipe.hst[j].internal) {
+            CK(cudaMemcpyAsync(h_ray + running, dray + lo, 4 * m, cudaMemcpyDeviceToHost, d2h));
+            CK(cudaMemcpyAsync(h_dist + running, ddist + lo, 4 * m, cudaMemcpyDeviceToHost, d2h));
+            CK(cudaMemcpyAsync(h_tri + running, dtri + lo, 4 * m, cudaMemcpyDeviceToHost, d2h));
+            CK(cudaMemcpyAsync(h_pt + 3 * running, dpt + 3 * lo, 12 * m, cudaMemcpyDeviceToHost, d2h));
+        }
+        running += m;
+        return RS_OK;
+    };
     for (int64_t k = 0; k < nchunks; ++k) {
         const int b = (int)(k & 1);
         const int64_t lo = k * chunk_rays;
@@ -1092,7 +1148,10 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
             fs[b].st = st + k;
             FastOut o;
             o.ray_offset = lo;
-            if (bary) {
+            if (bary && zc) {
+                o.c_ray = zray; o.c_dist = zdist; o.c_tri = ztri; o.c_pt = zpt;
+                o.row_base = d_rows;
+            } else if (bary) {
                 o.c_ray = dray + lo; o.c_dist = ddist + lo; o.c_tri = dtri + lo; o.c_pt = dpt + 3 * lo;
             } else {
                 o.flags = dflag[b];
@@ -1126,8 +1185,14 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
             CK(cudaStreamWaitEvent(d2h, g_pipe.ev_q[b], 0));
             CK(cudaMemcpyAsync(h_flags + lo, dflag[b], 4ull * cnt, cudaMemcpyDeviceToHost, d2h));
             CK(cudaEventRecord(g_pipe.ev_out[b], d2h));
+        } else if (lagged) {
+            CK(cudaStreamWaitEvent(d2h, g_pipe.ev_q[b], 0));
+            CK(cudaMemcpyAsync(g_pipe.hst + k, st + k, sizeof(RsStatus), cudaMemcpyDeviceToHost, d2h));
+            CK(cudaEventRecord(g_pipe.ev_out[b], d2h));
+            if (k >= 1 && (rc = retire(k - 1))) return rc;
         }
     }
+    if (lagged && (rc = retire(nchunks - 1))) return rc;
     cp = d2h;
     // statuses of every chunk; barycentric row counts come back with them
     RsStatus* hst = new RsStatus[nchunks];
@@ -1165,7 +1230,11 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
         if (hst[k].bad && (!badv || ~hst[k].bad < ~badv)) badv = hst[k].bad;
         internal |= hst[k].internal;
     }
-    if (bary && !badv && !internal) {
+    if (bary && zc) {
+        for (int64_t k = 0; k < nchunks; ++k) running += hst[k].hits;  // rows already in place
+    } else if (bary && lagged) {
+        CK(cudaStreamSynchronize(cp));  // rows already queued chunk by chunk
+    } else if (bary && !badv && !internal) {
         for (int64_t k = 0; k < nchunks; ++k) {
             const int64_t lo = k * chunk_rays;
             const size_t m = (size_t)hst[k].hits;

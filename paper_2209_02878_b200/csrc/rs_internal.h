@@ -137,6 +137,7 @@ struct CompactArgs {
     unsigned long long* tile_counter;
     unsigned long long* n_hits;
     long long ray_offset;
+    unsigned long long* row_base;  // optional: rows land at *row_base + rank, then *row_base += hits
 };
 void launch_trav(const TravArgs& a, bool stats, cudaStream_t s);
 
@@ -181,7 +182,7 @@ int sorted_option(const char* name, long long value, long long* old);
 const char* hot_kernel_name();
 void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);
 size_t bary_compact_scratch(long long n_r);
-void launch_bary_compact(const CompactArgs& a, cudaStream_t s);
+void launch_bary_compact(const CompactArgs& a, cudaStream_t s);  // also advances a.row_base
 void launch_bary_dense(const CompactArgs& a, int* detected, int* tri, float* dist, float* points,
                        cudaStream_t s);
 

@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
         }
     }
     __syncthreads();
-    const unsigned long long tb = s_prefix;
+    const unsigned long long tb = s_prefix + (a.row_base ? *a.row_base : 0ull);
 #pragma unroll
     for (int k = 0; k < kCompactItems; ++k) {
         if (tri[k] < 0) continue;
@@ -608,11 +608,19 @@ size_t bary_compact_scratch(long long n_r) {
     return (size_t)((n_r + kCompactTile - 1) / kCompactTile) * 8 + 8;
 }
 
+__global__ void k_advance_rows(unsigned long long* row_base, const unsigned long long* n_hits) {
+    *row_base += *n_hits;
+}
+
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s) {
     if (a.n_r <= 0) return;
     count_launches(1);
     k_bary_compact<<<(unsigned)((a.n_r + kCompactTile - 1) / kCompactTile), kCompactThreads, 0,
                      s>>>(a);
+    if (a.row_base) {
+        count_launches(1);
+        k_advance_rows<<<1, 1, 0, s>>>(a.row_base, a.n_hits);
+    }
 }
 
 void launch_bary_dense(const CompactArgs& a, int* detected, int* tri, float* dist, float* points,

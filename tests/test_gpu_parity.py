@@ -336,6 +336,29 @@ def test_host_pipeline_chunking(mode, chunk):
     assert_result_fields(result_dict(got), expected(fx, "batch", mode), f"chunk {chunk}")
 
 
+@pytest.mark.parametrize("chunk", [0, 1000])
+def test_host_pipeline_pageable_outputs(chunk):
+    """rs_run_batch_host with plain (pageable) numpy outputs: barycentric rows
+    come back by copy instead of being written into mapped host memory."""
+    import ctypes as C
+
+    fx = load("scene_c1")
+    V, T, s, e = fx["vertices"], fx["triangles"], fx["starts"], fx["ends"]
+    n = s.shape[0]
+    ray, dist = np.zeros(n, np.int32), np.zeros(n, np.float32)
+    tri, pt = np.zeros(n, np.int32), np.zeros((n, 3), np.float32)
+    n_hits, bad = C.c_int64(0), C.c_int64(-1)
+    p = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+    st = _lib.lib().rs_run_batch_host(p(V), V.shape[0], p(T), T.shape[0], p(s), p(e), n,
+                                      _lib.MODE_TAGS["barycentric"], _lib.TREE_KINDS["fast"], 32, 64,
+                                      chunk, None, p(ray), p(dist), p(tri), p(pt), C.byref(n_hits),
+                                      C.byref(bad), None)
+    _lib.check(st)
+    k = n_hits.value
+    got = {"ray_index": ray[:k], "distance": dist[:k], "triangle_id": tri[:k], "point": pt[:k]}
+    assert_result_fields(got, expected(fx, "batch", "barycentric"), f"pageable chunk {chunk}")
+
+
 # ----------------------------------------------- full-size, property-based --
 
 @pytest.mark.parametrize("mode", MODES)
