@@ -182,28 +182,41 @@ __device__ __forceinline__ void root_info_compute(const RsHeader* hdr, const Sor
     ri.bc = bits[pc];
 }
 
+// Key bit position of axis bit i for an axis of role r (0 = A, 1 = B, 2 = C;
+// see RootInfo): all three axes interleave over C's bits, then A and B,
+// then A alone.
+__device__ __forceinline__ int key_pos(int role, int i, int bb, int bc) {
+    if (i < bc) return 3 * i + role;
+    if (i < bb) return 3 * bc + 2 * (i - bc) + role;
+    return 2 * bb + bc + (i - bb);
+}
+
 // One thread derives the bin geometry; the CTA reads it from shared memory
-// and fills the bit-spreading tables the key uses (spread3 of C's <= 7 bits,
-// spread2 of up to 10 bits): table lookups instead of ~30 ALU ops per key.
+// and fills per-axis deposit tables: the key is the OR over axes of
+// T[axis][chunk][7-bit chunk of q], 9 table lookups instead of ~80 ALU ops
+// (axis ranking, bit spreading) per key.
 struct BinLut {
-    unsigned s3[128];
-    unsigned s2[1024];
+    unsigned t[3][3][128];
 };
 __device__ __forceinline__ void root_info(const SortedArgs& a, RootInfo& ri, const BinLut*& lut) {
     __shared__ RootInfo s_ri;
     __shared__ BinLut s_lut;
     if (threadIdx.x == 0) root_info_compute(a.hdr, a, s_ri);
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-        if (i < 128) s_lut.s3[i] = spread3((unsigned)i);
-        s_lut.s2[i] = spread2((unsigned)i);
-    }
     __syncthreads();
     ri = s_ri;
+    for (int e = threadIdx.x; e < 3 * 3 * 128; e += blockDim.x) {
+        const int axis = e / 384, chunk = (e / 128) % 3, v = e % 128;
+        const int role = axis == ri.pa ? 0 : (axis == ri.pb ? 1 : 2);
+        const int nb = axis == ri.pa ? (ri.nbits - ri.bb - ri.bc) : (axis == ri.pb ? ri.bb : ri.bc);
+        unsigned out = 0;
+        for (int j = 0; j < 7; ++j) {
+            const int i = 7 * chunk + j;
+            if (((v >> j) & 1) && i < nb) out |= 1u << key_pos(role, i, ri.bb, ri.bc);
+        }
+        s_lut.t[axis][chunk][v] = out;
+    }
+    __syncthreads();
     lut = &s_lut;
-}
-
-__device__ __forceinline__ unsigned pick3(const unsigned q[3], int k) {
-    return k == 0 ? q[0] : (k == 1 ? q[1] : q[2]);
 }
 
 // Returns the bin of a live segment, or -1 when its box misses the root box
@@ -217,19 +230,14 @@ __device__ __forceinline__ int seg_bin(const float s[3], const float e[3], const
     const bool live = (b[0] <= ri.hi[0]) & (b[1] >= ri.lo[0]) & (b[2] <= ri.hi[1]) &
                       (b[3] >= ri.lo[1]) & (b[4] <= ri.hi[2]) & (b[5] >= ri.lo[2]);
     if (!live) return -1;
-    unsigned q[3];
+    unsigned key = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const float c = 0.5f * (b[2 * k] + b[2 * k + 1]);
         const float f = fminf(fmaxf((c - ri.lo[k]) * ri.scale[k], 0.f), (float)ri.qmax[k]);
-        q[k] = (unsigned)f;
+        const unsigned q = (unsigned)f;
+        key |= lut->t[k][0][q & 127u] | lut->t[k][1][(q >> 7) & 127u] | lut->t[k][2][q >> 14];
     }
-    const unsigned qa = pick3(q, ri.pa), qb = pick3(q, ri.pb), qc = pick3(q, ri.pc);
-    const unsigned mc = (1u << ri.bc) - 1u;
-    const unsigned mb = (1u << (ri.bb - ri.bc)) - 1u;
-    unsigned key = lut->s3[qa & mc] | (lut->s3[qb & mc] << 1) | (lut->s3[qc] << 2);
-    key |= (lut->s2[(qa >> ri.bc) & mb] | (lut->s2[(qb >> ri.bc) & mb] << 1)) << (3 * ri.bc);
-    key |= (qa >> ri.bb) << (2 * ri.bb + ri.bc);
     return (int)key;
 }
 
