@@ -121,20 +121,32 @@ __device__ __forceinline__ bool mt_hit_pre(double ax, double ay, double az, doub
     const double det =
         __dadd_rn(__dadd_rn(__dmul_rn(e1x, px), __dmul_rn(e1y, py)), __dmul_rn(e1z, pz));
     if (fabs(det) < kDetEps) return false;
-    const double inv_det = __ddiv_rn(1.0, det);
     const double tx = __dsub_rn(sx, ax), ty = __dsub_rn(sy, ay), tz = __dsub_rn(sz, az);
-    const double u = __dmul_rn(
-        __dadd_rn(__dadd_rn(__dmul_rn(tx, px), __dmul_rn(ty, py)), __dmul_rn(tz, pz)), inv_det);
-    if (u < -kBaryEps || u > 1.0 + kBaryEps) return false;
+    const double un = __dadd_rn(__dadd_rn(__dmul_rn(tx, px), __dmul_rn(ty, py)), __dmul_rn(tz, pz));
     const double qx = __dsub_rn(__dmul_rn(ty, e1z), __dmul_rn(tz, e1y));
     const double qy = __dsub_rn(__dmul_rn(tz, e1x), __dmul_rn(tx, e1z));
     const double qz = __dsub_rn(__dmul_rn(tx, e1y), __dmul_rn(ty, e1x));
-    const double v = __dmul_rn(
-        __dadd_rn(__dadd_rn(__dmul_rn(dx, qx), __dmul_rn(dy, qy)), __dmul_rn(dz, qz)), inv_det);
+    const double vn = __dadd_rn(__dadd_rn(__dmul_rn(dx, qx), __dmul_rn(dy, qy)), __dmul_rn(dz, qz));
+    const double tn = __dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz));
+    // Division-free rejection of clear misses.  u = fl(un * fl(1/det)) is
+    // un/det to within 2.3e-16 relative, so comparing un*sign(det) against
+    // the bounds scaled by |det| with a 1e-9 relative margin only rejects
+    // segments the exact tests below reject too.  (t < 0 needs |t/det| >
+    // 1e-300 so that t cannot round to -0.0, which the reference accepts.)
+    {
+        const double ad = fabs(det);
+        const double su = det < 0.0 ? -un : un, sv = det < 0.0 ? -vn : vn, st = det < 0.0 ? -tn : tn;
+        const double m = ad * (1.0 + 1e-9);
+        if (su < -kBaryEps * m || su > (1.0 + kBaryEps) * m || sv < -kBaryEps * m ||
+            st < -1e-300 * ad || st > m)
+            return false;
+    }
+    const double inv_det = __ddiv_rn(1.0, det);
+    const double u = __dmul_rn(un, inv_det);
+    if (u < -kBaryEps || u > 1.0 + kBaryEps) return false;
+    const double v = __dmul_rn(vn, inv_det);
     if (v < -kBaryEps || __dadd_rn(u, v) > 1.0 + kBaryEps) return false;
-    const double t = __dmul_rn(
-        __dadd_rn(__dadd_rn(__dmul_rn(e2x, qx), __dmul_rn(e2y, qy)), __dmul_rn(e2z, qz)),
-        inv_det);
+    const double t = __dmul_rn(tn, inv_det);
     if (t < 0.0 || t > 1.0) return false;
     *t_out = t;
     return true;
