@@ -400,3 +400,73 @@ def test_device_path_matches_host_path_c2():
     dev = rs.run_batch(dm, db, rs.EngineConfig(mode="barycentric"))
     for f in ("ray_index", "distance", "triangle_id", "point"):
         assert np.array_equal(_np(getattr(dev, f)), getattr(host, f)), f
+
+
+# ------------------------------------------------ adversarial exact tests --
+
+def _adversarial(kind: str, seed: int):
+    """Inputs that sit on the exact test's decision boundaries: segments
+    through grid vertices and along shared edges, in the triangle plane,
+    zero-length, degenerate (collinear / repeated-coordinate) triangles,
+    duplicate triangles, and extreme coordinate scales."""
+    rng = np.random.default_rng(seed)
+    g = 12
+    gx, gy = np.meshgrid(np.arange(g + 1, dtype=np.float32), np.arange(g + 1, dtype=np.float32),
+                         indexing="ij")
+    z = rng.integers(-2, 3, size=gx.shape).astype(np.float32) * 0.5
+    V = np.column_stack([gx.ravel(), gy.ravel(), z.ravel()]).astype(np.float32)
+    ix, iy = np.meshgrid(np.arange(g), np.arange(g), indexing="ij")
+    ix, iy = ix.ravel(), iy.ravel()
+    c00, c10 = ix * (g + 1) + iy, (ix + 1) * (g + 1) + iy
+    c01, c11 = c00 + 1, c10 + 1
+    T = np.concatenate([np.column_stack([c00, c10, c11]), np.column_stack([c00, c11, c01])]).astype(np.int32)
+    n = 6000
+    # endpoints on the lattice of vertices, edge midpoints and cell centres
+    pts = rng.integers(0, 2 * g + 1, size=(n, 2)).astype(np.float32) * 0.5
+    s = np.column_stack([pts, np.full(n, -3.0, np.float32)])
+    e = np.column_stack([pts, np.full(n, 3.0, np.float32)])
+    if kind == "lattice":
+        slant = rng.random(n) < 0.3
+        e[slant, :2] = rng.integers(0, 2 * g + 1, size=(slant.sum(), 2)) * 0.5
+    elif kind == "inplane":
+        # segments inside triangle planes (z from the plane of a flat patch)
+        V[:, 2] = 0.0
+        s[:, 2] = 0.0
+        e[:, :2] = rng.integers(0, 2 * g + 1, size=(n, 2)) * 0.5
+        e[:, 2] = np.where(rng.random(n) < 0.5, 0.0, 1e-7)
+    elif kind == "degenerate":
+        # collinear and repeated-coordinate triangles, duplicates, zero-length segments
+        extra = np.array([[0, 1, 2], [0, 0 + (g + 1), 0 + 2 * (g + 1)], [5, 6, 5 + (g + 1)]], np.int32)
+        T = np.concatenate([T, T[: len(T) // 3], extra])
+        V[1] = V[0]  # two vertices share coordinates
+        zero = rng.random(n) < 0.2
+        e[zero] = s[zero]
+        s[zero, 2] = 0.0
+        e[zero, 2] = 0.0
+    elif kind == "scale":
+        f = np.float32(10.0 ** rng.integers(-5, 6))
+        V *= f
+        s *= f
+        e *= f
+    return V, T, s.astype(np.float32), e.astype(np.float32)
+
+
+@pytest.mark.parametrize("variant", ["auto", "tile", "warptile", "binary", "reference"])
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("kind", ["lattice", "inplane", "degenerate", "scale"])
+def test_adversarial_vs_oracle(kind, mode, variant):
+    V, T, s, e = _adversarial(kind, {"lattice": 1, "inplane": 2, "degenerate": 3, "scale": 4}[kind])
+    want = O.run_batch(V, T, s, e, mode=mode, max_stack=10**6)
+    mesh, batch = rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e)
+    if variant == "reference":
+        cfg = rs.EngineConfig(mode=mode, tree="reference", max_stack=256)
+        got = rs.run_batch(mesh, batch, cfg)
+    else:
+        cfg = rs.EngineConfig(mode=mode, tree="fast")
+        with contextlib.ExitStack() as stack:
+            if variant != "auto":
+                stack.enter_context(_lib.option("trav", TRAV[variant]))
+            got = rs.run_batch(mesh, batch, cfg)
+    assert_result_fields(result_dict(got), want, f"{kind} {mode} {variant}")
+    base = rs.run_baseline_allpairs(mesh, batch, rs.EngineConfig(mode=mode))
+    assert_result_fields(result_dict(base), want, f"{kind} {mode} baseline")
