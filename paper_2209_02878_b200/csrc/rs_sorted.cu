@@ -956,7 +956,10 @@ constexpr int kTileThreads = 128;
 constexpr int kTileMinBlocks = RS_TILE_MIN_BLOCKS;
 constexpr int kTileLCap = 512;  // leaf candidates per tile
 constexpr int kTileFCap = 256;  // walk frontier per level
-constexpr int kCutDepth = 6;    // the walk starts from the tree's depth-6 cut
+#ifndef RS_CUT_DEPTH
+#define RS_CUT_DEPTH 6
+#endif
+constexpr int kCutDepth = RS_CUT_DEPTH;  // the walk starts from the depth-6 cut (7, 8 measured slower: smem vs occupancy)
 constexpr int kCutCap = 1 << kCutDepth;
 constexpr int kWCap = 16;       // warp candidates prepared per round
 
@@ -1122,35 +1125,42 @@ __device__ __forceinline__ void build_cut(SM& sm, const RsSlot* nodes, int n_int
     __syncwarp();
     for (int d = 1; d < kCutDepth; ++d) {
         // expand every internal entry into its two children (in place: entry
-        // i's children go to slots i and n + (rank of i among internals))
-        float4 xy[2];
-        float2 z[2];
-        int ref = -1, c0 = -1, c1 = -1;
-        bool internal = false;
-        if (lane < n) {
-            ref = sm.cref[lane];
-            internal = ref < n_int;
-            if (internal) {
-                float f0[8], f1[8];
-                ld_slot(nodes + 2 * ref, f0);
-                ld_slot(nodes + 2 * ref + 1, f1);
-                xy[0] = make_float4(f0[0], f0[1], f0[2], f0[3]);
-                z[0] = make_float2(f0[4], f0[5]);
-                c0 = __float_as_int(f1[4]);
-                xy[1] = make_float4(f0[6], f0[7], f1[0], f1[1]);
-                z[1] = make_float2(f1[2], f1[3]);
-                c1 = __float_as_int(f1[5]);
+        // i's children go to slots i and n + (rank of i among internals)),
+        // 32 entries per step; all reads of a step precede its writes
+        const int n0 = n;
+        int added = 0;
+        for (int c0i = 0; c0i < n0; c0i += 32) {
+            const int i = c0i + lane;
+            float4 xy[2];
+            float2 z[2];
+            int c0 = -1, c1 = -1;
+            bool internal = false;
+            if (i < n0) {
+                const int ref = sm.cref[i];
+                internal = ref < n_int;
+                if (internal) {
+                    float f0[8], f1[8];
+                    ld_slot(nodes + 2 * ref, f0);
+                    ld_slot(nodes + 2 * ref + 1, f1);
+                    xy[0] = make_float4(f0[0], f0[1], f0[2], f0[3]);
+                    z[0] = make_float2(f0[4], f0[5]);
+                    c0 = __float_as_int(f1[4]);
+                    xy[1] = make_float4(f0[6], f0[7], f1[0], f1[1]);
+                    z[1] = make_float2(f1[2], f1[3]);
+                    c1 = __float_as_int(f1[5]);
+                }
             }
+            const unsigned m = __ballot_sync(kFullMask, internal);
+            __syncwarp();
+            if (internal) {
+                const int extra = n0 + added + __popc(m & ((1u << lane) - 1u));
+                sm.cxy[i] = xy[0]; sm.cz[i] = z[0]; sm.cref[i] = c0;
+                sm.cxy[extra] = xy[1]; sm.cz[extra] = z[1]; sm.cref[extra] = c1;
+            }
+            added += __popc(m);
+            __syncwarp();
         }
-        const unsigned m = __ballot_sync(kFullMask, internal);
-        __syncwarp();
-        if (internal) {
-            const int extra = n + __popc(m & ((1u << lane) - 1u));
-            sm.cxy[lane] = xy[0]; sm.cz[lane] = z[0]; sm.cref[lane] = c0;
-            sm.cxy[extra] = xy[1]; sm.cz[extra] = z[1]; sm.cref[extra] = c1;
-        }
-        n += __popc(m);
-        __syncwarp();
+        n = n0 + added;
     }
     if (lane == 0) sm.ncut = n;
 }
@@ -1213,13 +1223,13 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
                 else { u[k] = fminf(u[k], sm.part[w][k]); u[k + 1] = fmaxf(u[k + 1], sm.part[w][k + 1]); }
             }
         // 2. breadth-first walk with U, from the cut
-        if (tid < ncut) {
-            const int ref = sm.cref[tid];
-            if (box_ov(u, sm.cxy[tid], sm.cz[tid])) {
+        for (int ci = tid; ci < ncut; ci += kTileThreads) {
+            const int ref = sm.cref[ci];
+            if (box_ov(u, sm.cxy[ci], sm.cz[ci])) {
                 if (ref >= n_int) {
                     const int k = atomicAdd(&sm.nl, 1);
-                    sm.lxy[k] = sm.cxy[tid];
-                    sm.lz[k] = sm.cz[tid];
+                    sm.lxy[k] = sm.cxy[ci];
+                    sm.lz[k] = sm.cz[ci];
                     sm.lid[k] = ref - n_int;
                 } else {
                     sm.front[0][atomicAdd(&sm.nf[0], 1)] = ref;
