@@ -954,7 +954,10 @@ constexpr int kTileThreads = 128;
 #define RS_TILE_MIN_BLOCKS 8
 #endif
 constexpr int kTileMinBlocks = RS_TILE_MIN_BLOCKS;
-constexpr int kTileLCap = 512;  // leaf candidates per tile
+#ifndef RS_TILE_LCAP
+#define RS_TILE_LCAP 512
+#endif
+constexpr int kTileLCap = RS_TILE_LCAP;  // leaf candidates per tile
 constexpr int kTileFCap = 256;  // walk frontier per level
 #ifndef RS_CUT_DEPTH
 #define RS_CUT_DEPTH 6
