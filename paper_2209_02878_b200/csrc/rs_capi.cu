@@ -9,6 +9,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <string>
 
@@ -1026,9 +1027,23 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     if (rc) return rc;
     cudaStream_t s = S(stream);
     cudaStream_t cp = g_pipe.copy;
-    if (chunk_rays <= 0) chunk_rays = n_r > (8ll << 20) ? (n_r + 7) / 8 : (n_r > (1 << 20) ? (n_r + 3) / 4 : n_r);
+    const bool auto_chunks = chunk_rays <= 0;
+    if (auto_chunks) chunk_rays = n_r > (8ll << 20) ? (n_r + 7) / 8 : (n_r > (1 << 20) ? (n_r + 3) / 4 : n_r);
     chunk_rays = ((chunk_rays + 127) / 128) * 128;
-    const int64_t nchunks = (n_r + chunk_rays - 1) / chunk_rays;
+    // chunk boundaries: uniform; with automatic sizing the last chunk is
+    // split 3:1 so the work left after the final upload (its query and flag
+    // copy) is a quarter chunk
+    std::vector<int64_t> bounds;
+    for (int64_t lo = 0; lo < n_r; lo += chunk_rays) bounds.push_back(lo);
+    if (auto_chunks && bounds.size() > 1) {
+        const int64_t last = bounds.back(), rem = n_r - last;
+        const int64_t cut = ((rem * 3 / 4 + 127) / 128) * 128;
+        if (cut > 0 && cut < rem) bounds.push_back(last + cut);
+    }
+    bounds.push_back(n_r);
+    const int64_t nchunks = (int64_t)bounds.size() - 1;
+    auto chunk_lo = [&](int64_t k) { return bounds[k]; };
+    auto chunk_cnt = [&](int64_t k) { return bounds[k + 1] - bounds[k]; };
     const bool bary = mode == kBarycentric;
     const bool fast_tree = tree_kind == kTreeFast && !g_binary_fast;
     // Barycentric rows into pinned host outputs: each chunk's compaction
@@ -1124,7 +1139,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     auto retire = [&](int64_t j) -> int {
         CK(cudaEventSynchronize(g_pipe.ev_out[j & 1]));
         const size_t m = (size_t)g_pipe.hst[j].hits;
-        const int64_t lo = j * chunk_rays;
+        const int64_t lo = chunk_lo(j);
         if (m && !g_pipe.hst[j].bad && !g_pipe.hst[j].internal) {
             CK(cudaMemcpyAsync(h_ray + running, dray + lo, 4 * m, cudaMemcpyDeviceToHost, d2h));
             CK(cudaMemcpyAsync(h_dist + running, ddist + lo, 4 * m, cudaMemcpyDeviceToHost, d2h));
@@ -1136,8 +1151,8 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     };
     for (int64_t k = 0; k < nchunks; ++k) {
         const int b = (int)(k & 1);
-        const int64_t lo = k * chunk_rays;
-        const int64_t cnt = (lo + chunk_rays <= n_r) ? chunk_rays : n_r - lo;
+        const int64_t lo = chunk_lo(k);
+        const int64_t cnt = chunk_cnt(k);
         if (k >= 2) CK(cudaStreamWaitEvent(h2d, g_pipe.ev_q[b], 0));  // input buffer b free again
         CK(cudaMemcpyAsync(din[b][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
         CK(cudaMemcpyAsync(din[b][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
@@ -1205,8 +1220,8 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
         // sized to what its traversal claimed
         for (int64_t k = 0; k < nchunks; ++k) {
             if ((long long)hst[k].cand_count <= fs[0].cap) continue;
-            const int64_t lo = k * chunk_rays;
-            const int64_t cnt = (lo + chunk_rays <= n_r) ? chunk_rays : n_r - lo;
+            const int64_t lo = chunk_lo(k);
+            const int64_t cnt = chunk_cnt(k);
             CK(cudaStreamSynchronize(cp));
             CK(cudaMemcpyAsync(din[0][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, s));
             CK(cudaMemcpyAsync(din[0][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, s));
@@ -1236,7 +1251,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
         CK(cudaStreamSynchronize(cp));  // rows already queued chunk by chunk
     } else if (bary && !badv && !internal) {
         for (int64_t k = 0; k < nchunks; ++k) {
-            const int64_t lo = k * chunk_rays;
+            const int64_t lo = chunk_lo(k);
             const size_t m = (size_t)hst[k].hits;
             if (m) {
                 CK(cudaMemcpyAsync(h_ray + running, dray + lo, 4 * m, cudaMemcpyDeviceToHost, cp));
