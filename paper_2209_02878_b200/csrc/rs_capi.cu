@@ -53,6 +53,11 @@ thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr}
 thread_local float g_build_ms = 0.f, g_query_ms = 0.f, g_hot_ms = 0.f;
 thread_local bool g_ev_valid = false;
 
+// hot-kernel mark mask: bit 0 records the start event, bit 1 the end event
+// (a batch traversed in two parts marks the first part's start and the
+// second part's end)
+thread_local int g_hot_mark_mask = 3;
+
 void ev_record(int k, cudaStream_t s) {
     if (!g_timing) return;
     if (!g_ev[k]) cudaEventCreate(&g_ev[k]);
@@ -484,8 +489,9 @@ static int fast_bin(const rs_tree* t, const float* d_s, const float* d_e, int64_
 
 // Phase 2: traversal (+ barycentric compaction).
 static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
-                     const FastOut& o, FastScratch& f, bool stats, cudaStream_t s) {
-    ev_record(1, s);
+                     const FastOut& o, FastScratch& f, bool stats, cudaStream_t s,
+                     bool first = true, bool last = true) {
+    if (first) ev_record(1, s);
     launch_sorted_trav(sorted_args(t, d_s, d_e, n_r, o, f), mode, stats, s);
     if (mode == kBarycentric) {
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
@@ -494,7 +500,7 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
         else launch_bary_dense(ca, o.det, o.tri, o.dist, o.pts, s);
     }
     CK(cudaGetLastError());
-    ev_record(2, s);
+    if (last) ev_record(2, s);
     return RS_OK;
 }
 
@@ -704,7 +710,7 @@ int rs_baseline(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_
 
 struct Fork {
     cudaStream_t aux = nullptr;
-    cudaEvent_t prep = nullptr, bin = nullptr;
+    cudaEvent_t prep = nullptr, bin = nullptr, bin2 = nullptr;
 };
 static thread_local Fork g_fork;
 
@@ -713,7 +719,24 @@ static int fork_init() {
     CK(cudaStreamCreateWithFlags(&g_fork.aux, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g_fork.prep, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g_fork.bin, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g_fork.bin2, cudaEventDisableTiming));
     return RS_OK;
+}
+
+// RS_PIPELINE_PARTS=2: large batches are binned and traversed in two halves,
+// so the second half's binning (memory-bound) overlaps the first half's
+// traversal (latency-bound).
+static int pipeline_parts() {
+    static const int v = [] {
+        const char* e = getenv("RS_PIPELINE_PARTS");
+        return e && e[0] == '2' ? 2 : 1;
+    }();
+    return v;
+}
+
+__global__ void k_merge_status(RsStatus* dst, const RsStatus* src) {
+    dst->hits += src->hits;
+    dst->internal |= src->internal;
 }
 
 // Fast-tree run_batch with the binning forked onto a second stream right
@@ -726,14 +749,35 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
     int rc = fork_init();
     if (rc) return rc;
     cudaStream_t aux = g_fork.aux;
+    const bool two = pipeline_parts() == 2 && n_r >= (2ll << 20) && !o.det;
+    const int64_t n1 = two ? ((n_r / 2 + 1023) / 1024) * 1024 : n_r, n2 = n_r - n1;
+    FastOut o1 = o, o2 = o;
+    FastScratch f2;
     auto fork = [&](rs_tree* t) -> int {
         CK(cudaEventRecord(g_fork.prep, s));
         CK(cudaStreamWaitEvent(aux, g_fork.prep, 0));
-        int r = fast_alloc(f, n_r, mode, 2ll * n_r + 4096, aux);
+        int r = fast_alloc(f, n1, mode, 2ll * n1 + 4096, aux);
         if (r) return r;
-        r = fast_bin(t, d_starts, d_ends, n_r, mode, o, f, aux);
+        if (two) {
+            r = fast_alloc(f2, n2, mode, 2ll * n2 + 4096, aux);
+            if (r) return r;
+            if (o.flags) o2.flags = o.flags + n1;
+            o2.ray_offset = o.ray_offset + n1;
+            if (mode == kBarycentric) {  // both halves compact into the same rows, in order
+                unsigned long long* rows = reinterpret_cast<unsigned long long*>(f.n_live + 8);
+                CK(cudaMemsetAsync(rows, 0, sizeof(unsigned long long), aux));
+                o1.row_base = rows;
+                o2.row_base = rows;
+            }
+        }
+        r = fast_bin(t, d_starts, d_ends, n1, mode, o1, f, aux);
         if (r) return r;
         CK(cudaEventRecord(g_fork.bin, aux));
+        if (two) {
+            r = fast_bin(t, d_starts + 3 * n1, d_ends + 3 * n1, n2, mode, o2, f2, aux);
+            if (r) return r;
+            CK(cudaEventRecord(g_fork.bin2, aux));
+        }
         return RS_OK;
     };
     ev_record(0, s);
@@ -741,7 +785,19 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
     rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, s, &t, fork, true);
     if (rc) return rc;
     CK(cudaStreamWaitEvent(s, g_fork.bin, 0));
-    rc = fast_trav(t, d_starts, d_ends, n_r, mode, o, f, false, s);
+    if (!two) {
+        rc = fast_trav(t, d_starts, d_ends, n_r, mode, o1, f, false, s);
+    } else {
+        g_hot_mark_mask = 1;
+        rc = fast_trav(t, d_starts, d_ends, n1, mode, o1, f, false, s, true, false);
+        g_hot_mark_mask = 2;
+        CK(cudaStreamWaitEvent(s, g_fork.bin2, 0));
+        if (!rc) rc = fast_trav(t, d_starts + 3 * n1, d_ends + 3 * n1, n2, mode, o2, f2, false, s, false, true);
+        g_hot_mark_mask = 3;
+        count_launches(1);
+        k_merge_status<<<1, 1, 0, s>>>(f.st, f2.st);
+        CK(cudaFreeAsync(f2.blk, s));
+    }
     *tree_out = t;
     return rc;
 }
@@ -1001,7 +1057,9 @@ RS_API int rs_last_status(unsigned long long* out8) {
 
 }  // extern "C"
 
-void rs::hot_kernel_mark(int which, cudaStream_t s) { ev_record(3 + which, s); }
+void rs::hot_kernel_mark(int which, cudaStream_t s) {
+    if (g_hot_mark_mask & (1 << which)) ev_record(3 + which, s);
+}
 
 extern "C" {
 

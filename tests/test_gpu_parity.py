@@ -6,6 +6,7 @@ bit-exact as well (f64 Moller-Trumbore in the reference op order, no FMA).
 """
 
 import contextlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -388,6 +389,34 @@ def test_c2_full_size_ground_truth(mode):
         assert np.array_equal(got.triangle_id[pos], want["triangle_id"])
         assert np.array_equal(got.point[pos], want["point"])
         assert np.array_equal(got.distance[pos], want["distance"])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_two_part_pipeline_matches(mode):
+    """RS_PIPELINE_PARTS=2 (halves binned and traversed on two streams, both
+    compacting into the same rows) gives the same results as one part."""
+    import subprocess, sys, os
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.');"
+        "import paper_2209_02878_b200 as rs;"
+        "sc = rs.generate_scene(3000, 3_000_000, 0.5, seed=9);"
+        "dm = rs.Mesh.from_arrays(torch.from_numpy(sc.mesh.vertices).cuda(), torch.from_numpy(sc.mesh.triangles).cuda());"
+        "db = rs.SegmentBatch.from_arrays(torch.from_numpy(sc.segments.starts).cuda(), torch.from_numpy(sc.segments.ends).cuda());"
+        f"r = rs.run_batch(dm, db, rs.EngineConfig(mode='{mode}'));"
+        "out = [getattr(r, f) for f in ('crossing', 'counts', 'ray_index', 'distance', 'triangle_id', 'point') if getattr(r, f) is not None];"
+        "np.savez(sys.argv[1], *[o.cpu().numpy() for o in out])"
+    )
+    import tempfile
+    res = []
+    for parts in ("1", "2"):
+        f = tempfile.mktemp(suffix=".npz")
+        env = dict(os.environ, RS_PIPELINE_PARTS=parts)
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=env,
+                       cwd=str(Path(__file__).resolve().parents[1]))
+        with np.load(f) as z:
+            res.append([z[k] for k in sorted(z.files)])
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
 
 
 def test_device_path_matches_host_path_c2():
