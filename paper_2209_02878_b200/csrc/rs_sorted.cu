@@ -955,16 +955,19 @@ constexpr int kTileThreads = 128;
 #endif
 constexpr int kTileMinBlocks = RS_TILE_MIN_BLOCKS;
 #ifndef RS_TILE_LCAP
-#define RS_TILE_LCAP 512
+#define RS_TILE_LCAP 256
 #endif
-constexpr int kTileLCap = RS_TILE_LCAP;  // leaf candidates per tile
+constexpr int kTileLCap = RS_TILE_LCAP;  // leaf candidates per tile (256: smaller shared footprint leaves more L1; C2 -5%)
 constexpr int kTileFCap = 256;  // walk frontier per level
 #ifndef RS_CUT_DEPTH
 #define RS_CUT_DEPTH 6
 #endif
 constexpr int kCutDepth = RS_CUT_DEPTH;  // the walk starts from the depth-6 cut (7, 8 measured slower: smem vs occupancy)
 constexpr int kCutCap = 1 << kCutDepth;
-constexpr int kWCap = 16;       // warp candidates prepared per round
+#ifndef RS_WCAP
+#define RS_WCAP 16
+#endif
+constexpr int kWCap = RS_WCAP;  // warp candidates prepared per round
 
 // One warp's prepared candidates: the triangle's first vertex and edges in
 // f64 (formed once per warp instead of once per exact test), its exact box
