@@ -156,7 +156,8 @@ RS_API int rs_run_batch_host(const float *h_verts, int64_t n_v, const int32_t *h
  * ResultSet.timings "construct"/"query", engine.py:238-288): when enabled,
  * CUDA events on the caller's stream bracket the build, the whole query and
  * the dominant (traversal) kernel; rs_last_timings returns the last call's
- * milliseconds. */
+ * milliseconds.  enable = 2 records only the traversal kernel's events (the
+ * lightest instrumentation; build/query then read 0). */
 RS_API int rs_set_timing(int enable);
 RS_API int rs_last_timings(float *build_ms, float *query_ms, float *hot_kernel_ms);
 

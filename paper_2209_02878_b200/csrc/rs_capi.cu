@@ -48,7 +48,7 @@ const bool g_binary_fast = [] {
 
 // Phase timing (engine.py's timings dict, measured on device): when enabled,
 // events bracket the build and the query kernel on the caller's stream.
-thread_local bool g_timing = false;
+thread_local int g_timing = 0;  // 0 off, 1 phases + hot kernel, 2 hot kernel only
 thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 thread_local float g_build_ms = 0.f, g_query_ms = 0.f, g_hot_ms = 0.f;
 thread_local bool g_ev_valid = false;
@@ -59,7 +59,7 @@ thread_local bool g_ev_valid = false;
 thread_local int g_hot_mark_mask = 3;
 
 void ev_record(int k, cudaStream_t s) {
-    if (!g_timing) return;
+    if (!g_timing || (g_timing == 2 && k < 3)) return;
     if (!g_ev[k]) cudaEventCreate(&g_ev[k]);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
@@ -948,7 +948,7 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         std::memcpy(key.p, ptrs, sizeof ptrs);
         key.n_v = n_v; key.n_t = n_t; key.n_r = n_r;
         key.mode = mode; key.kind = tree_kind; key.mc = max_coll; key.ms = max_stack;
-        key.timing = g_timing ? 1 : 0;
+        key.timing = g_timing;
         key.opt_gen = g_opt_gen.load();
         GraphEntry* ge = nullptr;
         {
@@ -1012,8 +1012,11 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
                                s);
     }
     if (g_timing && (rc == RS_OK || rc == RS_STACK_OVERFLOW)) {
-        cudaEventElapsedTime(&g_build_ms, g_ev[0], g_ev[1]);
-        cudaEventElapsedTime(&g_query_ms, g_ev[1], g_ev[2]);
+        g_build_ms = g_query_ms = 0.f;
+        if (g_timing == 1) {
+            cudaEventElapsedTime(&g_build_ms, g_ev[0], g_ev[1]);
+            cudaEventElapsedTime(&g_query_ms, g_ev[1], g_ev[2]);
+        }
         g_hot_ms = 0.f;
         if (g_ev[3] && g_ev[4]) cudaEventElapsedTime(&g_hot_ms, g_ev[3], g_ev[4]);
         g_ev_valid = true;
@@ -1022,7 +1025,7 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
 }
 
 RS_API int rs_set_timing(int enable) {
-    g_timing = enable != 0;
+    g_timing = enable == 2 ? 2 : (enable != 0 ? 1 : 0);
     g_ev_valid = false;
     return RS_OK;
 }
