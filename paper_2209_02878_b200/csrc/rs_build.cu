@@ -128,7 +128,7 @@ __device__ __forceinline__ unsigned quant1(double p, double lo, double ext, doub
 
 __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ cent, int n,
                                               const RsHeader* __restrict__ hdr, int kind,
-                                              unsigned long long* keys, int* vals) {
+                                              unsigned long long* keys, int* vals, int fast_mode) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     double lo[3], ext[3], gmax;
@@ -137,9 +137,17 @@ __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ cent, i
         lo[k] = from_ord(~hdr->smin[k]);
         ext[k] = __dsub_rn(from_ord(hdr->smax[k]), lo[k]);
     }
-    if (kind == kTreeFast) {  // isotropic grid: one extent for every axis
-        const double e = fmax(fmax(ext[0], ext[1]), ext[2]);
-        ext[0] = ext[1] = ext[2] = e;
+    if (kind == kTreeFast) {
+        // 30-bit keys.  Isotropic grid (one extent for every axis) for flat
+        // meshes: a thin terrain's z splits would come early and prune
+        // nothing for segments crossing it.  Per-axis grid (fast_mode 1, or
+        // auto when the thinnest centroid extent is at least a fifth of the
+        // widest): stacked surfaces separate near the root, so segments in
+        // the empty space between them are culled in a few levels.
+        const double emax = fmax(fmax(ext[0], ext[1]), ext[2]);
+        const double emin = fmin(fmin(ext[0], ext[1]), ext[2]);
+        const bool per_axis = fast_mode == 1 || (fast_mode == 2 && emin >= 0.2 * emax);
+        if (!per_axis) ext[0] = ext[1] = ext[2] = emax;
         gmax = (double)((1u << kIsoBits) - 1u);
     } else {
         gmax = kGridMax21;
@@ -563,7 +571,7 @@ void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hd
 void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
                  unsigned long long* keys, int* vals, cudaStream_t s) {
     count_launches(1);
-    k_keys<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(cent, n, hdr, kind, keys, vals);
+    k_keys<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(cent, n, hdr, kind, keys, vals, fast_key_mode());
 }
 
 void launch_collapse(int n, const TreeArrays& ta, const RsNode* nodes, RsNode4* nodes4,
@@ -615,7 +623,7 @@ void launch_sort_segments(const float* S, const float* E, int n, float* So, floa
     cudaMemsetAsync(hdr, 0, sizeof(RsHeader), s);
     count_launches(3);
     k_mid_prep<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(S, E, n, mid, hdr);
-    k_keys<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(mid, n, hdr, kTreeReference, keys, vals);
+    k_keys<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(mid, n, hdr, kTreeReference, keys, vals, 0);
     launch_sort(keys, vals, keys2, vals2, n, 8, sort_scratch, s);  // 8 passes: result in (keys, vals)
     k_gather_segments<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(vals, S, E, n, So, Eo, perm);
 }

@@ -178,6 +178,8 @@ void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t 
 // Tuning knob by name (trav, tile_density, tile_balance, tile_area,
 // bin_occupancy); value < 0 (or 0 for counts) only reads.  -1: unknown name.
 int sorted_option(const char* name, long long value, long long* old);
+// Fast-tree key grid: 0 isotropic, 1 per-axis, 2 auto (option "fast_keys").
+int fast_key_mode();
 // Name of the traversal kernel the last launch_sorted_trav chose.
 const char* hot_kernel_name();
 void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);

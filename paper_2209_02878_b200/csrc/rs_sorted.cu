@@ -1540,6 +1540,7 @@ struct SortedOpts {
     int bin_rank = 0;            // histogram pass records slots; scatter without atomics (A/B: slower)
     int rec_ids = 0;             // scatter writes segment ids, not 32-B records (A/B: traversal gathers thrash L1)
     int auto_tile = 3;           // auto's dense variant: 3 CTA tiles, 4 warp tiles
+    int fast_keys = 0;           // fast-tree key grid: 0 isotropic, 1 per-axis, 2 auto
     unsigned warp_chunks = 4;    // warp tiles: records per warp unit / 32
 };
 static SortedOpts& opts() {
@@ -1560,6 +1561,7 @@ static SortedOpts& opts() {
         d.bin_tma = (int)num("RS_BIN_TMA", d.bin_tma);
         d.tile_wide = (int)num("RS_TILE_WIDE", d.tile_wide);
         d.auto_tile = (int)num("RS_AUTO_TILE", d.auto_tile);
+        d.fast_keys = (int)num("RS_FAST_KEYS", d.fast_keys);
         d.bin_rank = (int)num("RS_BIN_RANK", d.bin_rank);
         d.rec_ids = (int)num("RS_REC_IDS", d.rec_ids);
         d.warp_chunks = (unsigned)num("RS_WARP_CHUNKS", d.warp_chunks);
@@ -1580,6 +1582,7 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "tile_wide")) { prev = o.tile_wide; if (value >= 0) o.tile_wide = (int)value; }
     else if (!strcmp(name, "rec_ids")) { prev = o.rec_ids; if (value >= 0) o.rec_ids = (int)value; }
     else if (!strcmp(name, "bin_rank")) { prev = o.bin_rank; if (value >= 0) o.bin_rank = (int)value; }
+    else if (!strcmp(name, "fast_keys")) { prev = o.fast_keys; if (value >= 0 && value <= 2) o.fast_keys = (int)value; }
     else if (!strcmp(name, "auto_tile")) { prev = o.auto_tile; if (value == 3 || value == 4) o.auto_tile = (int)value; }
     else if (!strcmp(name, "warp_chunks")) { prev = o.warp_chunks; if (value > 0) o.warp_chunks = (unsigned)value; }
     else return -1;
@@ -1588,6 +1591,7 @@ int sorted_option(const char* name, long long value, long long* old) {
 }
 
 static int trav_variant() { return opts().trav; }
+int fast_key_mode() { return opts().fast_keys; }
 static unsigned tile_min_density() { return opts().tile_density; }
 static unsigned tile_balance() { return opts().tile_balance; }
 static unsigned bin_occupancy() { return opts().bin_occ; }
