@@ -1352,7 +1352,9 @@ struct WTileSmem {
     WarpTile w[kTileThreads / 32];
 };
 
-template <int MODE>
+// (K: one instantiation per calling kernel; ptxas 12.9 crashes on a
+// __noinline__ function shared by several kernels)
+template <int MODE, int K>
 __device__ __noinline__ void wtile_fallback(const SortedArgs& a, const RsSlot* nodes, int root,
                                             float4 r0, float4 r1, int& det, int& nh, int& btri,
                                             double& bt) {
@@ -1360,6 +1362,212 @@ __device__ __noinline__ void wtile_fallback(const SortedArgs& a, const RsSlot* n
     trav_one<MODE>(nodes, a.leaves, a.n_int, root, r0, r1, det, nh, btri, bt, ovf);
     if (ovf) atomicAdd(&a.status->internal, 1ull);
 }
+
+// One warp: union box of records [beg, end), then a breadth-first walk from
+// the CTA's cut (ballot-compacted levels, warp-level synchronisation only)
+// collecting every leaf that overlaps it into (lxy, lz, lid).  Returns the
+// leaf count; ovf is set when the list or a level exceeds its capacity.
+template <class CUT>
+__device__ __forceinline__ int warp_walk(const SortedArgs& a, const CUT& cut, int ncut,
+                                         const RsSlot* nodes, unsigned beg, unsigned end,
+                                         float4* lxy, float2* lz, int* lid, int lcap,
+                                         int (*front)[kWtFCap], int fcap, bool& ovf) {
+    const int n_int = a.n_int;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    float u[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
+    for (unsigned idx = beg + lane; idx < end; idx += 32) {
+        float4 r0, r1;
+        get_rec(a, idx, r0, r1);
+        u[0] = fminf(u[0], fminf(r0.x, r1.x)); u[1] = fmaxf(u[1], fmaxf(r0.x, r1.x));
+        u[2] = fminf(u[2], fminf(r0.y, r1.y)); u[3] = fmaxf(u[3], fmaxf(r0.y, r1.y));
+        u[4] = fminf(u[4], fminf(r0.z, r1.z)); u[5] = fmaxf(u[5], fmaxf(r0.z, r1.z));
+    }
+#pragma unroll
+    for (int k = 0; k < 6; k += 2) {
+        u[k] = wred_min(u[k]);
+        u[k + 1] = wred_max(u[k + 1]);
+    }
+    int nl = 0, nf = 0;
+    for (int i0 = 0; i0 < ncut; i0 += 32) {
+        const int i = i0 + lane;
+        const int ref = i < ncut ? cut.cref[i] : -1;
+        const bool hit = i < ncut && box_ov(u, cut.cxy[i], cut.cz[i]);
+        const bool leaf = ref >= n_int;
+        const unsigned ml = __ballot_sync(kFullMask, hit && leaf);
+        const unsigned mi = __ballot_sync(kFullMask, hit && !leaf);
+        if (hit && leaf) {
+            const int k = nl + __popc(ml & lt);
+            if (k < lcap) {
+                lxy[k] = cut.cxy[i];
+                lz[k] = cut.cz[i];
+                lid[k] = ref - n_int;
+            }
+        }
+        if (hit && !leaf) {
+            const int k = nf + __popc(mi & lt);
+            if (k < fcap) front[0][k] = ref;
+        }
+        nl += __popc(ml);
+        nf += __popc(mi);
+    }
+    ovf = nl > lcap || nf > fcap;
+    int cur = 0;
+    while (nf > 0 && !ovf) {
+        __syncwarp();
+        int nn = 0;
+        for (int i0 = 0; i0 < nf; i0 += 32) {
+            const int i = i0 + lane;
+            bool oa = false, ob = false;
+            int ca = -1, cb = -1;
+            float f0[8], f1[8];
+            if (i < nf) {
+                const int node = front[cur][i];
+                ld_slot(nodes + 2 * node, f0);
+                ld_slot(nodes + 2 * node + 1, f1);
+                ca = __float_as_int(f1[4]);
+                cb = __float_as_int(f1[5]);
+                oa = (u[0] <= f0[1]) & (u[1] >= f0[0]) & (u[2] <= f0[3]) & (u[3] >= f0[2]) &
+                     (u[4] <= f0[5]) & (u[5] >= f0[4]);
+                ob = (u[0] <= f0[7]) & (u[1] >= f0[6]) & (u[2] <= f1[1]) & (u[3] >= f1[0]) &
+                     (u[4] <= f1[3]) & (u[5] >= f1[2]);
+            }
+            const bool la = oa && ca >= n_int, ia = oa && ca < n_int;
+            const bool lb = ob && cb >= n_int, ib = ob && cb < n_int;
+            const unsigned mla = __ballot_sync(kFullMask, la), mlb = __ballot_sync(kFullMask, lb);
+            const unsigned mia = __ballot_sync(kFullMask, ia), mib = __ballot_sync(kFullMask, ib);
+            if (la) {
+                const int k = nl + __popc(mla & lt);
+                if (k < lcap) {
+                    lxy[k] = make_float4(f0[0], f0[1], f0[2], f0[3]);
+                    lz[k] = make_float2(f0[4], f0[5]);
+                    lid[k] = ca - n_int;
+                }
+            }
+            if (lb) {
+                const int k = nl + __popc(mla) + __popc(mlb & lt);
+                if (k < lcap) {
+                    lxy[k] = make_float4(f0[6], f0[7], f1[0], f1[1]);
+                    lz[k] = make_float2(f1[2], f1[3]);
+                    lid[k] = cb - n_int;
+                }
+            }
+            if (ia) {
+                const int k = nn + __popc(mia & lt);
+                if (k < fcap) front[cur ^ 1][k] = ca;
+            }
+            if (ib) {
+                const int k = nn + __popc(mia) + __popc(mib & lt);
+                if (k < fcap) front[cur ^ 1][k] = cb;
+            }
+            nl += __popc(mla) + __popc(mlb);
+            nn += __popc(mia) + __popc(mib);
+        }
+        nf = nn;
+        cur ^= 1;
+        ovf = nl > lcap || nf > fcap;
+    }
+    __syncwarp();
+    return nl;
+}
+
+// ---- pipelined tiles -------------------------------------------------------
+//
+// The CTA-tile scheme with the walk taken off the critical path: warp 0
+// walks the tree for the NEXT tile (warp_walk into the other half of a
+// double-buffered candidate list) while every warp, warp 0 included once its
+// walk is done, claims 32-record chunks of the current tile.  One CTA barrier
+// per tile instead of one per walk level.
+constexpr int kPtLCap = 192;
+
+struct PTileSmem {
+    float4 cxy[kCutCap];
+    float2 cz[kCutCap];
+    int cref[kCutCap];
+    int ncut;
+    float4 lxy[2][kPtLCap];
+    float2 lz[2][kPtLCap];
+    int lid[2][kPtLCap];
+    int front[2][kWtFCap];
+    WarpCand wc[kTileThreads / 32];
+    unsigned char slot[kTileThreads / 32][kWCap][32];
+    int nl[2];
+    int ovf[2];
+    unsigned tile[2];
+    unsigned chunk[2];
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_ptile(SortedArgs a) {
+    __shared__ PTileSmem sm;
+    const unsigned n_live = *a.n_live;
+    const int n_int = a.n_int;
+    const int root = __ldg(&a.hdr->root);
+    const RsSlot* const nodes = reinterpret_cast<const RsSlot*>(a.nodes);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned T = (unsigned)((unsigned long long)a.tile_area * n_live / (unsigned)(n_int + 1));
+    const unsigned per = a.tile_balance * gridDim.x;
+    const unsigned bal = (n_live + per - 1) / per;
+    T = T < bal ? T : bal;
+    T = (T + 31) / 32 * 32;
+    T = T < 64 ? 64 : (T > 16384 ? 16384 : T);
+    const unsigned n_tiles = (n_live + T - 1) / T;
+    unsigned* ctr = reinterpret_cast<unsigned*>(&a.status->tile_counter);
+    build_cut(sm, nodes, n_int, root);
+    __syncthreads();
+    const int ncut = sm.ncut;
+    auto produce = [&](int buf) {  // warp 0
+        unsigned tl = 0;
+        if (lane == 0) tl = atomicAdd(ctr, 1u);
+        tl = __shfl_sync(kFullMask, tl, 0);
+        int nl = 0;
+        bool ovf = false;
+        if (tl < n_tiles) {
+            const unsigned beg = tl * T, end = beg + T < n_live ? beg + T : n_live;
+            nl = warp_walk(a, sm, ncut, nodes, beg, end, sm.lxy[buf], sm.lz[buf], sm.lid[buf],
+                           kPtLCap, sm.front, kWtFCap, ovf);
+        }
+        if (lane == 0) {
+            sm.tile[buf] = tl;
+            sm.chunk[buf] = 0;
+            sm.nl[buf] = nl;
+            sm.ovf[buf] = ovf;
+        }
+    };
+    if (warp == 0) produce(0);
+    __syncthreads();
+    for (int k = 0;; ++k) {
+        const int cur = k & 1;
+        const unsigned tile = sm.tile[cur];
+        if (tile >= n_tiles) break;
+        const bool fallback = sm.ovf[cur] != 0;
+        const int nl = sm.nl[cur];
+        if (warp == 0) produce(cur ^ 1);
+        const unsigned beg = tile * T, end = beg + T < n_live ? beg + T : n_live;
+        const unsigned nchunks = (end - beg + 31) / 32;
+        for (;;) {
+            unsigned c = 0;
+            if (lane == 0) c = atomicAdd(&sm.chunk[cur], 1u);
+            c = __shfl_sync(kFullMask, c, 0);
+            if (c >= nchunks) break;
+            const unsigned idx = beg + 32 * c + lane;
+            const bool valid = idx < end;
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+            if (valid) get_rec(a, idx, r0, r1);
+            int det = 0, nh = 0, btri = -1;
+            double bt = 0.0;
+            if (fallback) {
+                if (valid) wtile_fallback<MODE, 1>(a, nodes, root, r0, r1, det, nh, btri, bt);
+            } else {
+                process_chunk<MODE>(a, r0, r1, valid, sm.lxy[cur], sm.lz[cur], sm.lid[cur], nl,
+                                    sm.wc[warp], sm.slot[warp], det, nh, btri, bt);
+            }
+            if (valid) write_result<MODE>(a, __float_as_int(r0.w), det, nh, btri, bt);
+        }
+        __syncthreads();  // tile done, next tile's list ready
+    }
+}
+
 
 template <int MODE>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_wtile(SortedArgs a) {
@@ -1384,100 +1592,9 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_wtile(Sor
         if (unit >= n_units) break;
         const unsigned beg = unit * U;
         const unsigned end = beg + U < n_live ? beg + U : n_live;
-        // union box of the unit's records
-        float u[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
-        for (unsigned idx = beg + lane; idx < end; idx += 32) {
-            float4 r0, r1;
-        get_rec(a, idx, r0, r1);
-            u[0] = fminf(u[0], fminf(r0.x, r1.x)); u[1] = fmaxf(u[1], fmaxf(r0.x, r1.x));
-            u[2] = fminf(u[2], fminf(r0.y, r1.y)); u[3] = fmaxf(u[3], fmaxf(r0.y, r1.y));
-            u[4] = fminf(u[4], fminf(r0.z, r1.z)); u[5] = fmaxf(u[5], fmaxf(r0.z, r1.z));
-        }
-#pragma unroll
-        for (int k = 0; k < 6; k += 2) {
-            u[k] = wred_min(u[k]);
-            u[k + 1] = wred_max(u[k + 1]);
-        }
-        // walk: the cut, then level by level (ballot-compacted lists)
-        int nl = 0, nf = 0;
-        for (int i0 = 0; i0 < ncut; i0 += 32) {
-            const int i = i0 + lane;
-            const int ref = i < ncut ? sm.cref[i] : -1;
-            const bool hit = i < ncut && box_ov(u, sm.cxy[i], sm.cz[i]);
-            const bool leaf = ref >= n_int;
-            const unsigned ml = __ballot_sync(kFullMask, hit && leaf);
-            const unsigned mi = __ballot_sync(kFullMask, hit && !leaf);
-            if (hit && leaf) {
-                const int k = nl + __popc(ml & lt);
-                if (k < kWtLCap) {
-                    wt.lxy[k] = sm.cxy[i];
-                    wt.lz[k] = sm.cz[i];
-                    wt.lid[k] = ref - n_int;
-                }
-            }
-            if (hit && !leaf) {
-                const int k = nf + __popc(mi & lt);
-                if (k < kWtFCap) wt.front[0][k] = ref;
-            }
-            nl += __popc(ml);
-            nf += __popc(mi);
-        }
-        bool ovf = nl > kWtLCap || nf > kWtFCap;
-        int cur = 0;
-        while (nf > 0 && !ovf) {
-            __syncwarp();
-            int nn = 0;
-            for (int i0 = 0; i0 < nf; i0 += 32) {
-                const int i = i0 + lane;
-                bool oa = false, ob = false;
-                int ca = -1, cb = -1;
-                float f0[8], f1[8];
-                if (i < nf) {
-                    const int node = wt.front[cur][i];
-                    ld_slot(nodes + 2 * node, f0);
-                    ld_slot(nodes + 2 * node + 1, f1);
-                    ca = __float_as_int(f1[4]);
-                    cb = __float_as_int(f1[5]);
-                    oa = (u[0] <= f0[1]) & (u[1] >= f0[0]) & (u[2] <= f0[3]) & (u[3] >= f0[2]) &
-                         (u[4] <= f0[5]) & (u[5] >= f0[4]);
-                    ob = (u[0] <= f0[7]) & (u[1] >= f0[6]) & (u[2] <= f1[1]) & (u[3] >= f1[0]) &
-                         (u[4] <= f1[3]) & (u[5] >= f1[2]);
-                }
-                const bool la = oa && ca >= n_int, ia = oa && ca < n_int;
-                const bool lb = ob && cb >= n_int, ib = ob && cb < n_int;
-                const unsigned mla = __ballot_sync(kFullMask, la), mlb = __ballot_sync(kFullMask, lb);
-                const unsigned mia = __ballot_sync(kFullMask, ia), mib = __ballot_sync(kFullMask, ib);
-                if (la) {
-                    const int k = nl + __popc(mla & lt);
-                    if (k < kWtLCap) {
-                        wt.lxy[k] = make_float4(f0[0], f0[1], f0[2], f0[3]);
-                        wt.lz[k] = make_float2(f0[4], f0[5]);
-                        wt.lid[k] = ca - n_int;
-                    }
-                }
-                if (lb) {
-                    const int k = nl + __popc(mla) + __popc(mlb & lt);
-                    if (k < kWtLCap) {
-                        wt.lxy[k] = make_float4(f0[6], f0[7], f1[0], f1[1]);
-                        wt.lz[k] = make_float2(f1[2], f1[3]);
-                        wt.lid[k] = cb - n_int;
-                    }
-                }
-                if (ia) {
-                    const int k = nn + __popc(mia & lt);
-                    if (k < kWtFCap) wt.front[cur ^ 1][k] = ca;
-                }
-                if (ib) {
-                    const int k = nn + __popc(mia) + __popc(mib & lt);
-                    if (k < kWtFCap) wt.front[cur ^ 1][k] = cb;
-                }
-                nl += __popc(mla) + __popc(mlb);
-                nn += __popc(mia) + __popc(mib);
-            }
-            nf = nn;
-            cur ^= 1;
-            ovf = nl > kWtLCap || nf > kWtFCap;
-        }
+        bool ovf;
+        const int nl = warp_walk(a, sm, ncut, nodes, beg, end, wt.lxy, wt.lz, wt.lid, kWtLCap,
+                                 wt.front, kWtFCap, ovf);
         __syncwarp();
 #ifdef RS_TILE_STATS
         if (lane == 0) {
@@ -1493,7 +1610,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_wtile(Sor
             int det = 0, nh = 0, btri = -1;
             double bt = 0.0;
             if (ovf) {
-                if (valid) wtile_fallback<MODE>(a, nodes, root, r0, r1, det, nh, btri, bt);
+                if (valid) wtile_fallback<MODE, 0>(a, nodes, root, r0, r1, det, nh, btri, bt);
             } else {
                 process_chunk<MODE>(a, r0, r1, valid, wt.lxy, wt.lz, wt.lid, nl, wt.wc, wt.slot, det,
                                     nh, btri, bt);
@@ -1583,7 +1700,7 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "rec_ids")) { prev = o.rec_ids; if (value >= 0) o.rec_ids = (int)value; }
     else if (!strcmp(name, "bin_rank")) { prev = o.bin_rank; if (value >= 0) o.bin_rank = (int)value; }
     else if (!strcmp(name, "fast_keys")) { prev = o.fast_keys; if (value >= 0 && value <= 2) o.fast_keys = (int)value; }
-    else if (!strcmp(name, "auto_tile")) { prev = o.auto_tile; if (value == 3 || value == 4) o.auto_tile = (int)value; }
+    else if (!strcmp(name, "auto_tile")) { prev = o.auto_tile; if (value >= 3 && value <= 5) o.auto_tile = (int)value; }
     else if (!strcmp(name, "warp_chunks")) { prev = o.warp_chunks; if (value > 0) o.warp_chunks = (unsigned)value; }
     else return -1;
     if (old) *old = prev;
@@ -1658,6 +1775,16 @@ static void launch_tile(const SortedArgs& a, int sms, cudaStream_t s) {
 }
 
 template <int MODE>
+static void launch_ptile(const SortedArgs& a, int sms, cudaStream_t s) {
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trav_ptile<MODE>, kTileThreads, 0);
+        if (occ < 1) occ = 1;
+    }
+    k_trav_ptile<MODE><<<sms * occ, kTileThreads, 0, s>>>(a);
+}
+
+template <int MODE>
 static void launch_wtile(const SortedArgs& a, int sms, cudaStream_t s) {
     static int occ = 0;
     if (!occ) {
@@ -1687,8 +1814,15 @@ void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t
         variant = a.n_r < (long long)a.tile_min_density * (a.n_int + 1) ? 1 : opts().auto_tile;
     if (a.n_int == 0) variant = 1;
     hot_kernel_mark(0, s);
-    g_hot_name = variant == 4 ? "k_trav_wtile" : variant == 3 ? "k_trav_tile"
+    g_hot_name = variant == 5 ? "k_trav_ptile" : variant == 4 ? "k_trav_wtile" : variant == 3 ? "k_trav_tile"
                  : variant == 1 ? "k_trav_sorted_bin" : "k_trav_sorted";
+    if (variant == 5 && !stats) {
+        if (mode == kBoolean) launch_ptile<kBoolean>(a, sms, s);
+        else if (mode == kCount) launch_ptile<kCount>(a, sms, s);
+        else launch_ptile<kBarycentric>(a, sms, s);
+        hot_kernel_mark(1, s);
+        return;
+    }
     if (variant == 4 && !stats) {
         if (mode == kBoolean) launch_wtile<kBoolean>(a, sms, s);
         else if (mode == kCount) launch_wtile<kCount>(a, sms, s);

@@ -150,7 +150,7 @@ def test_layered(cap, mode):
 # shared candidate lists, the per-thread binary and 4-wide walks.  Results
 # must not depend on the variant, the tile size, the spatial-bin resolution
 # or the tile fallback (candidate-list overflow -> per-record walk).
-TRAV = {"tile": 3, "warptile": 4, "binary": 1, "wide": 2}
+TRAV = {"tile": 3, "warptile": 4, "ptile": 5, "binary": 1, "wide": 2}
 
 
 @pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
@@ -180,7 +180,9 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"tile_wide": 1},                               # tile walk over 4-wide nodes
     {"trav": 4, "warp_chunks": 1},                  # warp tiles of one chunk
     {"trav": 4, "warp_chunks": 64},                 # warp tiles overflowing their lists
-], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64"])
+    {"trav": 5, "tile_balance": 1, "tile_area": 1 << 20},  # pipelined tiles, overflowing
+    {"trav": 5, "tile_balance": 64},                # pipelined tiles, small
+], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
 def test_tile_knobs_bitwise(name, mode, knobs):
@@ -226,7 +228,7 @@ def test_tile_random_soup_vs_oracle(seed, n_tri, n_seg, mode):
     V, T, s, _ = _random_soup(seed, n_tri, n_seg)
     e = s + np.random.default_rng(seed + 100).uniform(-1.5, 1.5, size=s.shape).astype(np.float32)
     want = O.run_batch(V, T, s, e, mode=mode, max_stack=10**6)
-    for variant in ("tile", "warptile", "binary"):
+    for variant in ("tile", "warptile", "ptile", "binary"):
         with _lib.option("trav", TRAV[variant]):
             got = rs.run_batch(rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e),
                                rs.EngineConfig(mode=mode, tree="fast"))
@@ -480,7 +482,7 @@ def _adversarial(kind: str, seed: int):
     return V, T, s.astype(np.float32), e.astype(np.float32)
 
 
-@pytest.mark.parametrize("variant", ["auto", "tile", "warptile", "binary", "reference"])
+@pytest.mark.parametrize("variant", ["auto", "tile", "warptile", "ptile", "binary", "reference"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("kind", ["lattice", "inplane", "degenerate", "scale"])
 def test_adversarial_vs_oracle(kind, mode, variant):
