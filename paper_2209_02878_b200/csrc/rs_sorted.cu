@@ -514,8 +514,14 @@ __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
 // each CTA keeps two 1024-segment stages in shared memory, filled by the TMA
 // engine (cp.async.bulk global->shared, completion on an mbarrier) one chunk
 // ahead of the compute, so the DRAM stream never waits for the key math.
-constexpr int kStreamSegs = 1024;
-constexpr int kStreamThreads = 256;
+#ifndef RS_STREAM_THREADS
+#define RS_STREAM_THREADS 256
+#endif
+#ifndef RS_STREAM_CTAS
+#define RS_STREAM_CTAS 4
+#endif
+constexpr int kStreamThreads = RS_STREAM_THREADS;
+constexpr int kStreamSegs = 4 * kStreamThreads;  // four segments per thread per stage
 constexpr unsigned kStreamStageBytes = 2u * kStreamSegs * 12u;  // starts + ends
 constexpr size_t kStreamSmem = 2 * kStreamStageBytes + 64;
 
@@ -1732,7 +1738,7 @@ void launch_binning(const SortedArgs& a0, cudaStream_t s) {
             attr = true;
         }
         const long long chunks = a.n_r / kStreamSegs;
-        const unsigned g = (unsigned)(chunks < sms * 4ll ? chunks : sms * 4ll);
+        const unsigned g = (unsigned)(chunks < sms * (long long)RS_STREAM_CTAS ? chunks : sms * (long long)RS_STREAM_CTAS);
         const bool rank = opts().bin_rank;
         if (rank) k_bin_count_tma<true><<<g, kStreamThreads, kStreamSmem, s>>>(a);
         else k_bin_count_tma<false><<<g, kStreamThreads, kStreamSmem, s>>>(a);
