@@ -9,6 +9,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <set>
 #include <vector>
 #include <mutex>
 #include <string>
@@ -914,6 +915,7 @@ static thread_local RsStatus g_last_status{};
 static std::atomic<int> g_opt_gen{0};  // bumped by rs_set_option: captured graphs bake the options in
 static std::mutex g_graph_mu;
 static std::map<GraphKey, GraphEntry> g_graphs;
+static std::set<GraphKey> g_seen;  // argument sets called once (captured on the next call)
 static unsigned long long g_graph_clock = 0;
 static const bool g_use_graphs = [] {
     const char* e = getenv("RS_NO_GRAPH");
@@ -951,12 +953,24 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         key.timing = g_timing;
         key.opt_gen = g_opt_gen.load();
         GraphEntry* ge = nullptr;
+        bool capture = true;
         {
             std::lock_guard<std::mutex> lk(g_graph_mu);
             auto it = g_graphs.find(key);
-            if (it != g_graphs.end()) ge = &it->second;
+            if (it != g_graphs.end()) {
+                ge = &it->second;
+            } else {
+                // capture only on an argument set's second call: a one-off
+                // call (fresh buffers every time) runs the direct launches
+                // instead of paying for capture + instantiation
+                capture = g_seen.count(key) != 0;
+                if (!capture) {
+                    if (g_seen.size() >= 64) g_seen.clear();
+                    g_seen.insert(key);
+                }
+            }
         }
-        if (!ge) {
+        if (!ge && capture) {
             GraphEntry e;
             CK(cudaHostAlloc(reinterpret_cast<void**>(&e.h_status), sizeof(RsStatus), cudaHostAllocDefault));
             // capture on a private stream (the caller's may be the legacy
