@@ -25,7 +25,7 @@ def _oracle_local(mesh, segs, cfg):
     return rs.ResultSet(cfg.mode, segs.count, **{k: v for k, v in d.items() if k != "mode"})
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, q, gpu=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -35,7 +35,8 @@ def _worker(rank, world, port, name, q):
         segs = rs.SegmentBatch.from_arrays(fx["starts"], fx["ends"])
         out = {}
         for mode in MODES:
-            r = run_batch_sharded(mesh, segs, rs.EngineConfig(mode=mode), local_run=_oracle_local)
+            r = run_batch_sharded(mesh, segs, rs.EngineConfig(mode=mode),
+                                  local_run=None if gpu else _oracle_local)
             out[mode] = {f: np.asarray(getattr(r, f)) for f in
                          ("crossing", "counts", "ray_index", "distance", "triangle_id", "point")
                          if getattr(r, f) is not None}
@@ -58,19 +59,36 @@ def test_shard_ranges_partition():
             assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
 
 
-@pytest.mark.parametrize("name", ["scene_s19", "soup_17"])
-def test_two_rank_gloo_matches_reference(name):
+def _run_two_ranks(name, gpu):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q, gpu)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("name", ["scene_s19", "soup_17"])
+def test_two_rank_gloo_matches_reference(name):
+    res = _run_two_ranks(name, gpu=False)
     fx = load(name)
     for rank in (0, 1):
         for mode in MODES:
             assert_result_fields(res[rank][mode], expected(fx, "batch", mode), f"rank {rank} {mode}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["scene_c1", "soup_20"])
+def test_two_rank_sharded_gpu_matches_reference(name):
+    """Both ranks run the real CUDA run_batch on their shard (sharing one
+    GPU here), gather over gloo, and every rank holds the reference result."""
+    res = _run_two_ranks(name, gpu=True)
+    fx = load(name)
+    for rank in (0, 1):
+        for mode in MODES:
+            assert_result_fields(res[rank][mode], expected(fx, "batch", mode), f"gpu rank {rank} {mode}")
