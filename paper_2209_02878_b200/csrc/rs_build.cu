@@ -37,8 +37,10 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
                                               int lean) {
     __shared__ double red[8][6];
     __shared__ float fred[8][6];
+    __shared__ float sred[8][3];
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     float blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    float tsz[3] = {0.f, 0.f, 0.f};
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         // _reset_tree (lbvh.py:181-189) for internal slot j; a lean build
         // (query-only tree, never downloaded) keeps just the visit counters
@@ -57,8 +59,10 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const float fa = V[3ll * ia + k], fb = V[3ll * ib + k], fc = V[3ll * ic + k];
-            blo[k] = fminf(blo[k], fminf(fminf(fa, fb), fc));  // root box = union of triangle boxes
-            bhi[k] = fmaxf(bhi[k], fmaxf(fmaxf(fa, fb), fc));
+            const float tl = fminf(fminf(fa, fb), fc), th = fmaxf(fmaxf(fa, fb), fc);
+            blo[k] = fminf(blo[k], tl);  // root box = union of triangle boxes
+            bhi[k] = fmaxf(bhi[k], th);
+            tsz[k] = fmaxf(tsz[k], th - tl);
             if (do_centroids) {
                 const double m = __ddiv_rn(__dadd_rn(__dadd_rn((double)fa, (double)fb), (double)fc), 3.0);
                 cent[3ll * j + k] = m;
@@ -75,6 +79,7 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
         for (int o = 16; o; o >>= 1) {
             blo[k] = fminf(blo[k], __shfl_xor_sync(0xffffffffu, blo[k], o));
             bhi[k] = fmaxf(bhi[k], __shfl_xor_sync(0xffffffffu, bhi[k], o));
+            tsz[k] = fmaxf(tsz[k], __shfl_xor_sync(0xffffffffu, tsz[k], o));
         }
     }
     if (l == 0)
@@ -83,8 +88,14 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
             red[w][3 + k] = hi[k];
             fred[w][k] = blo[k];
             fred[w][3 + k] = bhi[k];
+            sred[w][k] = tsz[k];
         }
     __syncthreads();
+    if (threadIdx.x < 3) {
+        float v = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) v = fmaxf(v, sred[i][threadIdx.x]);
+        if (v > 0.f) atomicMax(&hdr->tsize[threadIdx.x], __float_as_uint(v));
+    }
     if (threadIdx.x < 6) {
         const int k = threadIdx.x;
         double v = red[0][k];
@@ -109,22 +120,6 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
 }
 
 // ------------------------------------------------------------------ keys ---
-
-__device__ __forceinline__ unsigned long long split21(unsigned long long v) {
-    v &= 0x1FFFFFull;
-    v = (v | v << 32) & 0x1F00000000FFFFull;
-    v = (v | v << 16) & 0x1F0000FF0000FFull;
-    v = (v | v << 8) & 0x100F00F00F00F00Full;
-    v = (v | v << 4) & 0x10C30C30C30C30C3ull;
-    v = (v | v << 2) & 0x1249249249249249ull;
-    return v;
-}
-
-__device__ __forceinline__ unsigned quant1(double p, double lo, double ext, double gmax) {
-    double s = floor(__dmul_rn(__ddiv_rn(__dsub_rn(p, lo), ext), gmax));
-    s = s < 0.0 ? 0.0 : (s > gmax ? gmax : s);  // np.clip (morton.py:62)
-    return (unsigned)s;
-}
 
 __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ cent, int n,
                                               const RsHeader* __restrict__ hdr, int kind,
@@ -651,7 +646,8 @@ __global__ void __launch_bounds__(256) k_climb_lean(const float* __restrict__ V,
                                                     const int* __restrict__ T, int n,
                                                     const unsigned long long* __restrict__ codes,
                                                     const int* __restrict__ ids, int* visit,
-                                                    RsNode* nodes, RsLeaf* leaves, RsHeader* hdr) {
+                                                    RsNode* nodes, RsLeaf* leaves, RsHeader* hdr,
+                                                    float* leaf_boxes) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int n_int = n - 1;
@@ -675,6 +671,10 @@ __global__ void __launch_bounds__(256) k_climb_lean(const float* __restrict__ V,
     lf.p1 = make_float4(b[1], b[2], c[0], c[1]);
     lf.p2 = make_float4(c[2], __int_as_float(tid), 0.f, 0.f);
     leaves[i] = lf;
+    float2* lb = reinterpret_cast<float2*>(leaf_boxes + 6ll * i);  // for the Morton-range lists
+    lb[0] = make_float2(box[0], box[1]);
+    lb[1] = make_float2(box[2], box[3]);
+    lb[2] = make_float2(box[4], box[5]);
     if (n == 1) {
         hdr->root = n_int;
         return;
@@ -723,9 +723,23 @@ __global__ void __launch_bounds__(256) k_climb_lean(const float* __restrict__ V,
 
 void launch_climb_lean(const float* V, const int* T, int n, const unsigned long long* codes,
                        const int* ids, int* visit, RsNode* nodes, RsLeaf* leaves, RsHeader* hdr,
-                       cudaStream_t s) {
+                       float* leaf_boxes, cudaStream_t s) {
     count_launches(1);
-    k_climb_lean<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(V, T, n, codes, ids, visit, nodes, leaves, hdr);
+    k_climb_lean<<<grid_for(n, 256, 1 << 30), 256, 0, s>>>(V, T, n, codes, ids, visit, nodes, leaves,
+                                                           hdr, leaf_boxes);
+}
+
+// Every stride-th sorted key (the first level of the traversal's key search).
+__global__ void k_code_samples(const unsigned long long* __restrict__ codes, int n, int stride,
+                               unsigned long long* samples, int m) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < m) samples[k] = codes[(long long)k * stride];
+}
+
+void launch_code_samples(const unsigned long long* codes, int n, int stride,
+                         unsigned long long* samples, int m, cudaStream_t s) {
+    count_launches(1);
+    k_code_samples<<<(m + 255) / 256, 256, 0, s>>>(codes, n, stride, samples, m);
 }
 
 }  // namespace rs

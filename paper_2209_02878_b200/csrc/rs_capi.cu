@@ -35,6 +35,12 @@ struct rs_tree {
     RsLeaf* leaves;
     RsNode4* nodes4;  // fast trees only
     TreeArrays ta;
+    // lean fast trees keep their sorted keys (+ a sample of every stride-th)
+    // for the traversal's Morton-range candidate lists; freed with the tree
+    char* scratch = nullptr;
+    const unsigned long long* codes = nullptr;
+    unsigned long long* code_samples = nullptr;
+    int sample_stride = 0, n_samples = 0, key_mode = 0;
 };
 
 namespace {
@@ -227,8 +233,9 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
     } else {
         const int passes = kind == kTreeFast ? 4 : 8;  // 30-bit vs 63-bit keys
         const size_t sb = sort_scratch_bytes(n, passes);
+        constexpr int kMaxSamples = 1024;
         const size_t bytes = align256(24ull * n) + 2 * align256(8ull * n) + 2 * align256(4ull * n) +
-                             align256(sb);
+                             align256(sb) + align256(8ull * kMaxSamples);
         char* scratch = nullptr;
         CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s));
         Carver c{scratch};
@@ -238,6 +245,7 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
         int* vals = c.take<int>(n);
         int* vals2 = c.take<int>(n);
         void* sort_scratch = c.take<char>(sb);
+        unsigned long long* samples = c.take<unsigned long long>(kMaxSamples);
         // lean: a fast tree only this call queries (never downloaded, no
         // 4-wide collapse): records only
         lean = lean && kind == kTreeFast && !need_nodes4() && g_lean_build;
@@ -248,10 +256,21 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
         }
         launch_keys(cent, n, t->hdr, kind, keys, vals, s);
         launch_sort(keys, vals, keys2, vals2, n, passes, sort_scratch, s);
-        if (lean) launch_climb_lean(V, T, n, keys, vals, t->ta.visit, t->nodes, t->leaves, t->hdr, s);
+        if (lean) launch_climb_lean(V, T, n, keys, vals, t->ta.visit, t->nodes, t->leaves, t->hdr,
+                                    t->ta.leaf_bounds, s);
         else launch_climb(V, T, n, keys, vals, t->ta, t->nodes, t->leaves, t->hdr, s);
         if (kind == kTreeFast && need_nodes4()) launch_collapse(n, t->ta, t->nodes, t->nodes4, t->hdr, s);
-        CK(cudaFreeAsync(scratch, s));
+        if (lean) {  // sorted keys stay with the tree (4 passes: the result is in `keys`)
+            t->sample_stride = (n + kMaxSamples - 1) / kMaxSamples;
+            t->n_samples = (n + t->sample_stride - 1) / t->sample_stride;
+            launch_code_samples(keys, n, t->sample_stride, samples, t->n_samples, s);
+            t->scratch = scratch;
+            t->codes = keys;
+            t->code_samples = samples;
+            t->key_mode = fast_key_mode() == 1 ? 1 : 0;
+        } else {
+            CK(cudaFreeAsync(scratch, s));
+        }
     }
     CK(cudaGetLastError());
     *out = t;
@@ -384,6 +403,7 @@ int rs_tree_download(const rs_tree* t, float* ib, int32_t* cl, int32_t* cr, int3
 
 int rs_free(rs_tree* t, void* stream) {
     if (!t) return RS_OK;
+    if (t->scratch) cudaFreeAsync(t->scratch, S(stream));
     cudaError_t e = cudaFreeAsync(t->block, S(stream));
     delete t;
     if (e != cudaSuccess) return fail(RS_CUDA_ERROR, "cudaFreeAsync: %s", cudaGetErrorString(e));
@@ -465,9 +485,16 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
 
 static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r,
                               const FastOut& o, FastScratch& f) {
-    return SortedArgs{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r,
+    SortedArgs a{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r,
                       f.bins, f.cursor, f.n_live, reinterpret_cast<float*>(f.n_live + 64), f.bins + sorted_bins(), f.rec, f.seg_key, o.flags,
                       f.best_t, f.best_tri, f.st};
+    a.codes = t->codes;
+    a.code_samples = t->code_samples;
+    a.sample_stride = t->sample_stride;
+    a.n_samples = t->n_samples;
+    a.leaf_boxes = t->ta.leaf_bounds;
+    a.key_mode = t->key_mode;
+    return a;
 }
 
 // Phase 1 of the sorted fast path: output presets + spatial binning.  Needs

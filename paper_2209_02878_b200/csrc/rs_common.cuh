@@ -58,6 +58,7 @@ struct RsHeader {
     int height;
     unsigned bmin[3];            // ~ordered32(min triangle-box coordinate) = root box
     unsigned bmax[3];            //  ordered32(max triangle-box coordinate)
+    unsigned tsize[3];           // largest triangle-box side per axis (f32 bits, >= 0)
 };
 
 // Per-query device status (zeroed before a query).
@@ -96,6 +97,23 @@ __device__ __forceinline__ unsigned ord32(float f) {
 }
 __device__ __forceinline__ float from_ord32(unsigned o) {
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+// ---- Morton keys (morton.py:48-63,117-128) -------------------------------
+__device__ __forceinline__ unsigned long long split21(unsigned long long v) {
+    v &= 0x1FFFFFull;
+    v = (v | v << 32) & 0x1F00000000FFFFull;
+    v = (v | v << 16) & 0x1F0000FF0000FFull;
+    v = (v | v << 8) & 0x100F00F00F00F00Full;
+    v = (v | v << 4) & 0x10C30C30C30C30C3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+
+__device__ __forceinline__ unsigned quant1(double p, double lo, double ext, double gmax) {
+    double s = floor(__dmul_rn(__ddiv_rn(__dsub_rn(p, lo), ext), gmax));
+    s = s < 0.0 ? 0.0 : (s > gmax ? gmax : s);  // np.clip (morton.py:62)
+    return (unsigned)s;
 }
 
 // ---- f32 box test: touching counts (geometry.py:69-79, _core.pyx:44-49) ---

@@ -35,7 +35,9 @@ void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hd
 // Query-only climb: RsNode/RsLeaf records and the root, no SoA fields.
 void launch_climb_lean(const float* V, const int* T, int n, const unsigned long long* codes,
                        const int* ids, int* visit, RsNode* nodes, RsLeaf* leaves, RsHeader* hdr,
-                       cudaStream_t s);
+                       float* leaf_boxes, cudaStream_t s);
+void launch_code_samples(const unsigned long long* codes, int n, int stride,
+                         unsigned long long* samples, int m, cudaStream_t s);
 void launch_keys(const double* cent, int n, const RsHeader* hdr, int kind,
                  unsigned long long* keys, int* vals, cudaStream_t s);
 size_t sort_scratch_bytes(int n, int passes);
@@ -166,6 +168,14 @@ struct SortedArgs {
     unsigned bin_occupancy;  // binning: target live segments per bin (set at launch)
     int rec_ids;             // rec holds 4-B segment ids instead of 32-B records (set at launch)
     unsigned tile_area;  // tile traversal: target triangles' worth of records per tile (set at launch)
+    // Morton-range candidate lists (fast lean trees; codes == nullptr disables)
+    const unsigned long long* codes;         // sorted 30-bit keys, leaf order
+    const unsigned long long* code_samples;  // codes[k * sample_stride]
+    int sample_stride;
+    int n_samples;
+    const float* leaf_boxes;                 // (n, 6) exact leaf boxes, leaf order
+    unsigned range_max;                      // scan at most this many leaves, else walk
+    int key_mode;                            // keys' grid: 0 isotropic, 1 per-axis
     unsigned tile_balance;      // tile traversal: at least this many tiles per CTA
     unsigned warp_chunks;       // warp tiles: 32-record chunks per warp unit
     unsigned tile_min_density;  // tile traversal only above this many records per triangle

@@ -1001,6 +1001,7 @@ struct TileSmem {
     int ovf;
     int ncut;
     unsigned tile;
+    int ri0, ri1;  // Morton-range candidate interval [ri0, ri1)
 };
 
 __device__ __forceinline__ float wred_min(float v) {
@@ -1177,6 +1178,65 @@ __device__ __forceinline__ void build_cut(SM& sm, const RsSlot* nodes, int n_int
     if (lane == 0) sm.ncut = n;
 }
 
+// ---- Morton-range candidate lists ------------------------------------------
+// Triangle t's centroid lies in its box, so a box overlapping U has its
+// centroid inside U grown by the largest triangle side per axis, S.  Morton
+// order is monotone in every coordinate, so every such centroid's key lies
+// in [key(U.lo - S), key(U.hi + S)]: a contiguous run of the sorted leaves.
+// Scanning that run (exact box test against U) yields exactly the walk's
+// candidate list when the run is short; long runs (boxes straddling a coarse
+// Morton boundary) fall back to the walk.
+__device__ __forceinline__ unsigned long long range_key(const SortedArgs& a, const double p[3]) {
+    double lo[3], ext[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = from_ord(~__ldg(&a.hdr->smin[k]));
+        ext[k] = __dsub_rn(from_ord(__ldg(&a.hdr->smax[k])), lo[k]);
+    }
+    if (a.key_mode == 0) {
+        const double e = fmax(fmax(ext[0], ext[1]), ext[2]);
+        ext[0] = ext[1] = ext[2] = e;
+    }
+    const double gmax = (double)((1u << kIsoBits) - 1u);
+    unsigned long long code = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const unsigned q = ext[k] > 0.0 ? quant1(p[k], lo[k], ext[k], gmax) : 0u;
+        code |= split21(q) << k;
+    }
+    return code;
+}
+
+// First index i with codes[i] > key (upper) or >= key (lower), by warp 0:
+// two rounds over the sample table, then the stride window.
+__device__ __forceinline__ int warp_bound(const SortedArgs& a, unsigned long long key, bool upper) {
+    const int lane = threadIdx.x & 31;
+    const int n = a.n_int + 1, m = a.n_samples, st = a.sample_stride;
+    auto before = [&](unsigned long long c) { return upper ? c <= key : c < key; };
+    // sample index of the last sample "before" key (-1 if none)
+    const int step = (m + 31) / 32;
+    int j = lane * step;
+    bool b = j < m && before(__ldg(a.code_samples + j));
+    unsigned mk = __ballot_sync(kFullMask, b);
+    int s0 = mk ? (31 - __clz(mk)) * step : -1;
+    if (s0 >= 0) {
+        j = s0 + lane;
+        b = lane < step && j < m && before(__ldg(a.code_samples + j));
+        mk = __ballot_sync(kFullMask, b);
+        s0 += 31 - __clz(mk);
+    }
+    // window of codes after sample s0 (codes[s0*st] is "before" key)
+    int base = s0 < 0 ? 0 : s0 * st;
+    const int lim = s0 < 0 ? 0 : ((s0 + 1) * st < n ? (s0 + 1) * st : n);
+    for (; base < lim; base += 32) {
+        j = base + lane;
+        b = j < lim && before(__ldg(a.codes + j));
+        mk = __ballot_sync(kFullMask, b);
+        if (mk != kFullMask) return base + __popc(mk);
+    }
+    return lim;
+}
+
 template <int MODE, bool WIDE>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(SortedArgs a) {
     __shared__ TileSmem sm;
@@ -1234,7 +1294,49 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
                 if (w == 0) { u[k] = sm.part[0][k]; u[k + 1] = sm.part[0][k + 1]; }
                 else { u[k] = fminf(u[k], sm.part[w][k]); u[k + 1] = fmaxf(u[k + 1], sm.part[w][k + 1]); }
             }
-        // 2. breadth-first walk with U, from the cut
+        // 2a. the Morton-range list when the run of candidate keys is short
+        bool ranged = false;
+        if (a.codes) {
+            if (warp == 0) {
+                double plo[3], phi[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double sz = (double)__uint_as_float(__ldg(&a.hdr->tsize[k]));
+                    const double l = (double)u[2 * k], h = (double)u[2 * k + 1];
+                    plo[k] = l - sz - 1e-9 * (fabs(l) + sz + 1.0);
+                    phi[k] = h + sz + 1e-9 * (fabs(h) + sz + 1.0);
+                }
+                const int i0 = warp_bound(a, range_key(a, plo), false);
+                const int i1 = warp_bound(a, range_key(a, phi), true);
+                if (lane == 0) {
+                    sm.ri0 = i0;
+                    sm.ri1 = i1;
+                }
+            }
+            __syncthreads();
+            const int i0 = sm.ri0, i1 = sm.ri1;
+            if (i1 - i0 <= (int)a.range_max) {
+                ranged = true;
+                for (int i = i0 + tid; i < i1; i += kTileThreads) {
+                    const float2* lb = reinterpret_cast<const float2*>(a.leaf_boxes + 6ll * i);
+                    const float2 x = __ldg(lb), y = __ldg(lb + 1), z = __ldg(lb + 2);
+                    const float4 xy = make_float4(x.x, x.y, y.x, y.y);
+                    if (box_ov(u, xy, z)) {
+                        const int k = atomicAdd(&sm.nl, 1);
+                        if (k < kTileLCap) {
+                            sm.lxy[k] = xy;
+                            sm.lz[k] = z;
+                            sm.lid[k] = i;
+                        } else {
+                            sm.ovf = 1;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // 2b. otherwise the breadth-first walk with U, from the cut
+        if (!ranged) {
         for (int ci = tid; ci < ncut; ci += kTileThreads) {
             const int ref = sm.cref[ci];
             if (box_ov(u, sm.cxy[ci], sm.cz[ci])) {
@@ -1299,6 +1401,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
                 }
             }
             __syncthreads();
+        }
         }
         const bool fallback = sm.ovf != 0;
         const int nl = sm.nl;
@@ -1664,6 +1767,7 @@ struct SortedOpts {
     int rec_ids = 0;             // scatter writes segment ids, not 32-B records (A/B: traversal gathers thrash L1)
     int auto_tile = 3;           // auto's dense variant: 3 CTA tiles, 4 warp tiles
     int fast_keys = 0;           // fast-tree key grid: 0 isotropic, 1 per-axis, 2 auto
+    unsigned range_max = 4096;   // tile lists from a Morton key range of at most this many leaves (0: walk only)
     unsigned warp_chunks = 4;    // warp tiles: records per warp unit / 32
 };
 static SortedOpts& opts() {
@@ -1685,6 +1789,7 @@ static SortedOpts& opts() {
         d.tile_wide = (int)num("RS_TILE_WIDE", d.tile_wide);
         d.auto_tile = (int)num("RS_AUTO_TILE", d.auto_tile);
         d.fast_keys = (int)num("RS_FAST_KEYS", d.fast_keys);
+        d.range_max = (unsigned)num("RS_RANGE_MAX", d.range_max);
         d.bin_rank = (int)num("RS_BIN_RANK", d.bin_rank);
         d.rec_ids = (int)num("RS_REC_IDS", d.rec_ids);
         d.warp_chunks = (unsigned)num("RS_WARP_CHUNKS", d.warp_chunks);
@@ -1705,6 +1810,7 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "tile_wide")) { prev = o.tile_wide; if (value >= 0) o.tile_wide = (int)value; }
     else if (!strcmp(name, "rec_ids")) { prev = o.rec_ids; if (value >= 0) o.rec_ids = (int)value; }
     else if (!strcmp(name, "bin_rank")) { prev = o.bin_rank; if (value >= 0) o.bin_rank = (int)value; }
+    else if (!strcmp(name, "range_max")) { prev = o.range_max; if (value >= 0) o.range_max = (unsigned)value; }
     else if (!strcmp(name, "fast_keys")) { prev = o.fast_keys; if (value >= 0 && value <= 2) o.fast_keys = (int)value; }
     else if (!strcmp(name, "auto_tile")) { prev = o.auto_tile; if (value >= 3 && value <= 5) o.auto_tile = (int)value; }
     else if (!strcmp(name, "warp_chunks")) { prev = o.warp_chunks; if (value > 0) o.warp_chunks = (unsigned)value; }
@@ -1808,6 +1914,8 @@ void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t
     SortedArgs a = a0;
     a.tile_area = tile_area();
     a.rec_ids = opts().rec_ids;
+    a.range_max = opts().range_max;
+    if (!a.range_max) a.codes = nullptr;
     a.tile_min_density = tile_min_density();
     a.tile_balance = tile_balance();
     a.warp_chunks = opts().warp_chunks;

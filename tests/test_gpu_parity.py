@@ -182,7 +182,9 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"trav": 4, "warp_chunks": 64},                 # warp tiles overflowing their lists
     {"trav": 5, "tile_balance": 1, "tile_area": 1 << 20},  # pipelined tiles, overflowing
     {"trav": 5, "tile_balance": 64},                # pipelined tiles, small
-], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall"])
+    {"range_max": 0},                               # candidate lists from the walk only
+    {"range_max": 1 << 30},                         # candidate lists from key ranges only
+], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall", "walkonly", "rangeonly"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
 def test_tile_knobs_bitwise(name, mode, knobs):
