@@ -1001,7 +1001,9 @@ struct TileSmem {
     int ovf;
     int ncut;
     unsigned tile;
-    int ri0, ri1;  // Morton-range candidate interval [ri0, ri1)
+    unsigned long long rk[8][2];  // Morton-range sub-boxes: key bounds
+    int rr[8][2];                 // and their leaf intervals [i0, i1)
+    int nr;
 };
 
 __device__ __forceinline__ float wred_min(float v) {
@@ -1179,6 +1181,9 @@ __device__ __forceinline__ void build_cut(SM& sm, const RsSlot* nodes, int n_int
 }
 
 // ---- Morton-range candidate lists ------------------------------------------
+#ifndef RS_RANGE_SPLIT
+#define RS_RANGE_SPLIT 0
+#endif
 // Triangle t's centroid lies in its box, so a box overlapping U has its
 // centroid inside U grown by the largest triangle side per axis, S.  Morton
 // order is monotone in every coordinate, so every such centroid's key lies
@@ -1186,6 +1191,60 @@ __device__ __forceinline__ void build_cut(SM& sm, const RsSlot* nodes, int n_int
 // Scanning that run (exact box test against U) yields exactly the walk's
 // candidate list when the run is short; long runs (boxes straddling a coarse
 // Morton boundary) fall back to the walk.
+// Quantised key coordinates of a point, exactly as k_keys forms them.
+__device__ __forceinline__ void range_q(const SortedArgs& a, const double p[3], unsigned q[3]) {
+    double lo[3], ext[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = from_ord(~__ldg(&a.hdr->smin[k]));
+        ext[k] = __dsub_rn(from_ord(__ldg(&a.hdr->smax[k])), lo[k]);
+    }
+    if (a.key_mode == 0) {
+        const double e = fmax(fmax(ext[0], ext[1]), ext[2]);
+        ext[0] = ext[1] = ext[2] = e;
+    }
+    const double gmax = (double)((1u << kIsoBits) - 1u);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) q[k] = ext[k] > 0.0 ? quant1(p[k], lo[k], ext[k], gmax) : 0u;
+}
+
+__device__ __forceinline__ unsigned long long code_of(const unsigned q[3]) {
+    return split21(q[0]) | (split21(q[1]) << 1) | (split21(q[2]) << 2);
+}
+
+// Split the key box [ql, qh] at the highest key bit where its corner keys
+// differ (that bit is one axis's bit l: the halves lie below / above the
+// axis value with bit l set), up to three times: at most 8 sub-boxes whose
+// key ranges are disjoint and together hold every key of the box, far
+// tighter than the box's single range.  Returns the count; writes the
+// corner keys.
+__device__ __forceinline__ int range_split(const unsigned ql[3], const unsigned qh[3],
+                                           unsigned long long (*rk)[2]) {
+    unsigned lo[8][3], hi[8][3];
+    int n = 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { lo[0][k] = ql[k]; hi[0][k] = qh[k]; }
+    for (int d = 0; d < RS_RANGE_SPLIT; ++d) {
+        const int m = n;
+        for (int b = 0; b < m; ++b) {
+            const unsigned long long x = code_of(lo[b]) ^ code_of(hi[b]);
+            if (!x) continue;
+            const int p = 63 - __clzll((long long)x), ax = p % 3, l = p / 3;
+            const unsigned bnd = (hi[b][ax] >> l) << l;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) { lo[n][k] = lo[b][k]; hi[n][k] = hi[b][k]; }
+            hi[b][ax] = bnd - 1;  // box b keeps the lower half
+            lo[n][ax] = bnd;      // box n takes the upper half
+            ++n;
+        }
+    }
+    for (int b = 0; b < n; ++b) {
+        rk[b][0] = code_of(lo[b]);
+        rk[b][1] = code_of(hi[b]);
+    }
+    return n;
+}
+
 __device__ __forceinline__ unsigned long long range_key(const SortedArgs& a, const double p[3]) {
     double lo[3], ext[3];
 #pragma unroll
@@ -1294,10 +1353,10 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
                 if (w == 0) { u[k] = sm.part[0][k]; u[k + 1] = sm.part[0][k + 1]; }
                 else { u[k] = fminf(u[k], sm.part[w][k]); u[k + 1] = fmaxf(u[k + 1], sm.part[w][k + 1]); }
             }
-        // 2a. the Morton-range list when the run of candidate keys is short
+        // 2a. the Morton-range list when the runs of candidate keys are short
         bool ranged = false;
         if (a.codes) {
-            if (warp == 0) {
+            if (tid == 0) {
                 double plo[3], phi[3];
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
@@ -1306,29 +1365,39 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
                     plo[k] = l - sz - 1e-9 * (fabs(l) + sz + 1.0);
                     phi[k] = h + sz + 1e-9 * (fabs(h) + sz + 1.0);
                 }
-                const int i0 = warp_bound(a, range_key(a, plo), false);
-                const int i1 = warp_bound(a, range_key(a, phi), true);
-                if (lane == 0) {
-                    sm.ri0 = i0;
-                    sm.ri1 = i1;
-                }
+                unsigned ql[3], qh[3];
+                range_q(a, plo, ql);
+                range_q(a, phi, qh);
+                sm.nr = range_split(ql, qh, sm.rk);
             }
             __syncthreads();
-            const int i0 = sm.ri0, i1 = sm.ri1;
-            if (i1 - i0 <= (int)a.range_max) {
+            const int nr = sm.nr;
+            // one bound per warp: 2 * nr searches over the four warps
+            for (int t = warp; t < 2 * nr; t += kTileThreads / 32) {
+                const int r = t >> 1, hi = t & 1;
+                const int i = warp_bound(a, sm.rk[r][hi], hi != 0);
+                if (lane == 0) sm.rr[r][hi] = i;
+            }
+            __syncthreads();
+            int total = 0;
+            for (int r = 0; r < nr; ++r) total += sm.rr[r][1] - sm.rr[r][0];
+            if (total <= (int)a.range_max) {
                 ranged = true;
-                for (int i = i0 + tid; i < i1; i += kTileThreads) {
-                    const float2* lb = reinterpret_cast<const float2*>(a.leaf_boxes + 6ll * i);
-                    const float2 x = __ldg(lb), y = __ldg(lb + 1), z = __ldg(lb + 2);
-                    const float4 xy = make_float4(x.x, x.y, y.x, y.y);
-                    if (box_ov(u, xy, z)) {
-                        const int k = atomicAdd(&sm.nl, 1);
-                        if (k < kTileLCap) {
-                            sm.lxy[k] = xy;
-                            sm.lz[k] = z;
-                            sm.lid[k] = i;
-                        } else {
-                            sm.ovf = 1;
+                for (int r = 0; r < nr; ++r) {
+                    const int i0 = sm.rr[r][0], i1 = sm.rr[r][1];
+                    for (int i = i0 + tid; i < i1; i += kTileThreads) {
+                        const float2* lb = reinterpret_cast<const float2*>(a.leaf_boxes + 6ll * i);
+                        const float2 x = __ldg(lb), y = __ldg(lb + 1), z = __ldg(lb + 2);
+                        const float4 xy = make_float4(x.x, x.y, y.x, y.y);
+                        if (box_ov(u, xy, z)) {
+                            const int k = atomicAdd(&sm.nl, 1);
+                            if (k < kTileLCap) {
+                                sm.lxy[k] = xy;
+                                sm.lz[k] = z;
+                                sm.lid[k] = i;
+                            } else {
+                                sm.ovf = 1;
+                            }
                         }
                     }
                 }
