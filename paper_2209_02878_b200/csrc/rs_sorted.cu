@@ -81,15 +81,15 @@ __device__ __forceinline__ void get_rec(const SortedArgs& a, unsigned idx, float
         r0 = make_float4(__ldg(S), __ldg(S + 1), __ldg(S + 2), __int_as_float(id));
         r1 = make_float4(__ldg(E), __ldg(E + 1), __ldg(E + 2), 0.f);
     } else {
-        r0 = a.rec[2 * idx];
-        r1 = a.rec[2 * idx + 1];
+        r0 = a.rec[2ull * idx];
+        r1 = a.rec[2ull * idx + 1];
     }
 }
 
 __device__ __forceinline__ void put_rec(const SortedArgs& a, unsigned pos, const float s[3], int id,
                                         const float e[3]) {
     if (a.rec_ids) reinterpret_cast<int*>(a.rec)[pos] = id;
-    else st_rec(a.rec + 2 * pos, s, id, e);
+    else st_rec(a.rec + 2ull * pos, s, id, e);
 }
 
 __device__ __forceinline__ unsigned spread3(unsigned v) {  // bit i -> bit 3i (i < 10)
