@@ -1755,7 +1755,6 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_wtile(Sor
     const int root = __ldg(&a.hdr->root);
     const RsSlot* const nodes = reinterpret_cast<const RsSlot*>(a.nodes);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
     build_cut(sm, nodes, n_int, root);
     __syncthreads();
     const int ncut = sm.ncut;
