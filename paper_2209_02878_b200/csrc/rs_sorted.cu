@@ -1545,15 +1545,11 @@ __device__ __noinline__ void wtile_fallback(const SortedArgs& a, const RsSlot* n
 // the CTA's cut (ballot-compacted levels, warp-level synchronisation only)
 // collecting every leaf that overlaps it into (lxy, lz, lid).  Returns the
 // leaf count; ovf is set when the list or a level exceeds its capacity.
-template <class CUT>
-__device__ __forceinline__ int warp_walk(const SortedArgs& a, const CUT& cut, int ncut,
-                                         const RsSlot* nodes, unsigned beg, unsigned end,
-                                         float4* lxy, float2* lz, int* lid, int lcap,
-                                         int (*front)[kWtFCap], int fcap, bool& ovf) {
-    const int n_int = a.n_int;
+// One warp: the union box of records [beg, end).
+__device__ __forceinline__ void warp_union(const SortedArgs& a, unsigned beg, unsigned end, float u[6]) {
     const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    float u[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
+    u[0] = u[2] = u[4] = INFINITY;
+    u[1] = u[3] = u[5] = -INFINITY;
     for (unsigned idx = beg + lane; idx < end; idx += 32) {
         float4 r0, r1;
         get_rec(a, idx, r0, r1);
@@ -1566,6 +1562,63 @@ __device__ __forceinline__ int warp_walk(const SortedArgs& a, const CUT& cut, in
         u[k] = wred_min(u[k]);
         u[k + 1] = wred_max(u[k + 1]);
     }
+}
+
+
+// One warp: the candidate list of union box u from its Morton key range
+// (see k_trav_tile); -1 when the range holds more than a.range_max leaves.
+__device__ __forceinline__ int warp_range(const SortedArgs& a, const float u[6], float4* lxy,
+                                          float2* lz, int* lid, int lcap, bool& ovf) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    double plo[3], phi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double sz = (double)__uint_as_float(__ldg(&a.hdr->tsize[k]));
+        const double l = (double)u[2 * k], h = (double)u[2 * k + 1];
+        plo[k] = l - sz - 1e-9 * (fabs(l) + sz + 1.0);
+        phi[k] = h + sz + 1e-9 * (fabs(h) + sz + 1.0);
+    }
+    const int i0 = warp_bound(a, range_key(a, plo), false);
+    const int i1 = warp_bound(a, range_key(a, phi), true);
+    if (i1 - i0 > (int)a.range_max) return -1;
+    int nl = 0;
+    for (int b = i0; b < i1; b += 32) {
+        const int i = b + lane;
+        bool hit = false;
+        float4 xy;
+        float2 z;
+        if (i < i1) {
+            const float2* lb = reinterpret_cast<const float2*>(a.leaf_boxes + 6ll * i);
+            const float2 x = __ldg(lb), y = __ldg(lb + 1);
+            z = __ldg(lb + 2);
+            xy = make_float4(x.x, x.y, y.x, y.y);
+            hit = box_ov(u, xy, z);
+        }
+        const unsigned m = __ballot_sync(kFullMask, hit);
+        if (hit) {
+            const int k = nl + __popc(m & lt);
+            if (k < lcap) {
+                lxy[k] = xy;
+                lz[k] = z;
+                lid[k] = i;
+            }
+        }
+        nl += __popc(m);
+    }
+    ovf = nl > lcap;
+    __syncwarp();
+    return nl;
+}
+
+template <class CUT>
+__device__ __forceinline__ int warp_walk_u(const SortedArgs& a, const CUT& cut, int ncut,
+                                           const RsSlot* nodes, const float u[6], float4* lxy,
+                                           float2* lz, int* lid, int lcap, int (*front)[kWtFCap],
+                                           int fcap, bool& ovf) {
+    const int n_int = a.n_int;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     int nl = 0, nf = 0;
     for (int i0 = 0; i0 < ncut; i0 += 32) {
         const int i = i0 + lane;
@@ -1647,6 +1700,16 @@ __device__ __forceinline__ int warp_walk(const SortedArgs& a, const CUT& cut, in
     }
     __syncwarp();
     return nl;
+}
+
+template <class CUT>
+__device__ __forceinline__ int warp_walk(const SortedArgs& a, const CUT& cut, int ncut,
+                                         const RsSlot* nodes, unsigned beg, unsigned end,
+                                         float4* lxy, float2* lz, int* lid, int lcap,
+                                         int (*front)[kWtFCap], int fcap, bool& ovf) {
+    float u[6];
+    warp_union(a, beg, end, u);
+    return warp_walk_u(a, cut, ncut, nodes, u, lxy, lz, lid, lcap, front, fcap, ovf);
 }
 
 // ---- pipelined tiles -------------------------------------------------------
@@ -1769,9 +1832,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_wtile(Sor
         if (unit >= n_units) break;
         const unsigned beg = unit * U;
         const unsigned end = beg + U < n_live ? beg + U : n_live;
-        bool ovf;
-        const int nl = warp_walk(a, sm, ncut, nodes, beg, end, wt.lxy, wt.lz, wt.lid, kWtLCap,
-                                 wt.front, kWtFCap, ovf);
+        bool ovf = false;
+        float u[6];
+        warp_union(a, beg, end, u);
+        int nl = a.codes ? warp_range(a, u, wt.lxy, wt.lz, wt.lid, kWtLCap, ovf) : -1;
+        if (nl < 0)
+            nl = warp_walk_u(a, sm, ncut, nodes, u, wt.lxy, wt.lz, wt.lid, kWtLCap, wt.front, kWtFCap, ovf);
         __syncwarp();
 #ifdef RS_TILE_STATS
         if (lane == 0) {
