@@ -503,3 +503,28 @@ def test_adversarial_vs_oracle(kind, mode, variant):
     assert_result_fields(result_dict(got), want, f"{kind} {mode} {variant}")
     base = rs.run_baseline_allpairs(mesh, batch, rs.EngineConfig(mode=mode))
     assert_result_fields(result_dict(base), want, f"{kind} {mode} baseline")
+
+
+@pytest.mark.parametrize("n_tri,n_seg,seed", [(1, 1, 1), (2, 33, 2), (17, 5000, 3), (500, 300_000, 4),
+                                              (20_000, 300_000, 5), (20_000, 2_000, 6)])
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+def test_scene_sweep_ground_truth(n_tri, n_seg, seed, device):
+    """Generated scenes across sizes and segment densities (both sides of the
+    tile/per-record switch, host and device paths): every mode against the
+    generator's ground truth."""
+    sc = rs.generate_scene(n_tri, n_seg, 0.5, seed=seed)
+    mesh, batch = sc.mesh, sc.segments
+    if device:
+        mesh = rs.Mesh.from_arrays(torch.from_numpy(mesh.vertices).cuda(),
+                                   torch.from_numpy(mesh.triangles).cuda())
+        batch = rs.SegmentBatch.from_arrays(torch.from_numpy(batch.starts).cuda(),
+                                            torch.from_numpy(batch.ends).cuda())
+    truth = sc.expected_crossings.astype(np.int32)
+    for mode in MODES:
+        r = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode))
+        if mode == "boolean":
+            assert np.array_equal(_np(r.crossing), truth), mode
+        elif mode == "count":
+            assert np.array_equal(_np(r.counts), truth), mode
+        else:
+            assert np.array_equal(_np(r.ray_index), np.nonzero(truth)[0]), mode
