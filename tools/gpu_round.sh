@@ -47,6 +47,11 @@ for w in $WHAT; do
         env $(echo "$ev" | tr ',' ' ') timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
           --log-file "$OUT/kl_${c}_$tag.csv" python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>> "$OUT/bench.err";
         python tools/launch_table.py "$OUT/kl_${c}_$tag.csv" 18 > "$OUT/kl_${c}_$tag.txt"; done; done;;
+    ab) # interleaved A/B of libraries RS_LIBS (names under lib/, default "base ''") on RS_CFGS
+      for rep in 1 2; do for l in ${RS_LIBS:-base cur}; do for c in ${RS_CFGS:-c2 c4 c5}; do
+        if [ "$l" = cur ]; then lib=paper_2209_02878_b200/lib/libraysurf_b200.so; else lib=paper_2209_02878_b200/lib/libraysurf_b200_$l.so; fi
+        RS_LIB=$lib timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 30 > "$OUT/ab_${c}_${l}_$rep.json" 2>> "$OUT/bench.err"
+      done; done; done;;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
