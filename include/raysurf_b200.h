@@ -157,9 +157,15 @@ RS_API int rs_run_batch_host(const float *h_verts, int64_t n_v, const int32_t *h
  * CUDA events on the caller's stream bracket the build, the whole query and
  * the dominant (traversal) kernel; rs_last_timings returns the last call's
  * milliseconds.  enable = 2 records only the traversal kernel's events (the
- * lightest instrumentation; build/query then read 0). */
+ * lightest instrumentation; build/query then read 0).  enable = 3 adds stage
+ * marks on both streams of the fast path (diagnostics): rs_stage_times fills
+ * ms[k] with the time from the call's start to mark k (-1 when not reached):
+ * 0 prep done, 1 keys+sort done, 2 climb done, 4 binning presets done,
+ * 5 sample done, 6 histogram done, 7 scan done, 8 scatter done, 14 traversal
+ * start, 15 traversal end. */
 RS_API int rs_set_timing(int enable);
 RS_API int rs_last_timings(float *build_ms, float *query_ms, float *hot_kernel_ms);
+RS_API int rs_stage_times(float *ms, int n);
 
 /* Cumulative number of kernels this library has launched. */
 RS_API long long rs_kernel_launches(void);

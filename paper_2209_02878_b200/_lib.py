@@ -43,6 +43,7 @@ _SIGS = {
                                 p, p, p, p, p, p, p, p]),
     "rs_set_timing": (i32, [i32]),
     "rs_last_timings": (i32, [p, p, p]),
+    "rs_stage_times": (i32, [p, i32]),
     "rs_kernel_launches": (C.c_longlong, []),
     "rs_last_status": (i32, [p]),
     "rs_set_option": (i32, [C.c_char_p, C.c_longlong, p]),
@@ -67,6 +68,8 @@ def lib() -> C.CDLL:
                 "(the engine has no CPU fallback)")
         dll = C.CDLL(str(LIB_PATH))
         for name, (res, args) in _SIGS.items():
+            if "RS_LIB" in _os.environ and not hasattr(dll, name):
+                continue  # an older A/B build without a newer diagnostic entry point
             fn = getattr(dll, name)
             fn.restype = res
             fn.argtypes = args

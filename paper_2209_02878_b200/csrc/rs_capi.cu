@@ -55,8 +55,10 @@ const bool g_binary_fast = [] {
 
 // Phase timing (engine.py's timings dict, measured on device): when enabled,
 // events bracket the build and the query kernel on the caller's stream.
-thread_local int g_timing = 0;  // 0 off, 1 phases + hot kernel, 2 hot kernel only
-thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+thread_local int g_timing = 0;  // 0 off, 1 phases + hot kernel, 2 hot kernel only, 3 stages
+constexpr int kStageEvents = 16;  // level 3 (diagnostics): stage marks on both streams
+thread_local cudaEvent_t g_ev[5 + kStageEvents] = {};
+thread_local float g_stage_ms[kStageEvents] = {};
 thread_local float g_build_ms = 0.f, g_query_ms = 0.f, g_hot_ms = 0.f;
 thread_local bool g_ev_valid = false;
 
@@ -66,7 +68,7 @@ thread_local bool g_ev_valid = false;
 thread_local int g_hot_mark_mask = 3;
 
 void ev_record(int k, cudaStream_t s) {
-    if (!g_timing || (g_timing == 2 && k < 3)) return;
+    if (!g_timing || (g_timing == 2 && k < 3) || (g_timing != 3 && k >= 5)) return;
     if (!g_ev[k]) cudaEventCreate(&g_ev[k]);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
@@ -254,12 +256,15 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
             rc = after_prep(t);
             if (rc) return rc;
         }
+        stage_mark(0, s);
         launch_keys(cent, n, t->hdr, kind, keys, vals, s);
         launch_sort(keys, vals, keys2, vals2, n, passes, sort_scratch, s);
+        stage_mark(1, s);
         if (lean) launch_climb_lean(V, T, n, keys, vals, t->ta.visit, t->nodes, t->leaves, t->hdr,
                                     t->ta.leaf_bounds, s);
         else launch_climb(V, T, n, keys, vals, t->ta, t->nodes, t->leaves, t->hdr, s);
         if (kind == kTreeFast && need_nodes4()) launch_collapse(n, t->ta, t->nodes, t->nodes4, t->hdr, s);
+        stage_mark(2, s);
         if (lean) {  // sorted keys stay with the tree (4 passes: the result is in `keys`)
             t->sample_stride = (n + kMaxSamples - 1) / kMaxSamples;
             t->n_samples = (n + t->sample_stride - 1) / t->sample_stride;
@@ -500,18 +505,29 @@ static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d
 // Phase 1 of the sorted fast path: output presets + spatial binning.  Needs
 // only the tree header's root box, so it may run concurrently with the rest
 // of the build on another stream.
-static int fast_bin(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
-                    const FastOut& o, FastScratch& f, cudaStream_t s) {
+static int fast_presets(const float* d_s, const float* d_e, int64_t n_r, int mode, const FastOut& o,
+                        FastScratch& f, cudaStream_t s) {
     const bool bary = mode == kBarycentric;
     CK(cudaMemsetAsync(f.st, 0, sizeof(RsStatus), s));
-    if (!bary) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
+    // boolean/count outputs start at 0: zeroed by the histogram pass when it can
+    if (!bary && !binning_zeroes_flags(d_s, d_e, n_r, o.flags)) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
     if (bary) {
         CK(cudaMemsetAsync(f.best_t, 0xFF, 8ull * n_r, s));
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
         CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
     }
     CK(cudaMemsetAsync(f.bins, 0, 4 * sorted_bins() + 4 * (2 * (sorted_bins() / 1024) + 64), s));  // counters, look-back words, ticket
-    launch_binning(sorted_args(t, d_s, d_e, n_r, o, f), s);
+    stage_mark(4, s);
+    return RS_OK;
+}
+
+static int fast_bin(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
+                    const FastOut& o, FastScratch& f, cudaStream_t s, bool presets = true) {
+    if (presets) {
+        const int rc = fast_presets(d_s, d_e, n_r, mode, o, f, s);
+        if (rc) return rc;
+    }
+    launch_binning(sorted_args(t, d_s, d_e, n_r, o, f), s, mode != kBarycentric);
     return RS_OK;
 }
 
@@ -1060,13 +1076,21 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         }
         g_hot_ms = 0.f;
         if (g_ev[3] && g_ev[4]) cudaEventElapsedTime(&g_hot_ms, g_ev[3], g_ev[4]);
+        for (int k = 0; k < kStageEvents; ++k) {
+            g_stage_ms[k] = -1.f;
+            if (g_timing == 3 && g_ev[0] && g_ev[5 + k]) cudaEventElapsedTime(&g_stage_ms[k], g_ev[0], g_ev[5 + k]);
+        }
+        if (g_timing == 3 && g_ev[0] && g_ev[3] && g_ev[4]) {  // 14, 15: the traversal's start and end
+            cudaEventElapsedTime(&g_stage_ms[14], g_ev[0], g_ev[3]);
+            cudaEventElapsedTime(&g_stage_ms[15], g_ev[0], g_ev[4]);
+        }
         g_ev_valid = true;
     }
     return rc;
 }
 
 RS_API int rs_set_timing(int enable) {
-    g_timing = enable == 2 ? 2 : (enable != 0 ? 1 : 0);
+    g_timing = enable == 2 || enable == 3 ? enable : (enable != 0 ? 1 : 0);
     g_ev_valid = false;
     return RS_OK;
 }
@@ -1076,6 +1100,12 @@ RS_API int rs_last_timings(float* build_ms, float* query_ms, float* hot_ms) {
     if (build_ms) *build_ms = g_build_ms;
     if (query_ms) *query_ms = g_query_ms;
     if (hot_ms) *hot_ms = g_hot_ms;
+    return RS_OK;
+}
+
+RS_API int rs_stage_times(float* ms, int n) {
+    if (!g_ev_valid || g_timing != 3) return fail(RS_INVALID_ARG, "no stage-timed call yet (rs_set_timing(3))");
+    for (int k = 0; k < n && k < kStageEvents; ++k) ms[k] = g_stage_ms[k];
     return RS_OK;
 }
 
@@ -1100,6 +1130,10 @@ RS_API int rs_last_status(unsigned long long* out8) {
 }
 
 }  // extern "C"
+
+void rs::stage_mark(int k, cudaStream_t s) {
+    if (k >= 0 && k < kStageEvents) ev_record(5 + k, s);
+}
 
 void rs::hot_kernel_mark(int which, cudaStream_t s) {
     if (g_hot_mark_mask & (1 << which)) ev_record(3 + which, s);

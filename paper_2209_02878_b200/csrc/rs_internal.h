@@ -11,6 +11,7 @@ namespace rs {
 void count_launches(long long k);
 // Device timing of the dominant kernel (bench.py roofline): 0 before, 1 after.
 void hot_kernel_mark(int which, cudaStream_t s);
+void stage_mark(int k, cudaStream_t s);  // rs_set_timing(3) diagnostics
 
 // The reference BvhTree SoA fields (lbvh.py:39-55) plus climb scratch.
 struct TreeArrays {
@@ -179,11 +180,15 @@ struct SortedArgs {
     unsigned tile_balance;      // tile traversal: at least this many tiles per CTA
     unsigned warp_chunks;       // warp tiles: 32-record chunks per warp unit
     unsigned tile_min_density;  // tile traversal only above this many records per triangle
+    int zero_flags;             // the histogram pass zeroes flags (instead of a preset memset)
 };
 size_t sorted_bins();
 bool sorted_wide();  // RS_SORTED_WIDE=1: 4-wide per-thread traversal (needs nodes4)
 // binning needs only the header's root box (available right after k_prep)
-void launch_binning(const SortedArgs& a, cudaStream_t s);
+void launch_binning(const SortedArgs& a, cudaStream_t s, bool zero_flags = false);
+// whether launch_binning(..., zero_flags=true) can zero `flags` in its
+// histogram pass (TMA path, 16-B aligned rows and flags)
+bool binning_zeroes_flags(const float* starts, const float* ends, long long n_r, const int* flags);
 void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t s);
 // Tuning knob by name (trav, tile_density, tile_balance, tile_area,
 // bin_occupancy); value < 0 (or 0 for counts) only reads.  -1: unknown name.

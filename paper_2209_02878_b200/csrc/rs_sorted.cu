@@ -629,6 +629,13 @@ __global__ void __launch_bounds__(kStreamThreads) k_bin_count_tma(SortedArgs a) 
     root_info(a, ri, lut);
     const int lane = threadIdx.x & 31;
     stream_segments(a, [&](float (&s)[4][3], float (&e)[4][3], int cnt, long long q) {
+        if (!RANK && a.zero_flags) {  // the boolean/count outputs' zero preset, fused
+            if (cnt == 4) {
+                *reinterpret_cast<int4*>(a.flags + 4 * q) = make_int4(0, 0, 0, 0);
+            } else {
+                for (int j = 0; j < cnt; ++j) a.flags[4 * q + j] = 0;
+            }
+        }
         int bin[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) bin[j] = j < cnt ? seg_bin(s[j], e[j], ri, lut) : -1;
@@ -1960,8 +1967,15 @@ static unsigned tile_balance() { return opts().tile_balance; }
 static unsigned bin_occupancy() { return opts().bin_occ; }
 static unsigned tile_area() { return opts().tile_area; }
 
-void launch_binning(const SortedArgs& a0, cudaStream_t s) {
+bool binning_zeroes_flags(const float* starts, const float* ends, long long n_r, const int* flags) {
+    const uintptr_t al = reinterpret_cast<uintptr_t>(starts) | reinterpret_cast<uintptr_t>(ends) |
+                         reinterpret_cast<uintptr_t>(flags);
+    return flags && (al & 15) == 0 && opts().bin_tma && !opts().bin_rank && n_r >= kStreamSegs;
+}
+
+void launch_binning(const SortedArgs& a0, cudaStream_t s, bool zero_flags) {
     SortedArgs a = a0;
+    a.zero_flags = zero_flags && binning_zeroes_flags(a.starts, a.ends, a.n_r, a.flags);
     a.bin_occupancy = bin_occupancy();
     a.rec_ids = opts().rec_ids;
     if (a.n_r <= 0) return;
@@ -1980,9 +1994,12 @@ void launch_binning(const SortedArgs& a0, cudaStream_t s) {
         const long long chunks = a.n_r / kStreamSegs;
         const unsigned g = (unsigned)(chunks < sms * (long long)RS_STREAM_CTAS ? chunks : sms * (long long)RS_STREAM_CTAS);
         const bool rank = opts().bin_rank;
+        stage_mark(5, s);
         if (rank) k_bin_count_tma<true><<<g, kStreamThreads, kStreamSmem, s>>>(a);
         else k_bin_count_tma<false><<<g, kStreamThreads, kStreamSmem, s>>>(a);
+        stage_mark(6, s);
         k_bin_scan1<<<kScanTiles, 256, 0, s>>>(a);
+        stage_mark(7, s);
         if (rank) {
             const long long want = (a.n_r + 1023) / 1024;
             const unsigned g2 = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
@@ -1994,6 +2011,7 @@ void launch_binning(const SortedArgs& a0, cudaStream_t s) {
             const unsigned g2 = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
             k_bin_scatter<true><<<g2, 256, 0, s>>>(a);
         }
+        stage_mark(8, s);
         return;
     }
     const long long want = (a.n_r + 1023) / 1024;

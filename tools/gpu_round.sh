@@ -50,7 +50,7 @@ for w in $WHAT; do
     ab) # interleaved A/B of libraries RS_LIBS (names under lib/, default "base ''") on RS_CFGS
       for rep in 1 2; do for l in ${RS_LIBS:-base cur}; do for c in ${RS_CFGS:-c2 c4 c5}; do
         if [ "$l" = cur ]; then lib=paper_2209_02878_b200/lib/libraysurf_b200.so; else lib=paper_2209_02878_b200/lib/libraysurf_b200_$l.so; fi
-        RS_LIB=$lib timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 30 > "$OUT/ab_${c}_${l}_$rep.json" 2>> "$OUT/bench.err"
+        RS_LIB=$lib timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps ${RS_AB_STEPS:-30} > "$OUT/ab_${c}_${l}_$rep.json" 2>> "$OUT/bench.err"
       done; done; done;;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
