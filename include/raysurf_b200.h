@@ -161,8 +161,9 @@ RS_API int rs_run_batch_host(const float *h_verts, int64_t n_v, const int32_t *h
  * marks on both streams of the fast path (diagnostics): rs_stage_times fills
  * ms[k] with the time from the call's start to mark k (-1 when not reached):
  * 0 prep done, 1 keys+sort done, 2 climb done, 4 binning presets done,
- * 5 sample done, 6 histogram done, 7 scan done, 8 scatter done, 14 traversal
- * start, 15 traversal end. */
+ * 5 sample done, 6 histogram done, 7 scan done, 8 scatter done, 9 status copied,
+ * 10 frees done, 14 traversal start, 15 traversal end; 11 and 12 are the host
+ * milliseconds spent in the graph launch and in the wait. */
 RS_API int rs_set_timing(int enable);
 RS_API int rs_last_timings(float *build_ms, float *query_ms, float *hot_kernel_ms);
 RS_API int rs_stage_times(float *ms, int n);

@@ -3,6 +3,7 @@
 // pool), tree lifetime, status read-back, and the chunked H2D / query / D2H
 // pipeline of rs_run_batch_host.
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -59,6 +60,7 @@ thread_local int g_timing = 0;  // 0 off, 1 phases + hot kernel, 2 hot kernel on
 constexpr int kStageEvents = 16;  // level 3 (diagnostics): stage marks on both streams
 thread_local cudaEvent_t g_ev[5 + kStageEvents] = {};
 thread_local float g_stage_ms[kStageEvents] = {};
+thread_local float g_host_ms[2] = {};
 thread_local float g_build_ms = 0.f, g_query_ms = 0.f, g_hot_ms = 0.f;
 thread_local bool g_ev_valid = false;
 
@@ -443,6 +445,7 @@ struct FastScratch {
     unsigned *bins = nullptr, *cursor = nullptr, *n_live = nullptr;
     float4* rec = nullptr;
     unsigned long long* seg_key = nullptr;
+    void* geom = nullptr;
 };
 
 // RS_FAST_PATH=buffer: pair traversal -> collision buffer -> exact pass
@@ -464,7 +467,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
                  align256(bary_compact_scratch(n_r));
     if (g_buffer_path) total += align256(4 * trav_gstack_ints());
     total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r) +
-             align256(8ull * n_r);
+             align256(8ull * n_r) + align256(bin_geom_bytes());
     CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
@@ -484,6 +487,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     f.n_live = c.take<unsigned>(64 + 4 * 32);
     f.rec = c.take<float4>(2ull * n_r);
     f.seg_key = c.take<unsigned long long>(n_r);
+    f.geom = c.take<char>(bin_geom_bytes());
     f.cap = cap;
     return RS_OK;
 }
@@ -499,6 +503,7 @@ static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d
     a.n_samples = t->n_samples;
     a.leaf_boxes = t->ta.leaf_bounds;
     a.key_mode = t->key_mode;
+    a.geom = f.geom;
     return a;
 }
 
@@ -886,13 +891,43 @@ static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d
     return rc ? rc : rc2;
 }
 
+// The status words go to mapped pinned host memory from a one-warp kernel:
+// a D2H copy node at the end of the graph cost ~11 us of copy-engine latency
+// per call, the kernel's PCIe writes ~2 us.
+__global__ void k_status_out(RsStatus* dst, const RsStatus* src) {
+    constexpr int kWords = sizeof(RsStatus) / 8;
+    static_assert(sizeof(RsStatus) % 8 == 0 && kWords <= 32, "status is copied as 8-B words");
+    if (threadIdx.x < kWords)
+        reinterpret_cast<volatile unsigned long long*>(dst)[threadIdx.x] =
+            reinterpret_cast<const volatile unsigned long long*>(src)[threadIdx.x];
+    __threadfence_system();
+}
+static const bool g_status_copy = [] {  // RS_STATUS_COPY=1: D2H copy node instead (A/B)
+    const char* e = getenv("RS_STATUS_COPY");
+    return e && e[0] == '1';
+}();
+struct StatusDst {
+    RsStatus* host;  // pinned, mapped
+    RsStatus* dev;   // its device alias
+};
+static int status_out(const StatusDst& d, const RsStatus* st, cudaStream_t s) {
+    if (g_status_copy) {
+        CK(cudaMemcpyAsync(d.host, st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+        return RS_OK;
+    }
+    count_launches(1);
+    k_status_out<<<1, 32, 0, s>>>(d.dev, st);
+    CK(cudaGetLastError());
+    return RS_OK;
+}
+
 // Everything rs_run_batch_device does, enqueued without a host sync so it can
 // be captured into one CUDA graph: build, query, status -> pinned host.
 static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t* d_tris,
                                 int64_t n_t, const float* d_starts, const float* d_ends,
                                 int64_t n_r, int mode, int tree_kind, int max_coll, int max_stack,
                                 int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri,
-                                float* d_pt, RsStatus* h_status, cudaStream_t s) {
+                                float* d_pt, const StatusDst& h_status, cudaStream_t s) {
     rs_tree* t = nullptr;
     if (tree_kind == kTreeFast && !g_buffer_path && !g_binary_fast) {
         FastOut o;
@@ -902,9 +937,13 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
         int rc = enqueue_fast_forked(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode, o, f,
                                      s, &t);
         if (rc) return rc;
-        CK(cudaMemcpyAsync(h_status, f.st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+        rc = status_out(h_status, f.st, s);
+        if (rc) return rc;
+        stage_mark(9, s);
         CK(cudaFreeAsync(f.blk, s));
-        return rs_free(t, s);
+        rc = rs_free(t, s);
+        stage_mark(10, s);
+        return rc;
     }
     ev_record(0, s);
     int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
@@ -918,7 +957,8 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
         if (rc) return rc;
         rc = fast_launch(t, d_starts, d_ends, n_r, mode, o, f, false, s);
         if (rc) return rc;
-        CK(cudaMemcpyAsync(h_status, f.st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+        rc = status_out(h_status, f.st, s);
+        if (rc) return rc;
         CK(cudaFreeAsync(f.blk, s));
     } else {
         const bool compact = mode == kBarycentric;
@@ -936,7 +976,8 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
         if (launch_query(a, mode, ref != 0, compact, kstack_for(ref != 0, max_stack), false, s))
             return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
         ev_record(2, s);
-        CK(cudaMemcpyAsync(h_status, st, sizeof(RsStatus), cudaMemcpyDeviceToHost, s));
+        rc = status_out(h_status, st, s);
+        if (rc) return rc;
         CK(cudaFreeAsync(blk, s));
     }
     return rs_free(t, s);
@@ -950,7 +991,8 @@ struct GraphKey {
 };
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
-    RsStatus* h_status = nullptr;  // pinned
+    RsStatus* h_status = nullptr;  // pinned, mapped
+    RsStatus* d_status = nullptr;  // its device alias
     unsigned long long stamp = 0;
     long long kernels = 0;         // kernel nodes in the graph (for rs_kernel_launches)
 };
@@ -1015,7 +1057,8 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         }
         if (!ge && capture) {
             GraphEntry e;
-            CK(cudaHostAlloc(reinterpret_cast<void**>(&e.h_status), sizeof(RsStatus), cudaHostAllocDefault));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&e.h_status), sizeof(RsStatus), cudaHostAllocMapped));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e.d_status), e.h_status, 0));
             // capture on a private stream (the caller's may be the legacy
             // default stream, which cannot be captured); replay on the caller's
             static thread_local cudaStream_t cap = nullptr;
@@ -1025,7 +1068,7 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
             CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
             const int erc = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
                                                  tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
-                                                 d_tri, d_pt, e.h_status, cap);
+                                                 d_tri, d_pt, StatusDst{e.h_status, e.d_status}, cap);
             const cudaError_t ce = cudaStreamEndCapture(cap, &g);
             e.kernels = rs::g_launches.load() - k0;
             rs::g_launches.fetch_sub(e.kernels);  // counted when replayed
@@ -1049,10 +1092,17 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         }
         if (ge) {
             ge->stamp = ++g_graph_clock;
+            using clk = std::chrono::steady_clock;
+            const auto h0 = clk::now();
             CK(cudaGraphLaunch(ge->exec, s));
+            const auto h1 = clk::now();
             rs::g_launches.fetch_add(ge->kernels);
             CK(cudaStreamSynchronize(s));
-            const RsStatus h = *ge->h_status;
+            if (g_timing == 3) {  // host side of the call: launch and wait (ms)
+                g_host_ms[0] = std::chrono::duration<float, std::milli>(h1 - h0).count();
+                g_host_ms[1] = std::chrono::duration<float, std::milli>(clk::now() - h1).count();
+            }
+            const RsStatus h = *ge->h_status;  // written by k_status_out before the sync returned
             g_last_status = h;
             if (!h.internal) {
                 if (n_hits) *n_hits = (int64_t)h.hits;
@@ -1079,6 +1129,10 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         for (int k = 0; k < kStageEvents; ++k) {
             g_stage_ms[k] = -1.f;
             if (g_timing == 3 && g_ev[0] && g_ev[5 + k]) cudaEventElapsedTime(&g_stage_ms[k], g_ev[0], g_ev[5 + k]);
+        }
+        if (g_timing == 3) {  // 11, 12: host time in cudaGraphLaunch and in the wait
+            g_stage_ms[11] = g_host_ms[0];
+            g_stage_ms[12] = g_host_ms[1];
         }
         if (g_timing == 3 && g_ev[0] && g_ev[3] && g_ev[4]) {  // 14, 15: the traversal's start and end
             cudaEventElapsedTime(&g_stage_ms[14], g_ev[0], g_ev[3]);

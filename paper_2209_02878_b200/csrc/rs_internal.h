@@ -181,8 +181,11 @@ struct SortedArgs {
     unsigned warp_chunks;       // warp tiles: 32-record chunks per warp unit
     unsigned tile_min_density;  // tile traversal only above this many records per triangle
     int zero_flags;             // the histogram pass zeroes flags (instead of a preset memset)
+    void* geom;                 // bin_geom_bytes(): bin geometry, written by k_seg_sample
+    int geom_mode;              // 1: binning CTAs copy geom; 0: each derives it
 };
 size_t sorted_bins();
+size_t bin_geom_bytes();
 bool sorted_wide();  // RS_SORTED_WIDE=1: 4-wide per-thread traversal (needs nodes4)
 // binning needs only the header's root box (available right after k_prep)
 void launch_binning(const SortedArgs& a, cudaStream_t s, bool zero_flags = false);

@@ -40,6 +40,9 @@ constexpr int kBins = 1 << kBinBits;
 constexpr int kScanShift = 10;
 constexpr int kScanTile = 1 << kScanShift;
 constexpr int kScanTiles = kBins / kScanTile;
+// zeroed words in tile_sum after the look-back words: the scan's ticket, then
+// k_seg_sample's completion counter
+constexpr int kScanTicket = 2 * kScanTiles;
 constexpr int kSortedThreads = 128;
 constexpr int kSortedStack = 64;  // fast tree: <= 3 pending per 4-wide level; deeper -> fallback
 #ifndef RS_SORTED_MIN_BLOCKS
@@ -127,7 +130,7 @@ struct RootInfo {
 // The root box (union of all triangle boxes) comes from the build's k_prep,
 // so the binning can run concurrently with the rest of the build.
 __device__ __forceinline__ void root_info_compute(const RsHeader* hdr, const SortedArgs& a,
-                                                  RootInfo& ri) {
+                                                  const float st[4], RootInfo& ri) {
     float e0, e1, e2;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -137,10 +140,6 @@ __device__ __forceinline__ void root_info_compute(const RsHeader* hdr, const Sor
     e0 = fmaxf(ri.hi[0] - ri.lo[0], 0.f);
     e1 = fmaxf(ri.hi[1] - ri.lo[1], 0.f);
     e2 = fmaxf(ri.hi[2] - ri.lo[2], 0.f);
-    float st[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int c = 0; c < kSampleCtas; ++c)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) st[k] += a.seg_stats[4 * c + k];
     // a cell side below the typical segment-box side along that axis buys
     // no coherence (neighbouring boxes overlap anyway): such an axis only
     // gets bits once every other axis is that fine too
@@ -191,19 +190,23 @@ __device__ __forceinline__ int key_pos(int role, int i, int bb, int bc) {
     return 2 * bb + bc + (i - bb);
 }
 
-// One thread derives the bin geometry; the CTA reads it from shared memory
-// and fills per-axis deposit tables: the key is the OR over axes of
-// T[axis][chunk][7-bit chunk of q], 9 table lookups instead of ~80 ALU ops
-// (axis ranking, bit spreading) per key.
-struct BinLut {
+// The bin geometry is derived once per call, by the last CTA of
+// k_seg_sample (bin_geom_fill), into global memory: the RootInfo and
+// per-axis deposit tables (the key is the OR over axes of
+// T[axis][chunk][7-bit chunk of q], 9 table lookups instead of ~80 ALU ops of
+// axis ranking and bit spreading per key).  Every binning CTA copies it to
+// shared memory instead of re-deriving it serially on one thread.
+struct alignas(16) BinLut {
     unsigned t[3][3][128];
 };
-__device__ __forceinline__ void root_info(const SortedArgs& a, RootInfo& ri, const BinLut*& lut) {
-    __shared__ RootInfo s_ri;
-    __shared__ BinLut s_lut;
-    if (threadIdx.x == 0) root_info_compute(a.hdr, a, s_ri);
-    __syncthreads();
-    ri = s_ri;
+struct BinGeom {
+    RootInfo ri;
+    BinLut lut;
+};
+size_t bin_geom_bytes() { return sizeof(BinGeom); }
+
+// the 3x3x128 deposit tables of a bin geometry (all threads of the CTA)
+__device__ __forceinline__ void lut_fill(const RootInfo& ri, unsigned (*t)[3][128]) {
     for (int e = threadIdx.x; e < 3 * 3 * 128; e += blockDim.x) {
         const int axis = e / 384, chunk = (e / 128) % 3, v = e % 128;
         const int role = axis == ri.pa ? 0 : (axis == ri.pb ? 1 : 2);
@@ -213,9 +216,66 @@ __device__ __forceinline__ void root_info(const SortedArgs& a, RootInfo& ri, con
             const int i = 7 * chunk + j;
             if (((v >> j) & 1) && i < nb) out |= 1u << key_pos(role, i, ri.bb, ri.bc);
         }
-        s_lut.t[axis][chunk][v] = out;
+        t[axis][chunk][v] = out;
+    }
+}
+
+// the sample CTAs' partials (one thread, fixed order)
+__device__ __forceinline__ void stats_serial(const SortedArgs& a, float st[4]) {
+    st[0] = st[1] = st[2] = st[3] = 0.f;
+    for (int c = 0; c < kSampleCtas; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st[k] += a.seg_stats[4 * c + k];
+}
+
+__device__ __forceinline__ void bin_geom_fill(const SortedArgs& a) {
+    __shared__ RootInfo s_ri;
+    BinGeom* g = reinterpret_cast<BinGeom*>(a.geom);
+    static_assert(kSampleCtas == 32, "one lane per sample CTA");
+    if (threadIdx.x < 32) {
+        // the sample CTAs' partials, summed in a fixed shuffle tree (deterministic)
+        float st[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float v = __ldcg(a.seg_stats + 4 * threadIdx.x + k);
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+            st[k] = v;
+        }
+        if (threadIdx.x == 0) {
+            root_info_compute(a.hdr, a, st, s_ri);
+            g->ri = s_ri;
+        }
     }
     __syncthreads();
+    lut_fill(s_ri, g->lut.t);
+}
+
+// geom_mode 1: copy the precomputed geometry; 0 (A/B): thread 0 derives it
+// and the CTA fills the tables itself
+__device__ __forceinline__ void root_info(const SortedArgs& a, RootInfo& ri, const BinLut*& lut) {
+    __shared__ RootInfo s_ri;
+    __shared__ BinLut s_lut;
+    if (a.geom_mode) {
+        const BinGeom* g = reinterpret_cast<const BinGeom*>(a.geom);
+        constexpr int kRiWords = sizeof(RootInfo) / 4;
+        static_assert(sizeof(RootInfo) % 4 == 0, "RootInfo is copied as words");
+        if (threadIdx.x < kRiWords)
+            reinterpret_cast<unsigned*>(&s_ri)[threadIdx.x] = __ldg(reinterpret_cast<const unsigned*>(&g->ri) + threadIdx.x);
+        const uint4* src = reinterpret_cast<const uint4*>(&g->lut);
+        uint4* dst = reinterpret_cast<uint4*>(&s_lut);
+        for (int e = threadIdx.x; e < (int)(sizeof(BinLut) / 16); e += blockDim.x) dst[e] = __ldg(src + e);
+        __syncthreads();
+    } else {
+        if (threadIdx.x == 0) {
+            float st[4];
+            stats_serial(a, st);
+            root_info_compute(a.hdr, a, st, s_ri);
+        }
+        __syncthreads();
+        lut_fill(s_ri, s_lut.t);
+        __syncthreads();
+    }
+    ri = s_ri;
     lut = &s_lut;
 }
 
@@ -322,7 +382,16 @@ __global__ void __launch_bounds__(kSampleThreads) k_seg_sample(SortedArgs a) {
         float v = 0.f;
         for (int j = 0; j < kSampleThreads / 32; ++j) v += red[threadIdx.x][j];
         a.seg_stats[4 * blockIdx.x + threadIdx.x] = v;
+        __threadfence();
     }
+    // the last CTA to finish derives the bin geometry for the binning passes
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.tile_sum + kScanTicket + 1, 1u) == kSampleCtas - 1;
+    __syncthreads();
+    if (!s_last || !a.geom_mode) return;
+    __threadfence();
+    bin_geom_fill(a);
 }
 
 // Histogram pass.  Inputs arrive in caller order, so a warp's bins rarely
@@ -426,15 +495,22 @@ __global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
 // per 1024-bin tile in ticket order, decoupled look-back across tiles; the
 // last active tile publishes the live count.  Tiles beyond the active range
 // exit at once.
-constexpr int kScanTicket = 2 * kScanTiles;  // word offset of the ticket in tile_sum
 __global__ void __launch_bounds__(256) k_bin_scan1(SortedArgs a) {
     __shared__ unsigned wtot[8];
     __shared__ int s_tile, s_active;
     __shared__ unsigned s_excl;
     if (threadIdx.x == 0) {
-        RootInfo ri;
-        root_info_compute(a.hdr, a, ri);
-        const int active = (1 << ri.nbits) > kScanTile ? (1 << ri.nbits) / kScanTile : 1;
+        int nbits;
+        if (a.geom_mode) {
+            nbits = (int)__ldg(&reinterpret_cast<const BinGeom*>(a.geom)->ri.nbits);
+        } else {
+            float st[4];
+            RootInfo ri;
+            stats_serial(a, st);
+            root_info_compute(a.hdr, a, st, ri);
+            nbits = ri.nbits;
+        }
+        const int active = (1 << nbits) > kScanTile ? (1 << nbits) / kScanTile : 1;
         s_active = active;
         s_tile = (int)atomicAdd(a.tile_sum + kScanTicket, 1u);
     }
@@ -1910,6 +1986,7 @@ struct SortedOpts {
     int fast_keys = 0;           // fast-tree key grid: 0 isotropic, 1 per-axis, 2 auto
     unsigned range_max = 4096;   // tile lists from a Morton key range of at most this many leaves (0: walk only)
     unsigned warp_chunks = 4;    // warp tiles: records per warp unit / 32
+    int geom = 0;                // 1: bin geometry derived once by k_seg_sample (A/B: C3/C5 -1..2%, C2 +3%)
 };
 static SortedOpts& opts() {
     static SortedOpts o = [] {
@@ -1934,6 +2011,7 @@ static SortedOpts& opts() {
         d.bin_rank = (int)num("RS_BIN_RANK", d.bin_rank);
         d.rec_ids = (int)num("RS_REC_IDS", d.rec_ids);
         d.warp_chunks = (unsigned)num("RS_WARP_CHUNKS", d.warp_chunks);
+        d.geom = (int)num("RS_GEOM", d.geom);
         return d;
     }();
     return o;
@@ -1955,6 +2033,7 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "fast_keys")) { prev = o.fast_keys; if (value >= 0 && value <= 2) o.fast_keys = (int)value; }
     else if (!strcmp(name, "auto_tile")) { prev = o.auto_tile; if (value >= 3 && value <= 5) o.auto_tile = (int)value; }
     else if (!strcmp(name, "warp_chunks")) { prev = o.warp_chunks; if (value > 0) o.warp_chunks = (unsigned)value; }
+    else if (!strcmp(name, "geom")) { prev = o.geom; if (value >= 0) o.geom = value ? 1 : 0; }
     else return -1;
     if (old) *old = prev;
     return 0;
@@ -1976,6 +2055,7 @@ bool binning_zeroes_flags(const float* starts, const float* ends, long long n_r,
 void launch_binning(const SortedArgs& a0, cudaStream_t s, bool zero_flags) {
     SortedArgs a = a0;
     a.zero_flags = zero_flags && binning_zeroes_flags(a.starts, a.ends, a.n_r, a.flags);
+    a.geom_mode = opts().geom;
     a.bin_occupancy = bin_occupancy();
     a.rec_ids = opts().rec_ids;
     if (a.n_r <= 0) return;

@@ -184,7 +184,8 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"trav": 5, "tile_balance": 64},                # pipelined tiles, small
     {"range_max": 0},                               # candidate lists from the walk only
     {"range_max": 1 << 30},                         # candidate lists from key ranges only
-], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall", "walkonly", "rangeonly"])
+    {"geom": 1},                                    # bin geometry derived once by the sample kernel
+], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall", "walkonly", "rangeonly", "geom"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
 def test_tile_knobs_bitwise(name, mode, knobs):
@@ -528,3 +529,27 @@ def test_scene_sweep_ground_truth(n_tri, n_seg, seed, device):
             assert np.array_equal(_np(r.counts), truth), mode
         else:
             assert np.array_equal(_np(r.ray_index), np.nonzero(truth)[0]), mode
+
+
+@pytest.mark.parametrize("n_seg", [1023, 1024, 5003, 70_001])
+@pytest.mark.parametrize("geom", [0, 1])
+def test_outputs_over_garbage_buffers(n_seg, geom):
+    """The boolean/count outputs' zero preset is fused into the histogram pass
+    (16-B aligned rows, >= 1024 segments): caller buffers full of garbage must
+    come back exactly right, ragged tails (n % 4, n % 1024) included, with
+    the bin geometry derived per CTA or once."""
+    from paper_2209_02878_b200.engine import run_device
+
+    sc = rs.generate_scene(3000, n_seg, 0.5, seed=n_seg)
+    mesh = rs.Mesh.from_arrays(torch.from_numpy(sc.mesh.vertices).cuda(),
+                               torch.from_numpy(sc.mesh.triangles).cuda())
+    batch = rs.SegmentBatch.from_arrays(torch.from_numpy(sc.segments.starts).cuda(),
+                                        torch.from_numpy(sc.segments.ends).cuda())
+    truth = sc.expected_crossings.astype(np.int32)
+    with _lib.option("geom", geom):
+        for mode in ("boolean", "count"):
+            for _ in range(3):  # the third call replays a captured graph
+                out = {"flags": torch.full((n_seg,), 7, dtype=torch.int32, device="cuda")}
+                r = run_device(mesh, batch, rs.EngineConfig(mode=mode), "fast", out=out)
+                got = _np(r.crossing if mode == "boolean" else r.counts)
+                assert np.array_equal(got, truth), (mode, n_seg, geom)

@@ -52,6 +52,11 @@ for w in $WHAT; do
         if [ "$l" = cur ]; then lib=paper_2209_02878_b200/lib/libraysurf_b200.so; else lib=paper_2209_02878_b200/lib/libraysurf_b200_$l.so; fi
         RS_LIB=$lib timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps ${RS_AB_STEPS:-30} > "$OUT/ab_${c}_${l}_$rep.json" 2>> "$OUT/bench.err"
       done; done; done;;
+    abenv) # interleaved A/B of env sets RS_ENVS ("A=1,B=2 A=3"; commas -> spaces) on RS_CFGS
+      for rep in 1 2 3; do for ev in ${RS_ENVS:-RS_NONE=1}; do for c in ${RS_CFGS:-c2}; do
+        tag=$(echo "$ev" | tr ',=/' '_-_')
+        env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps ${RS_AB_STEPS:-100} > "$OUT/ab_${c}_${tag}_$rep.json" 2>> "$OUT/bench.err"
+      done; done; done;;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -48,14 +48,18 @@ def measure(mesh_d, seg_d, n, label, reps=200):
     # GPU span of one call (trav end from the start mark) via the stage timing
     lib.rs_set_timing(3)
     arr = (C.c_float * 16)()
-    spans = []
-    for _ in range(10):
+    rows = []
+    for _ in range(12):
         lib.rs_run_batch_device(*args, C.byref(nh), C.byref(bad), s)
         lib.rs_stage_times(arr, 16)
-        spans.append(arr[15] * 1e3)
+        rows.append([x * 1e3 for x in arr])
     lib.rs_set_timing(0)
-    print(f"{label}: wall/call {wall:.1f} us, C call {capi:.1f} us, device span (start..trav end) "
-          f"{np.median(spans):.1f} us")
+    med = [float(np.median([r[k] for r in rows[2:]])) for k in range(16)]
+    names = {0: "prep", 1: "sort", 2: "climb", 4: "presets", 5: "sample", 6: "hist", 7: "scan",
+             8: "scatter", 14: "trav0", 15: "trav1", 9: "status", 10: "frees", 11: "host launch",
+             12: "host wait"}
+    print(f"{label}: wall/call {wall:.1f} us, C call {capi:.1f} us; stages (us): " +
+          ", ".join(f"{names[k]} {med[k]:.1f}" for k in sorted(names)))
 
 
 def main():
