@@ -61,6 +61,10 @@ constexpr int kStageEvents = 16;  // level 3 (diagnostics): stage marks on both 
 thread_local cudaEvent_t g_ev[5 + kStageEvents] = {};
 thread_local float g_stage_ms[kStageEvents] = {};
 thread_local float g_host_ms[2] = {};
+thread_local cudaStream_t g_tstream = nullptr;
+thread_local cudaEvent_t g_tfork[2] = {}, g_tjoin[2] = {};
+thread_local int g_tpending = 0;  // bit k: join k outstanding
+
 thread_local float g_build_ms = 0.f, g_query_ms = 0.f, g_hot_ms = 0.f;
 thread_local bool g_ev_valid = false;
 
@@ -923,7 +927,7 @@ static int status_out(const StatusDst& d, const RsStatus* st, cudaStream_t s) {
 
 // Everything rs_run_batch_device does, enqueued without a host sync so it can
 // be captured into one CUDA graph: build, query, status -> pinned host.
-static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t* d_tris,
+static int enqueue_device_batch_body(const float* d_verts, int64_t n_v, const int32_t* d_tris,
                                 int64_t n_t, const float* d_starts, const float* d_ends,
                                 int64_t n_r, int mode, int tree_kind, int max_coll, int max_stack,
                                 int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri,
@@ -981,6 +985,20 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
         CK(cudaFreeAsync(blk, s));
     }
     return rs_free(t, s);
+}
+
+static void timing_join(cudaStream_t s);
+static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t* d_tris,
+                                int64_t n_t, const float* d_starts, const float* d_ends,
+                                int64_t n_r, int mode, int tree_kind, int max_coll, int max_stack,
+                                int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri,
+                                float* d_pt, const StatusDst& h_status, cudaStream_t s) {
+    g_tpending = 0;
+    const int rc = enqueue_device_batch_body(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
+                                             tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
+                                             d_tri, d_pt, h_status, s);
+    timing_join(s);  // the timing branches end the graph
+    return rc;
 }
 
 struct GraphKey {
@@ -1189,8 +1207,39 @@ void rs::stage_mark(int k, cudaStream_t s) {
     if (k >= 0 && k < kStageEvents) ev_record(5 + k, s);
 }
 
+// Timing level 2 inside a captured graph: the traversal's two event-record
+// nodes hang off side branches (a fork from the caller's stream, joined back
+// only at the end of the graph) instead of sitting in the kernel chain, where
+// each added ~6 us of node latency to every step.
+
 void rs::hot_kernel_mark(int which, cudaStream_t s) {
-    if (g_hot_mark_mask & (1 << which)) ev_record(3 + which, s);
+    if (!(g_hot_mark_mask & (1 << which))) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (g_timing != 2 || cs != cudaStreamCaptureStatusActive) {
+        ev_record(3 + which, s);
+        return;
+    }
+    if (!g_tstream) {
+        cudaStreamCreateWithFlags(&g_tstream, cudaStreamNonBlocking);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventCreateWithFlags(&g_tfork[k], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&g_tjoin[k], cudaEventDisableTiming);
+        }
+    }
+    // each mark gets its own branch: fork from s, record, and remember the join
+    cudaEventRecord(g_tfork[which], s);
+    cudaStreamWaitEvent(g_tstream, g_tfork[which], 0);
+    ev_record(3 + which, g_tstream);
+    cudaEventRecord(g_tjoin[which], g_tstream);
+    g_tpending |= 1 << which;
+}
+
+// joins the timing branches back into s (before a capture ends)
+static void timing_join(cudaStream_t s) {
+    for (int k = 0; k < 2; ++k)
+        if (g_tpending & (1 << k)) cudaStreamWaitEvent(s, g_tjoin[k], 0);
+    g_tpending = 0;
 }
 
 extern "C" {
