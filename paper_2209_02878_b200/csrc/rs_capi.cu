@@ -176,13 +176,43 @@ int check_mesh(int64_t n_v, int64_t n_t) {
     return RS_OK;
 }
 
+// Device memory of a captured graph.  A graph replayed every call keeps its
+// scratch in one arena it owns (one cudaMalloc at capture time) instead of
+// stream-ordered allocation and free nodes: the capture runs twice, once to
+// size the arena (mode 1: allocations pass through and are summed), once to
+// bump-allocate from it (mode 2: frees inside it are no-ops).
+struct Arena {
+    char* base = nullptr;
+    size_t cap = 0, off = 0;
+    int mode = 0;  // 0 off, 1 sizing, 2 bump
+};
+static thread_local Arena g_arena;
+
+static cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t s) {
+    const size_t need = align256(bytes > 0 ? bytes : 1);
+    if (g_arena.mode == 2) {
+        if (g_arena.off + need > g_arena.cap) return cudaErrorMemoryAllocation;
+        *p = g_arena.base + g_arena.off;
+        g_arena.off += need;
+        return cudaSuccess;
+    }
+    if (g_arena.mode == 1) g_arena.off += need;
+    return cudaMallocAsync(p, bytes, s);
+}
+static cudaError_t dfree(void* p, cudaStream_t s) {
+    if (g_arena.mode == 2 && static_cast<char*>(p) >= g_arena.base &&
+        static_cast<char*>(p) < g_arena.base + g_arena.cap)
+        return cudaSuccess;
+    return cudaFreeAsync(p, s);
+}
+
 int alloc_tree(int64_t n, int kind, cudaStream_t s, rs_tree** out) {
     int rc = configure_pool();
     if (rc) return rc;
     rs_tree* t = new rs_tree();
     t->n = n;
     t->kind = kind;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&t->block), tree_bytes(n), s);
+    cudaError_t e = dmalloc(reinterpret_cast<void**>(&t->block), tree_bytes(n), s);
     if (e != cudaSuccess) {
         delete t;
         return fail(RS_CUDA_ERROR, "device allocation of %zu bytes failed: %s", tree_bytes(n),
@@ -245,7 +275,7 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
         const size_t bytes = align256(24ull * n) + 2 * align256(8ull * n) + 2 * align256(4ull * n) +
                              align256(sb) + align256(8ull * kMaxSamples);
         char* scratch = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s));
+        CK(dmalloc(reinterpret_cast<void**>(&scratch), bytes, s));
         Carver c{scratch};
         double* cent = c.take<double>(3ull * n);
         unsigned long long* keys = c.take<unsigned long long>(n);
@@ -280,7 +310,7 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
             t->code_samples = samples;
             t->key_mode = fast_key_mode() == 1 ? 1 : 0;
         } else {
-            CK(cudaFreeAsync(scratch, s));
+            CK(dfree(scratch, s));
         }
     }
     CK(cudaGetLastError());
@@ -414,8 +444,8 @@ int rs_tree_download(const rs_tree* t, float* ib, int32_t* cl, int32_t* cr, int3
 
 int rs_free(rs_tree* t, void* stream) {
     if (!t) return RS_OK;
-    if (t->scratch) cudaFreeAsync(t->scratch, S(stream));
-    cudaError_t e = cudaFreeAsync(t->block, S(stream));
+    if (t->scratch) dfree(t->scratch, S(stream));
+    cudaError_t e = dfree(t->block, S(stream));
     delete t;
     if (e != cudaSuccess) return fail(RS_CUDA_ERROR, "cudaFreeAsync: %s", cudaGetErrorString(e));
     return RS_OK;
@@ -472,7 +502,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     if (g_buffer_path) total += align256(4 * trav_gstack_ints());
     total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r) +
              align256(8ull * n_r) + align256(bin_geom_bytes());
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&f.blk), total, s));
+    CK(dmalloc(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
     f.cand = c.take<int2>(cap);
@@ -599,7 +629,7 @@ static int fast_query(const rs_tree* t, const float* d_s, const float* d_e, int6
         if (rc) return rc;
         rc = fast_launch(t, d_s, d_e, n_r, mode, o, f, stats, s);
         if (!rc) rc = read_status(f.st, s, h);
-        CK(cudaFreeAsync(f.blk, s));
+        CK(dfree(f.blk, s));
         if (rc) return rc;
         if ((long long)h->cand_count <= f.cap) return RS_OK;
         cap = (long long)h->cand_count;  // collision buffer overflow: re-launch once, sized
@@ -643,7 +673,7 @@ static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int6
     const bool compact = c_ray != nullptr;
     const size_t cs = compact ? compact_scratch_bytes(n_r) : 0;
     char* blk = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
+    CK(dmalloc(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
     RsStatus* st = reinterpret_cast<RsStatus*>(blk);
     CK(cudaMemsetAsync(blk, 0, align256(sizeof(RsStatus)) + cs, s));
     QueryArgs a = make_args(t, d_s, d_e, n_r, max_coll, max_stack, st);
@@ -657,7 +687,7 @@ static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int6
     ev_record(2, s);
     RsStatus h;
     rc = read_status(st, s, &h);
-    CK(cudaFreeAsync(blk, s));
+    CK(dfree(blk, s));
     if (rc) return rc;
     if (n_hits) *n_hits = (int64_t)h.hits;
     if (visits) *visits = (int64_t)h.visits;
@@ -670,7 +700,7 @@ static int binary_query(const rs_tree* t, const float* d_s, const float* d_e, in
     const bool compact = o.c_ray != nullptr;
     char* blk = nullptr;
     const size_t cs = compact ? compact_scratch_bytes(n_r) : 0;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
+    CK(dmalloc(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
     CK(cudaMemsetAsync(blk, 0, align256(sizeof(RsStatus)) + cs, s));
     RsStatus* st = reinterpret_cast<RsStatus*>(blk);
     QueryArgs a = make_args(t, d_s, d_e, n_r, 32, 1 << 30, st);
@@ -685,7 +715,7 @@ static int binary_query(const rs_tree* t, const float* d_s, const float* d_e, in
         return fail(RS_INTERNAL, "no binary kernel variant");
     CK(cudaGetLastError());
     int rc = read_status(st, s, h);
-    CK(cudaFreeAsync(blk, s));
+    CK(dfree(blk, s));
     return rc;
 }
 
@@ -717,7 +747,7 @@ int rs_query_stats(const rs_tree* t, const float* d_starts, const float* d_ends,
     cudaStream_t s = S(stream);
     // outputs go to a scratch block: stats runs are diagnostics
     char* blk = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(28ull * (n_r > 0 ? n_r : 1)), s));
+    CK(dmalloc(reinterpret_cast<void**>(&blk), align256(28ull * (n_r > 0 ? n_r : 1)), s));
     int32_t* i0 = reinterpret_cast<int32_t*>(blk);
     float* f1 = reinterpret_cast<float*>(blk + 8ull * n_r);
     float* f3 = reinterpret_cast<float*>(blk + 16ull * n_r);
@@ -725,7 +755,7 @@ int rs_query_stats(const rs_tree* t, const float* d_starts, const float* d_ends,
     int64_t bad;
     int rc = query_impl(t, d_starts, d_ends, n_r, mode, max_coll, max_stack, ref, i0, i0, i2, f1,
                         f3, nullptr, nullptr, nullptr, nullptr, nullptr, &bad, true, visits, mts, s);
-    cudaFreeAsync(blk, s);
+    dfree(blk, s);
     return rc;
 }
 
@@ -736,11 +766,11 @@ int rs_sort_segments(const float* d_starts, const float* d_ends, int64_t n, floa
     if (!(d_starts && d_ends && d_out_starts && d_out_ends && d_perm)) return fail(RS_INVALID_ARG, "null pointer");
     cudaStream_t s = S(stream);
     char* blk = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), sort_segments_scratch_bytes((int)n), s));
+    CK(dmalloc(reinterpret_cast<void**>(&blk), sort_segments_scratch_bytes((int)n), s));
     launch_sort_segments(d_starts, d_ends, (int)n, d_out_starts, d_out_ends,
                          reinterpret_cast<long long*>(d_perm), blk, s);
     CK(cudaGetLastError());
-    CK(cudaFreeAsync(blk, s));
+    CK(dfree(blk, s));
     return RS_OK;
 }
 
@@ -849,7 +879,7 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
         g_hot_mark_mask = 3;
         count_launches(1);
         k_merge_status<<<1, 1, 0, s>>>(f.st, f2.st);
-        CK(cudaFreeAsync(f2.blk, s));
+        CK(dfree(f2.blk, s));
     }
     *tree_out = t;
     return rc;
@@ -870,7 +900,7 @@ static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d
                                      s, &t);
         RsStatus h{};
         if (!rc) rc = read_status(f.st, s, &h);
-        if (f.blk) cudaFreeAsync(f.blk, s);
+        if (f.blk) dfree(f.blk, s);
         if (!rc && h.internal) rc = binary_query(t, d_starts, d_ends, n_r, mode, o, &h, s);
         if (!rc) {
             if (n_hits) *n_hits = (int64_t)h.hits;
@@ -944,7 +974,7 @@ static int enqueue_device_batch_body(const float* d_verts, int64_t n_v, const in
         rc = status_out(h_status, f.st, s);
         if (rc) return rc;
         stage_mark(9, s);
-        CK(cudaFreeAsync(f.blk, s));
+        CK(dfree(f.blk, s));
         rc = rs_free(t, s);
         stage_mark(10, s);
         return rc;
@@ -963,12 +993,12 @@ static int enqueue_device_batch_body(const float* d_verts, int64_t n_v, const in
         if (rc) return rc;
         rc = status_out(h_status, f.st, s);
         if (rc) return rc;
-        CK(cudaFreeAsync(f.blk, s));
+        CK(dfree(f.blk, s));
     } else {
         const bool compact = mode == kBarycentric;
         const size_t cs = compact ? compact_scratch_bytes(n_r) : 0;
         char* blk = nullptr;
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
+        CK(dmalloc(reinterpret_cast<void**>(&blk), align256(sizeof(RsStatus)) + cs + 256, s));
         CK(cudaMemsetAsync(blk, 0, align256(sizeof(RsStatus)) + cs, s));
         RsStatus* st = reinterpret_cast<RsStatus*>(blk);
         const int ref = tree_kind == kTreeReference;
@@ -982,7 +1012,7 @@ static int enqueue_device_batch_body(const float* d_verts, int64_t n_v, const in
         ev_record(2, s);
         rc = status_out(h_status, st, s);
         if (rc) return rc;
-        CK(cudaFreeAsync(blk, s));
+        CK(dfree(blk, s));
     }
     return rs_free(t, s);
 }
@@ -1011,6 +1041,7 @@ struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     RsStatus* h_status = nullptr;  // pinned, mapped
     RsStatus* d_status = nullptr;  // its device alias
+    char* arena = nullptr;         // the graph's scratch (see Arena)
     unsigned long long stamp = 0;
     long long kernels = 0;         // kernel nodes in the graph (for rs_kernel_launches)
 };
@@ -1020,6 +1051,10 @@ static std::mutex g_graph_mu;
 static std::map<GraphKey, GraphEntry> g_graphs;
 static std::set<GraphKey> g_seen;  // argument sets called once (captured on the next call)
 static unsigned long long g_graph_clock = 0;
+static const bool g_use_arena = [] {  // RS_GRAPH_ARENA=0: allocation nodes in the graph (A/B)
+    const char* e = getenv("RS_GRAPH_ARENA");
+    return !(e && e[0] == '0');
+}();
 static const bool g_use_graphs = [] {
     const char* e = getenv("RS_NO_GRAPH");
     return !(e && e[0] == '1');
@@ -1083,15 +1118,35 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
             if (!cap) CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
             cudaGraph_t g = nullptr;
             const long long k0 = rs::g_launches.load();
-            CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-            const int erc = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
-                                                 tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
-                                                 d_tri, d_pt, StatusDst{e.h_status, e.d_status}, cap);
-            const cudaError_t ce = cudaStreamEndCapture(cap, &g);
+            auto capture_once = [&](cudaGraph_t* out) -> int {
+                CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+                const int r = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
+                                                   tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
+                                                   d_tri, d_pt, StatusDst{e.h_status, e.d_status}, cap);
+                const cudaError_t ce = cudaStreamEndCapture(cap, out);
+                return r != RS_OK ? r : (ce == cudaSuccess && *out ? RS_OK : RS_CUDA_ERROR);
+            };
+            // pass 1 sizes the arena (its graph is discarded), pass 2 captures from it
+            g_arena = Arena{nullptr, 0, 0, 1};
+            int erc = capture_once(&g);
+            const size_t arena_bytes = g_arena.off;
+            g_arena = Arena{};
+            if (g) cudaGraphDestroy(g);
+            g = nullptr;
+            rs::g_launches.store(k0);
+            if (erc == RS_OK && g_use_arena &&
+                cudaMalloc(reinterpret_cast<void**>(&e.arena), arena_bytes) == cudaSuccess) {
+                g_arena = Arena{e.arena, arena_bytes, 0, 2};
+                erc = capture_once(&g);
+                g_arena = Arena{};
+            } else if (erc == RS_OK) {
+                cudaGetLastError();
+                e.arena = nullptr;
+                erc = capture_once(&g);  // stream-ordered allocation nodes instead
+            }
             e.kernels = rs::g_launches.load() - k0;
             rs::g_launches.fetch_sub(e.kernels);  // counted when replayed
-            if (erc == RS_OK && ce == cudaSuccess && g &&
-                cudaGraphInstantiate(&e.exec, g, 0) == cudaSuccess) {
+            if (erc == RS_OK && g && cudaGraphInstantiate(&e.exec, g, 0) == cudaSuccess) {
                 std::lock_guard<std::mutex> lk(g_graph_mu);
                 if (g_graphs.size() >= 8) {  // bounded cache: evict the least recently used
                     auto victim = g_graphs.begin();
@@ -1099,12 +1154,14 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
                         if (it->second.stamp < victim->second.stamp) victim = it;
                     cudaGraphExecDestroy(victim->second.exec);
                     cudaFreeHost(victim->second.h_status);
+                    if (victim->second.arena) cudaFree(victim->second.arena);
                     g_graphs.erase(victim);
                 }
                 ge = &(g_graphs[key] = e);
             } else {
                 cudaGetLastError();
                 cudaFreeHost(e.h_status);
+                if (e.arena) cudaFree(e.arena);
             }
             if (g) cudaGraphDestroy(g);
         }
@@ -1310,7 +1367,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     const size_t tiles_b = align256(compact_scratch_bytes(chunk_rays)) * (size_t)nchunks;
     const size_t st_b = align256(sizeof(RsStatus) * (size_t)nchunks);
     char* blk = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&blk), mesh_b + in_b + out_b + tiles_b + st_b, s));
+    CK(dmalloc(reinterpret_cast<void**>(&blk), mesh_b + in_b + out_b + tiles_b + st_b, s));
     Carver c{blk};
     float* dV = c.take<float>(3ull * n_v);
     int* dT = c.take<int>(3ull * n_t);
@@ -1352,7 +1409,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     rs_tree* t = nullptr;
     rc = build_impl(dV, n_v, dT, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
     if (rc) {
-        cudaFreeAsync(blk, s);
+        dfree(blk, s);
         return rc;
     }
     const int ref = tree_kind == kTreeReference;
@@ -1429,7 +1486,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
             }
             if (launch_query(a, mode, ref != 0, bary, kstack_for(ref != 0, max_stack), false, s)) {
                 rs_free(t, stream);
-                cudaFreeAsync(blk, s);
+                dfree(blk, s);
                 return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
             }
             CK(cudaGetLastError());
@@ -1454,7 +1511,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     CK(cudaMemcpyAsync(hst, st, sizeof(RsStatus) * nchunks, cudaMemcpyDeviceToHost, cp));
     CK(cudaStreamSynchronize(cp));
     if (fast) {
-        for (int b = 0; b < 2; ++b) CK(cudaFreeAsync(fs[b].blk, s));
+        for (int b = 0; b < 2; ++b) CK(dfree(fs[b].blk, s));
         // collision-buffer overflow in a chunk: redo that chunk with a buffer
         // sized to what its traversal claimed
         for (int64_t k = 0; k < nchunks; ++k) {
@@ -1504,7 +1561,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     }
     delete[] hst;
     rs_free(t, stream);
-    CK(cudaFreeAsync(blk, s));
+    CK(dfree(blk, s));
     CK(cudaStreamSynchronize(s));
     if (n_hits) *n_hits = (int64_t)running;
     RsStatus agg{};
