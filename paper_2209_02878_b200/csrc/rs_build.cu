@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     float blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
     float tsz[3] = {0.f, 0.f, 0.f};
+    float parea = 0.f;  // depth complexity numerator (tile sizing only; order-free use)
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         // _reset_tree (lbvh.py:181-189) for internal slot j; a lean build
         // (query-only tree, never downloaded) keeps just the visit counters
@@ -56,6 +57,7 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
         }
         ta.visit[j] = 0;
         const int ia = T[3ll * j], ib = T[3ll * j + 1], ic = T[3ll * j + 2];
+        float dside[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const float fa = V[3ll * ia + k], fb = V[3ll * ib + k], fc = V[3ll * ic + k];
@@ -63,6 +65,7 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
             blo[k] = fminf(blo[k], tl);  // root box = union of triangle boxes
             bhi[k] = fmaxf(bhi[k], th);
             tsz[k] = fmaxf(tsz[k], th - tl);
+            dside[k] = th - tl;
             if (do_centroids) {
                 const double m = __ddiv_rn(__dadd_rn(__dadd_rn((double)fa, (double)fb), (double)fc), 3.0);
                 cent[3ll * j + k] = m;
@@ -70,8 +73,12 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
                 hi[k] = fmax(hi[k], m);
             }
         }
+        parea += dside[0] * dside[1] + dside[1] * dside[2] + dside[2] * dside[0];
     }
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int o = 16; o; o >>= 1) parea += __shfl_xor_sync(0xffffffffu, parea, o);
+    __shared__ float pred[32];
+    if (l == 0) pred[w] = parea;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         lo[k] = warp_min(lo[k]);
@@ -95,6 +102,11 @@ __global__ void __launch_bounds__(256) k_prep(const float* __restrict__ V,
         float v = 0.f;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) v = fmaxf(v, sred[i][threadIdx.x]);
         if (v > 0.f) atomicMax(&hdr->tsize[threadIdx.x], __float_as_uint(v));
+    }
+    if (threadIdx.x == 32) {  // one float atomic per CTA (tile sizing only: order-free)
+        float v = 0.f;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) v += pred[i];
+        if (v > 0.f) atomicAdd(&hdr->parea, v);
     }
     if (threadIdx.x < 6) {
         const int k = threadIdx.x;

@@ -59,6 +59,7 @@ struct RsHeader {
     unsigned bmin[3];            // ~ordered32(min triangle-box coordinate) = root box
     unsigned bmax[3];            //  ordered32(max triangle-box coordinate)
     unsigned tsize[3];           // largest triangle-box side per axis (f32 bits, >= 0)
+    float parea;                 // sum over triangles of the box's three projected face areas
 };
 
 // Per-query device status (zeroed before a query).

@@ -169,6 +169,7 @@ struct SortedArgs {
     unsigned bin_occupancy;  // binning: target live segments per bin (set at launch)
     int rec_ids;             // rec holds 4-B segment ids instead of 32-B records (set at launch)
     unsigned tile_area;  // tile traversal: target triangles' worth of records per tile (set at launch)
+    unsigned tile_depth; // tile traversal: records per tile <= tile_depth / depth complexity (0: off)
     // Morton-range candidate lists (fast lean trees; codes == nullptr disables)
     const unsigned long long* codes;         // sorted 30-bit keys, leaf order
     const unsigned long long* code_samples;  // codes[k * sample_stride]

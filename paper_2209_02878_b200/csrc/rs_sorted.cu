@@ -1393,6 +1393,21 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
     const unsigned per = a.tile_balance * gridDim.x;
     const unsigned bal = (n_live + per - 1) / per;
     T = T < bal ? T : bal;
+    if (a.tile_depth) {
+        // stacked surfaces: the candidate lists grow with the depth
+        // complexity (projected triangle-box area over the root box's), so
+        // the tile shrinks with it
+        float r[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            r[k] = from_ord32(__ldg(&a.hdr->bmax[k])) - from_ord32(~__ldg(&a.hdr->bmin[k]));
+        const float ra = r[0] * r[1] + r[1] * r[2] + r[2] * r[0];
+        const float depth = ra > 0.f ? __ldg(&a.hdr->parea) / ra : 0.f;
+        if (depth > 1.f) {
+            const float cap = (float)a.tile_depth / depth;
+            T = (float)T < cap ? T : (unsigned)cap;
+        }
+    }
     T = (T + kTileThreads - 1) / kTileThreads * kTileThreads;
     T = T < kTileThreads ? kTileThreads : (T > 16384 ? 16384 : T);
     const unsigned n_tiles = (n_live + T - 1) / T;
@@ -1977,6 +1992,7 @@ struct SortedOpts {
     unsigned tile_density = 16;  // auto: tiles when segments >= this x triangles
     unsigned tile_balance = 8;   // at least this many tiles per CTA
     unsigned tile_area = 48;     // about this many triangles' worth of records per tile
+    unsigned tile_depth = 4900;  // and at most this / depth-complexity records (0: off)
     unsigned bin_occ = 16;       // target live segments per spatial bin
     int bin_tma = 1;             // binning passes stream through TMA bulk copies
     int tile_wide = 0;           // tile walk over the collapsed 4-wide nodes (A/B: no gain on C2)
@@ -2002,6 +2018,7 @@ static SortedOpts& opts() {
         d.tile_density = (unsigned)num("RS_TILE_DENSITY", d.tile_density);
         d.tile_balance = (unsigned)num("RS_TILE_BALANCE", d.tile_balance);
         d.tile_area = (unsigned)num("RS_TILE_AREA", d.tile_area);
+        d.tile_depth = (unsigned)num("RS_TILE_DEPTH", d.tile_depth);
         d.bin_occ = (unsigned)num("RS_BIN_OCC", d.bin_occ);
         d.bin_tma = (int)num("RS_BIN_TMA", d.bin_tma);
         d.tile_wide = (int)num("RS_TILE_WIDE", d.tile_wide);
@@ -2024,6 +2041,7 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "tile_density")) { prev = o.tile_density; if (value >= 0) o.tile_density = (unsigned)value; }
     else if (!strcmp(name, "tile_balance")) { prev = o.tile_balance; if (value > 0) o.tile_balance = (unsigned)value; }
     else if (!strcmp(name, "tile_area")) { prev = o.tile_area; if (value > 0) o.tile_area = (unsigned)value; }
+    else if (!strcmp(name, "tile_depth")) { prev = o.tile_depth; if (value >= 0) o.tile_depth = (unsigned)value; }
     else if (!strcmp(name, "bin_occupancy")) { prev = o.bin_occ; if (value > 0) o.bin_occ = (unsigned)value; }
     else if (!strcmp(name, "bin_tma")) { prev = o.bin_tma; if (value >= 0) o.bin_tma = (int)value; }
     else if (!strcmp(name, "tile_wide")) { prev = o.tile_wide; if (value >= 0) o.tile_wide = (int)value; }
@@ -2145,6 +2163,7 @@ void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t
     if (a0.n_r <= 0) return;
     SortedArgs a = a0;
     a.tile_area = tile_area();
+    a.tile_depth = opts().tile_depth;
     a.rec_ids = opts().rec_ids;
     a.range_max = opts().range_max;
     if (!a.range_max) a.codes = nullptr;

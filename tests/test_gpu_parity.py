@@ -185,7 +185,9 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"range_max": 0},                               # candidate lists from the walk only
     {"range_max": 1 << 30},                         # candidate lists from key ranges only
     {"geom": 1},                                    # bin geometry derived once by the sample kernel
-], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall", "walkonly", "rangeonly", "geom"])
+    {"tile_depth": 1, "tile_balance": 1},           # depth-complexity cap: one-CTA-size tiles
+    {"tile_depth": 0, "tile_balance": 1},           # no depth cap
+], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall", "walkonly", "rangeonly", "geom", "depth1", "depth0"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
 def test_tile_knobs_bitwise(name, mode, knobs):
