@@ -57,7 +57,7 @@ for w in $WHAT; do
         tag=$(echo "$ev" | tr ',=/' '_-_')
         env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps ${RS_AB_STEPS:-100} > "$OUT/ab_${c}_${tag}_$rep.json" 2>> "$OUT/bench.err"
       done; done; done;;
-    bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps 10 > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
+    bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps ${RS_ALL_STEPS:-10} > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_bench.log" 2>&1
