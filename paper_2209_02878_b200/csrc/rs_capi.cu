@@ -1301,11 +1301,11 @@ static void timing_join(cudaStream_t s) {
 
 extern "C" {
 
-int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, int64_t n_t,
-                      const float* h_starts, const float* h_ends, int64_t n_r, int mode,
-                      int tree_kind, int max_coll, int max_stack, int64_t chunk_rays,
-                      int32_t* h_flags, int32_t* h_ray, float* h_dist, int32_t* h_tri,
-                      float* h_pt, int64_t* n_hits, int64_t* bad, void* stream) {
+static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t* h_tris, int64_t n_t,
+                               const float* h_starts, const float* h_ends, int64_t n_r, int mode,
+                               int tree_kind, int max_coll, int max_stack, int64_t chunk_rays,
+                               int32_t* h_flags, int32_t* h_ray, float* h_dist, int32_t* h_tri,
+                               float* h_pt, int64_t* n_hits, int64_t* bad, void* stream) {
     int rc = check_query(mode, max_coll, max_stack);
     if (rc) return rc;
     if (bad) *bad = -1;
@@ -1568,6 +1568,19 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
     agg.bad = badv;
     agg.internal = internal;
     return status_code(agg, bad);
+}
+
+int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, int64_t n_t,
+                      const float* h_starts, const float* h_ends, int64_t n_r, int mode,
+                      int tree_kind, int max_coll, int max_stack, int64_t chunk_rays,
+                      int32_t* h_flags, int32_t* h_ray, float* h_dist, int32_t* h_tri,
+                      float* h_pt, int64_t* n_hits, int64_t* bad, void* stream) {
+    rs::set_batch_rays(n_r);  // chunks choose their traversal by the whole batch's density
+    const int rc = run_batch_host_impl(h_verts, n_v, h_tris, n_t, h_starts, h_ends, n_r, mode, tree_kind,
+                                       max_coll, max_stack, chunk_rays, h_flags, h_ray, h_dist, h_tri,
+                                       h_pt, n_hits, bad, stream);
+    rs::set_batch_rays(0);
+    return rc;
 }
 
 }  // extern "C"

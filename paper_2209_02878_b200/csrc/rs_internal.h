@@ -194,6 +194,8 @@ void launch_binning(const SortedArgs& a, cudaStream_t s, bool zero_flags = false
 // histogram pass (TMA path, 16-B aligned rows and flags)
 bool binning_zeroes_flags(const float* starts, const float* ends, long long n_r, const int* flags);
 void launch_sorted_trav(const SortedArgs& a, int mode, bool stats, cudaStream_t s);
+// the whole batch's segment count while its chunks are traversed (0: none)
+void set_batch_rays(long long n);
 // Tuning knob by name (trav, tile_density, tile_balance, tile_area,
 // bin_occupancy); value < 0 (or 0 for counts) only reads.  -1: unknown name.
 int sorted_option(const char* name, long long value, long long* old);

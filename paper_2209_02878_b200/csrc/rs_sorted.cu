@@ -2159,6 +2159,9 @@ static void launch_wtile(const SortedArgs& a, int sms, cudaStream_t s) {
 static const char* g_hot_name = "";
 const char* hot_kernel_name() { return g_hot_name; }
 
+static thread_local long long g_batch_rays = 0;
+void set_batch_rays(long long n) { g_batch_rays = n; }
+
 void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t s) {
     if (a0.n_r <= 0) return;
     SortedArgs a = a0;
@@ -2175,8 +2178,12 @@ void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t
     int variant = trav_variant();
     // tiles pay off only with many segments per triangle (a tile's walk is
     // amortised over its records); a single triangle has no tree to walk
+    // (a chunk of a streamed batch decides by the whole batch's density: the
+    // same scene must not switch to the per-record walk because it arrives
+    // in pieces)
+    const long long n_density = a.n_r > g_batch_rays ? a.n_r : g_batch_rays;
     if (variant == 0)
-        variant = a.n_r < (long long)a.tile_min_density * (a.n_int + 1) ? 1 : opts().auto_tile;
+        variant = n_density < (long long)a.tile_min_density * (a.n_int + 1) ? 1 : opts().auto_tile;
     if (a.n_int == 0) variant = 1;
     hot_kernel_mark(0, s);
     g_hot_name = variant == 5 ? "k_trav_ptile" : variant == 4 ? "k_trav_wtile" : variant == 3 ? "k_trav_tile"
