@@ -555,3 +555,16 @@ def test_outputs_over_garbage_buffers(n_seg, geom):
                 r = run_device(mesh, batch, rs.EngineConfig(mode=mode), "fast", out=out)
                 got = _np(r.crossing if mode == "boolean" else r.counts)
                 assert np.array_equal(got, truth), (mode, n_seg, geom)
+
+
+def test_chunked_host_batch_keeps_the_batch_traversal():
+    """A host batch streamed in chunks picks its traversal kernel by the whole
+    batch's segments per triangle: 2M segments over 80k triangles (25 per
+    triangle) take the tile kernel even though each 500k chunk alone is
+    below the tile threshold (16 per triangle); results stay exact."""
+    sc = rs.generate_scene(80_000, 2_000_000, 0.5, seed=11)
+    truth = sc.expected_crossings.astype(np.int32)
+    for mode in ("boolean", "count"):
+        r = rs.run_batch(sc.mesh, sc.segments, rs.EngineConfig(mode=mode))
+        assert _lib.lib().rs_hot_kernel().decode() == "k_trav_tile"
+        assert np.array_equal(_np(r.crossing if mode == "boolean" else r.counts), truth), mode
