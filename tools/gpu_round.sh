@@ -57,6 +57,10 @@ for w in $WHAT; do
         tag=$(echo "$ev" | tr ',=/' '_-_')
         env $(echo "$ev" | tr ',' ' ') timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e --steps ${RS_AB_STEPS:-100} > "$OUT/ab_${c}_${tag}_$rep.json" 2>> "$OUT/bench.err"
       done; done; done;;
+    sanitize) for tool in memcheck synccheck racecheck; do
+        arg=""; [ $tool = racecheck ] && arg=small
+        timeout 1200 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize.py $arg > "$OUT/sanitize_$tool.txt" 2>&1
+        echo "rc=$?" >> "$OUT/sanitize_$tool.txt"; done;;
     bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps ${RS_ALL_STEPS:-10} > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -1,0 +1,67 @@
+"""Small workloads for compute-sanitizer (memcheck / racecheck / synccheck).
+
+Every default kernel of the product path runs at least once, on device and
+host inputs, and through a captured graph:
+  build:      k_prep, k_keys, k_sort_hist, k_onesweep, k_climb_lean (fast
+              query-only trees), k_climb (reference / downloadable trees)
+  binning:    k_seg_sample, k_bin_count_tma, k_bin_scan1, k_bin_scatter
+  traversal:  k_trav_tile (dense batch), k_trav_sorted_bin (sparse batch),
+              k_query_dense (reference semantics)
+  output:     k_bary_compact, k_status_out, k_baseline
+Exits non-zero if any result differs from the generator's ground truth.
+
+usage: compute-sanitizer --tool memcheck python tools/sanitize.py [small]
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+
+import paper_2209_02878_b200 as rs
+
+small = len(sys.argv) > 1 and sys.argv[1] == "small"
+
+
+def dev(sc):
+    t = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    return (rs.Mesh.from_arrays(t(sc.mesh.vertices), t(sc.mesh.triangles)),
+            rs.SegmentBatch.from_arrays(t(sc.segments.starts), t(sc.segments.ends)))
+
+
+def check(r, truth, mode, what):
+    if mode == "boolean":
+        got = r.crossing
+    elif mode == "count":
+        got = r.counts
+    else:
+        got = r.ray_index
+        truth = np.nonzero(truth)[0]
+    got = got.cpu().numpy() if hasattr(got, "cpu") else np.asarray(got)
+    assert np.array_equal(got, truth.astype(got.dtype)), what
+
+
+# dense: >= 16 segments per triangle -> k_trav_tile; sparse -> k_trav_sorted_bin
+cases = [(500, 20_000 if small else 60_000, "dense"), (4000, 5000, "sparse")]
+for n_tri, n_seg, tag in cases:
+    sc = rs.generate_scene(n_tri, n_seg, 0.5, seed=3)
+    truth = sc.expected_crossings.astype(np.int32)
+    dm, db = dev(sc)
+    for mode in rs.MODES:
+        for rep in range(3):  # call 2 captures the graph, call 3 replays it
+            check(rs.run_batch(dm, db, rs.EngineConfig(mode=mode)), truth, mode, f"{tag} dev {mode}")
+        check(rs.run_batch(sc.mesh, sc.segments, rs.EngineConfig(mode=mode)), truth, mode, f"{tag} host {mode}")
+        check(rs.run_batch(sc.mesh, sc.segments, rs.EngineConfig(mode=mode, tree="reference")), truth, mode,
+              f"{tag} reference {mode}")
+    from paper_2209_02878_b200._backend import b200
+    b200.DeviceTree(sc.mesh, kind="fast").download()
+    b200.DeviceTree(sc.mesh, kind="reference").download()
+
+sc = rs.generate_scene(300, 3000, 0.5, seed=4)
+truth = sc.expected_crossings.astype(np.int32)
+for mode in rs.MODES:
+    check(rs.run_baseline_allpairs(sc.mesh, sc.segments, rs.EngineConfig(mode=mode)), truth, mode, f"baseline {mode}")
+    check(rs.run_batch(sc.mesh, sc.segments, rs.EngineConfig(mode=mode, sort_rays=True)), truth, mode, f"sort_rays {mode}")
+torch.cuda.synchronize()
+print("sanitize workload ok")
