@@ -152,19 +152,34 @@ RS_API int rs_run_batch_host(const float *h_verts, int64_t n_v, const int32_t *h
                       int32_t *h_triangle_id, float *h_point, int64_t *n_hits,
                       int64_t *bad_segment, void *stream);
 
-/* Device phase timing for rs_run_batch_device (the reference's
- * ResultSet.timings "construct"/"query", engine.py:238-288): when enabled,
- * CUDA events on the caller's stream bracket the build, the whole query and
- * the dominant (traversal) kernel; rs_last_timings returns the last call's
- * milliseconds.  enable = 2 records only the traversal kernel's events (the
- * lightest instrumentation; build/query then read 0).  enable = 3 adds stage
- * marks on both streams of the fast path (diagnostics): rs_stage_times fills
- * ms[k] with the time from the call's start to mark k (-1 when not reached):
- * 0 prep done, 1 keys+sort done, 2 climb done, 4 binning presets done,
- * 5 sample done, 6 histogram done, 7 scan done, 8 scatter done, 9 status copied,
- * 10 frees done, 14 traversal start, 15 traversal end; 11 and 12 are the host
- * milliseconds spent in the graph launch and in the wait. */
+/* Device phase timing (the reference's ResultSet.timings, engine.py:238-288,
+ * measured with CUDA events on the device).  Thread-local level, default 1
+ * (env RS_TIMING overrides): 0 off; 1 the reference's phases plus the
+ * traversal kernel; 2 the traversal kernel only (the lightest: bench.py's
+ * timed region); 3 every stage (diagnostics).  Inside a captured graph the
+ * marks are side-branch nodes, off the kernel chain.
+ *
+ * rs_last_phases fills up to n of, in this order (ms; -1 = phase not run):
+ *   0 "ray boxes"    segment boxes + spatial binning (k_seg_sample ..
+ *                    scatter; runs beside the build on a second stream)
+ *   1 "quantization" centroid quantisation and Morton encoding (k_keys:
+ *   2 "encoding"     one fused kernel, so "encoding" reads 0)
+ *   3 "sorting"      the device radix sort of the keys
+ *   4 "reset"        tree reset fused with triangle boxes, centroids, support (k_prep)
+ *   5 "construct"    the Apetrei climb
+ *   6 "query"        traversal + exact tests + compaction (summed over chunks
+ *                    on the host path)
+ * for the calling thread's last call of rs_build, rs_build_from_sorted,
+ * rs_query*, rs_run_batch_device or rs_run_batch_host.
+ * rs_last_timings gives build (start .. climb done), query and the traversal
+ * kernel alone.  rs_stage_times (level 3) fills ms[k] = time from the call's
+ * start to stage mark k (-1 when not reached): 0 prep done, 1 keys+sort done,
+ * 2 climb done, 4 binning start, 5 sample done, 6 histogram done, 7 scan
+ * done, 8 binning done, 9 status copied, 10 frees done, 13 keys done, 14
+ * traversal start, 15 traversal end; 11 and 12 are the host milliseconds
+ * spent in the graph launch and in the wait. */
 RS_API int rs_set_timing(int enable);
+RS_API int rs_last_phases(float *ms, int n);
 RS_API int rs_last_timings(float *build_ms, float *query_ms, float *hot_kernel_ms);
 RS_API int rs_stage_times(float *ms, int n);
 

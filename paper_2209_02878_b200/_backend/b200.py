@@ -17,7 +17,6 @@ ABI; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
-import time
 
 import numpy as np
 
@@ -157,14 +156,13 @@ class DeviceTree:
 # ---------------------------------------------------------------- protocol --
 
 def build_tree(mesh, sorted_codes, sorted_ids, workers: int = 1):
-    """_compiled.py:27-69: returns (tree, reset_s, construct_s).  Reset and
-    construction are fused on device, so reset_s is reported as 0.0."""
-    torch = _torch()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    """_compiled.py:27-69: returns (tree, reset_s, construct_s), the device
+    times of the reset (k_prep: tree reset fused with the triangle boxes) and
+    of the climb, from CUDA events (rs_last_phases)."""
     dt = DeviceTree(mesh, sorted_codes=sorted_codes, sorted_ids=sorted_ids)
+    ph = _lib.last_phases()  # before download: the build's marks
     tree = dt.download()
-    return tree, 0.0, time.perf_counter() - t0
+    return tree, ph.get("reset", 0.0), ph.get("construct", 0.0)
 
 
 def _device_tree_for(mesh, tree: BvhTree) -> DeviceTree:

@@ -43,6 +43,7 @@ _SIGS = {
                                 p, p, p, p, p, p, p, p]),
     "rs_set_timing": (i32, [i32]),
     "rs_last_timings": (i32, [p, p, p]),
+    "rs_last_phases": (i32, [p, i32]),
     "rs_stage_times": (i32, [p, i32]),
     "rs_kernel_launches": (C.c_longlong, []),
     "rs_last_status": (i32, [p]),
@@ -86,6 +87,20 @@ def option(name: str, value: int):
         yield
     finally:
         lib().rs_set_option(name.encode(), old.value, None)
+
+
+# ResultSet.timings keys filled from device events (engine.py:238-288), in
+# rs_last_phases order; "ray sort" is timed by the engine around its sort.
+PHASES = ("ray boxes", "quantization", "encoding", "sorting", "reset", "construct", "query")
+
+
+def last_phases() -> dict:
+    """Seconds per reference phase of the calling thread's last native call
+    (phases that did not run are absent)."""
+    arr = (C.c_float * len(PHASES))()
+    if lib().rs_last_phases(arr, len(PHASES)) != RS_OK:
+        return {}
+    return {k: arr[i] / 1e3 for i, k in enumerate(PHASES) if arr[i] >= 0}
 
 
 def last_error() -> str:

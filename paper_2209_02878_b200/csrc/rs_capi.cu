@@ -10,6 +10,8 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <tuple>
+#include <memory>
 #include <set>
 #include <vector>
 #include <mutex>
@@ -25,6 +27,54 @@ namespace rs {
 void hot_kernel_mark(int which, cudaStream_t s);
 static std::atomic<long long> g_launches{0};
 void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// Per-device launch facts, safe for concurrent callers and for processes
+// that drive several GPUs: the SM count, occupancy per (kernel, block,
+// dynamic smem) and the max-dynamic-shared-memory opt-in (a per-device,
+// per-function attribute) are cached per device under one mutex.
+static std::mutex g_dev_mu;
+static std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+static std::set<std::pair<int, const void*>> g_smem_attr;
+static std::map<int, int> g_sms;
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+int device_sms() {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 1;
+    g_sms[dev] = sms;
+    return sms;
+}
+
+int occupancy(const void* kernel, int threads, size_t smem) {
+    const auto key = std::make_tuple(current_device(), kernel, threads, smem);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, smem);
+    cudaGetLastError();
+    if (o < 1) o = 1;
+    g_occ[key] = o;
+    return o;
+}
+
+void ensure_dynamic_smem(const void* kernel, int bytes) {
+    const auto key = std::make_pair(current_device(), kernel);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_smem_attr.count(key)) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    g_smem_attr.insert(key);
+}
 }  // namespace rs
 
 struct rs_tree {
@@ -54,34 +104,167 @@ const bool g_binary_fast = [] {
     return e && e[0] == '1';
 }();
 
-// Phase timing (engine.py's timings dict, measured on device): when enabled,
-// events bracket the build and the query kernel on the caller's stream.
-thread_local int g_timing = 0;  // 0 off, 1 phases + hot kernel, 2 hot kernel only, 3 stages
-constexpr int kStageEvents = 16;  // level 3 (diagnostics): stage marks on both streams
-thread_local cudaEvent_t g_ev[5 + kStageEvents] = {};
-thread_local float g_stage_ms[kStageEvents] = {};
-thread_local float g_host_ms[2] = {};
+// ---- device timing marks ---------------------------------------------------
+//
+// The reference fills ResultSet.timings with per-phase seconds
+// (engine.py:238-288: "ray sort", "ray boxes", "quantization", "encoding",
+// "sorting", "reset", "construct", "query").  Here the phases run on the
+// device (two streams), so they are timed with CUDA events: every call
+// records (tag, event) marks in enqueue order, and a phase is the summed
+// elapsed time over its (start tag, next end tag) pairs, which also covers
+// the host pipeline's per-chunk binning and traversal.  Tags: 0 call start,
+// 1/2 query start/end, 3/4 traversal kernel start/end, 5 + k stage k (0 prep
+// done, 1 sort done, 2 climb done, 4 binning start, 8 binning done, 13 keys
+// done, others diagnostic).
+//
+// Levels (rs_set_timing): 0 off, 1 the reference's phases (+ traversal
+// kernel), 2 the traversal kernel only (bench's timed region), 3 every stage.
+// Inside a captured graph each mark hangs off a side branch (forked from
+// its stream, joined only at the graph's end): in the kernel chain every
+// event-record node added ~6 us of latency per call.
+int default_timing() {  // RS_TIMING overrides the default level (1) of a new thread
+    const char* e = getenv("RS_TIMING");
+    return e && e[0] >= '0' && e[0] <= '3' ? e[0] - '0' : 1;
+}
+thread_local int g_timing = default_timing();
+constexpr int kStageEvents = 16;
+constexpr int kTagStage = 5;
+constexpr int kTagCount = kTagStage + kStageEvents;
+struct Mark {
+    int tag;
+    cudaEvent_t ev;
+};
+thread_local std::vector<cudaEvent_t> g_pool;  // timing events, reused across calls
+thread_local size_t g_pool_used = 0;
+thread_local std::vector<Mark> g_marks;        // the current call's marks
+thread_local std::vector<cudaEvent_t> g_fj;    // capture-time fork/join events
+thread_local size_t g_fj_used = 0;
+thread_local std::vector<cudaEvent_t> g_joins;
 thread_local cudaStream_t g_tstream = nullptr;
-thread_local cudaEvent_t g_tfork[2] = {}, g_tjoin[2] = {};
-thread_local int g_tpending = 0;  // bit k: join k outstanding
+thread_local float g_host_ms[2] = {};
 
-thread_local float g_build_ms = 0.f, g_query_ms = 0.f, g_hot_ms = 0.f;
-thread_local bool g_ev_valid = false;
+// the last call's results, computed from its marks (eagerly after a graph
+// replay, whose events belong to the graph; lazily otherwise)
+constexpr int kPhaseCount = 7;  // ray boxes, quantization, encoding, sorting, reset, construct, query
+struct TimingResult {
+    bool valid = false;
+    float phase[kPhaseCount];
+    float build, query, hot;
+    float stage[kStageEvents];
+};
+thread_local TimingResult g_tres;
+thread_local bool g_have_marks = false;
 
 // hot-kernel mark mask: bit 0 records the start event, bit 1 the end event
 // (a batch traversed in two parts marks the first part's start and the
 // second part's end)
 thread_local int g_hot_mark_mask = 3;
 
-void ev_record(int k, cudaStream_t s) {
-    if (!g_timing || (g_timing == 2 && k < 3) || (g_timing != 3 && k >= 5)) return;
-    if (!g_ev[k]) cudaEventCreate(&g_ev[k]);
+bool mark_enabled(int tag) {
+    switch (g_timing) {
+        case 1:
+            return tag <= 4 || tag == kTagStage + 0 || tag == kTagStage + 1 || tag == kTagStage + 2 ||
+                   tag == kTagStage + 4 || tag == kTagStage + 8 || tag == kTagStage + 13;
+        case 2: return tag == 3 || tag == 4;
+        case 3: return true;
+        default: return false;
+    }
+}
+
+cudaEvent_t take_event(std::vector<cudaEvent_t>& pool, size_t& used, unsigned flags) {
+    if (used == pool.size()) {
+        cudaEvent_t e = nullptr;
+        cudaEventCreateWithFlags(&e, flags);
+        pool.push_back(e);
+    }
+    return pool[used++];
+}
+
+// A new top-level call: forget the previous call's marks.
+void marks_reset() {
+    g_pool_used = 0;
+    g_marks.clear();
+    g_tres.valid = false;
+    g_have_marks = false;
+}
+
+void mark(int tag, cudaStream_t s) {
+    if (!mark_enabled(tag)) return;
+    cudaEvent_t ev = take_event(g_pool, g_pool_used, cudaEventDefault);
+    g_marks.push_back({tag, ev});
+    g_have_marks = true;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
-    if (cs == cudaStreamCaptureStatusActive)  // becomes a timing node of the graph
-        cudaEventRecordWithFlags(g_ev[k], s, cudaEventRecordExternal);
-    else
-        cudaEventRecord(g_ev[k], s);
+    if (cs != cudaStreamCaptureStatusActive) {
+        cudaEventRecord(ev, s);
+        return;
+    }
+    if (!g_tstream) cudaStreamCreateWithFlags(&g_tstream, cudaStreamNonBlocking);
+    cudaEvent_t fork = take_event(g_fj, g_fj_used, cudaEventDisableTiming);
+    cudaEvent_t join = take_event(g_fj, g_fj_used, cudaEventDisableTiming);
+    cudaEventRecord(fork, s);
+    cudaStreamWaitEvent(g_tstream, fork, 0);
+    cudaEventRecordWithFlags(ev, g_tstream, cudaEventRecordExternal);  // a timing node of the graph
+    cudaEventRecord(join, g_tstream);
+    g_joins.push_back(join);
+}
+
+void ev_record(int k, cudaStream_t s) { mark(k, s); }
+
+// joins the side branches back into s (before a capture ends)
+void timing_join(cudaStream_t s) {
+    for (cudaEvent_t j : g_joins) cudaStreamWaitEvent(s, j, 0);
+    g_joins.clear();
+    g_fj_used = 0;
+}
+
+// Summed elapsed ms over (a, next b) pairs of `m`; -1 when no pair exists.
+float pair_sum(const std::vector<Mark>& m, int a, int b) {
+    float total = 0.f;
+    bool any = false;
+    for (size_t i = 0; i < m.size(); ++i) {
+        if (m[i].tag != a) continue;
+        for (size_t j = i + 1; j < m.size(); ++j) {
+            if (m[j].tag != b) continue;
+            float ms = 0.f;
+            cudaEventSynchronize(m[j].ev);
+            if (cudaEventElapsedTime(&ms, m[i].ev, m[j].ev) == cudaSuccess) {
+                total += ms;
+                any = true;
+            }
+            break;
+        }
+    }
+    cudaGetLastError();
+    return any ? total : -1.f;
+}
+
+TimingResult compute_timings(const std::vector<Mark>& m) {
+    TimingResult r;
+    const int S = kTagStage;
+    r.phase[0] = pair_sum(m, S + 4, S + 8);   // ray boxes: segment boxes + spatial binning
+    r.phase[1] = pair_sum(m, S + 0, S + 13);  // quantization (+ encoding, one fused kernel)
+    r.phase[2] = r.phase[1] >= 0.f ? 0.f : -1.f;
+    r.phase[3] = pair_sum(m, S + 13, S + 1);  // sorting
+    r.phase[4] = pair_sum(m, 0, S + 0);       // reset (+ triangle boxes, centroids, support)
+    r.phase[5] = pair_sum(m, S + 1, S + 2);   // construct (climb)
+    if (r.phase[5] < 0.f) r.phase[5] = pair_sum(m, S + 0, S + 2);  // from caller-sorted keys
+    r.phase[6] = pair_sum(m, 1, 2);           // query (traversal + compaction)
+    r.build = pair_sum(m, 0, S + 2);
+    r.query = r.phase[6];
+    r.hot = pair_sum(m, 3, 4);
+    for (int k = 0; k < kStageEvents; ++k) r.stage[k] = pair_sum(m, 0, S + k);
+    r.stage[11] = g_host_ms[0];
+    r.stage[12] = g_host_ms[1];
+    r.stage[14] = pair_sum(m, 0, 3);
+    r.stage[15] = pair_sum(m, 0, 4);
+    r.valid = true;
+    return r;
+}
+
+const TimingResult* last_timings() {
+    if (!g_tres.valid && g_have_marks) g_tres = compute_timings(g_marks);
+    return g_tres.valid ? &g_tres : nullptr;
 }
 
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
@@ -153,17 +336,19 @@ void carve_tree(rs_tree* t) {
     t->nodes4 = c.take<RsNode4>(n > 1 ? n - 1 : 1);
 }
 
-bool g_pool_configured = false;
+std::mutex g_pool_mu;
+std::set<int> g_pool_configured;  // devices whose default pool keeps freed blocks
 
 int configure_pool() {
-    if (g_pool_configured) return RS_OK;
     int dev = 0;
     CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (g_pool_configured.count(dev)) return RS_OK;
     cudaMemPool_t pool;
     CK(cudaDeviceGetDefaultMemPool(&pool, dev));
     unsigned long long thr = ~0ull;  // keep freed blocks cached in the pool
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    g_pool_configured = true;
+    g_pool_configured.insert(dev);
     return RS_OK;
 }
 
@@ -223,12 +408,10 @@ int alloc_tree(int64_t n, int kind, cudaStream_t s, rs_tree** out) {
     return RS_OK;
 }
 
-// nodes4 (the 4-wide collapse) is read only by the A/B traversal variants
+// nodes4 (the 4-wide collapse) is read by the collision-buffer path and the
+// A/B traversal variants
 bool need_nodes4() {
-    static const bool buffer = [] {
-        const char* e = getenv("RS_FAST_PATH");
-        return e && e[0] == 'b';
-    }();
+    const bool buffer = rs::fast_path() == 1;
     long long trav = 0, wide = 0;
     rs::sorted_option("trav", -1, &trav);
     rs::sorted_option("tile_wide", -1, &wide);
@@ -266,8 +449,10 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
     CK(cudaMemsetAsync(t->hdr, 0, sizeof(RsHeader), s));
     if (sorted_codes) {
         launch_prep(V, T, n, nullptr, t->hdr, t->ta, false, s);
+        stage_mark(0, s);
         launch_climb(V, T, n, reinterpret_cast<const unsigned long long*>(sorted_codes),
                      sorted_ids, t->ta, t->nodes, t->leaves, t->hdr, s);
+        stage_mark(2, s);
     } else {
         const int passes = kind == kTreeFast ? 4 : 8;  // 30-bit vs 63-bit keys
         const size_t sb = sort_scratch_bytes(n, passes);
@@ -294,6 +479,7 @@ int build_impl(const float* V, int64_t n_v, const int* T, int64_t n_t, int kind,
         }
         stage_mark(0, s);
         launch_keys(cent, n, t->hdr, kind, keys, vals, s);
+        stage_mark(13, s);
         launch_sort(keys, vals, keys2, vals2, n, passes, sort_scratch, s);
         stage_mark(1, s);
         if (lean) launch_climb_lean(V, T, n, keys, vals, t->ta.visit, t->nodes, t->leaves, t->hdr,
@@ -399,14 +585,18 @@ const char* rs_last_error(void) { return g_err.c_str(); }
 
 int rs_build(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
              int tree_kind, void* stream, rs_tree** out) {
+    marks_reset();
     if (!out) return fail(RS_INVALID_ARG, "null output handle");
+    mark(0, S(stream));
     return build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, S(stream), out);
 }
 
 int rs_build_from_sorted(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
                          const uint64_t* d_sorted_codes, const int32_t* d_sorted_ids,
                          void* stream, rs_tree** out) {
+    marks_reset();
     if (!out || !d_sorted_codes || !d_sorted_ids) return fail(RS_INVALID_ARG, "null argument");
+    mark(0, S(stream));
     return build_impl(d_verts, n_v, d_tris, n_t, kTreeReference, d_sorted_codes, d_sorted_ids,
                       S(stream), out);
 }
@@ -482,15 +672,13 @@ struct FastScratch {
     void* geom = nullptr;
 };
 
-// RS_FAST_PATH=buffer: pair traversal -> collision buffer -> exact pass
-// (A/B tuning); default: coherent sorted traversal.
-static const bool g_buffer_path = [] {
-    const char* e = getenv("RS_FAST_PATH");
-    return e && e[0] == 'b';
-}();
+// fast_path option 1 (or RS_FAST_PATH=buffer): pair traversal -> collision
+// buffer -> exact pass; default 0: the binned tile traversal.
+static bool buffer_path() { return rs::fast_path() == 1; }
 
 static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cudaStream_t s) {
-    if (!g_buffer_path) cap = kCandChunk;  // the sorted path has no collision buffer
+    if (!buffer_path()) cap = kCandChunk;  // the sorted path has no collision buffer
+    else if (rs::cand_cap_override() > 0) cap = rs::cand_cap_override();
     cap = ((cap + kCandChunk - 1) / kCandChunk) * kCandChunk;
     const bool bary = mode == kBarycentric;
     size_t total = 256;
@@ -499,7 +687,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     if (bary)
         total += align256(8ull * n_r) + align256(4ull * n_r) + align256(8ull * cap) +
                  align256(bary_compact_scratch(n_r));
-    if (g_buffer_path) total += align256(4 * trav_gstack_ints());
+    if (buffer_path()) total += align256(4 * trav_gstack_ints());
     total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r) +
              align256(8ull * n_r) + align256(bin_geom_bytes());
     CK(dmalloc(reinterpret_cast<void**>(&f.blk), total, s));
@@ -515,7 +703,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         f.tile_ctr = f.tiles + (bary_compact_scratch(n_r) / 8 - 1);
         f.tiles_bytes = bary_compact_scratch(n_r);
     }
-    if (g_buffer_path) f.gstack = c.take<int>(trav_gstack_ints());
+    if (buffer_path()) f.gstack = c.take<int>(trav_gstack_ints());
     f.bins = c.take<unsigned>(2 * sorted_bins());  // counters + look-back words (zeroed together)
     f.cursor = c.take<unsigned>(sorted_bins());
     f.n_live = c.take<unsigned>(64 + 4 * 32);
@@ -590,7 +778,7 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
 static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r, int mode,
                        const FastOut& o, FastScratch& f, bool stats, cudaStream_t s) {
     const bool bary = mode == kBarycentric;
-    if (!g_buffer_path) {
+    if (!buffer_path()) {
         int rc = fast_bin(t, d_s, d_e, n_r, mode, o, f, s);
         if (rc) return rc;
         return fast_trav(t, d_s, d_e, n_r, mode, o, f, stats, s);
@@ -607,7 +795,7 @@ static int fast_launch(const rs_tree* t, const float* d_s, const float* d_e, int
                 f.st, f.gstack};
     launch_trav(ta, stats, s);
     ExactArgs ea{f.cand, &f.st->cand_count, f.cap, f.chunk_fill, d_s, d_e, t->leaves,
-                 o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts};
+                 o.flags, f.best_t, f.best_tri, f.cand_t, &f.st->mts, &f.st->dropped};
     launch_exact(ea, mode, stats, s);
     if (bary) {
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
@@ -722,6 +910,7 @@ static int binary_query(const rs_tree* t, const float* d_s, const float* d_e, in
 int rs_query(const rs_tree* t, const float* d_starts, const float* d_ends, int64_t n_r, int mode,
              int max_coll, int max_stack, int ref, int32_t* d_detected, int32_t* d_counts,
              int32_t* d_tri, float* d_dist, float* d_points, int64_t* bad, void* stream) {
+    marks_reset();
     if (mode == kBoolean && !d_detected) return fail(RS_INVALID_ARG, "boolean needs d_detected");
     if (mode == kCount && !d_counts) return fail(RS_INVALID_ARG, "count needs d_counts");
     if (mode == kBarycentric && !(d_detected && d_tri && d_dist && d_points))
@@ -734,6 +923,7 @@ int rs_query(const rs_tree* t, const float* d_starts, const float* d_ends, int64
 int rs_query_compact(const rs_tree* t, const float* d_starts, const float* d_ends, int64_t n_r,
                      int max_coll, int max_stack, int ref, int32_t* d_ray, float* d_dist,
                      int32_t* d_tri, float* d_pt, int64_t* n_hits, int64_t* bad, void* stream) {
+    marks_reset();
     if (!(d_ray && d_dist && d_tri && d_pt)) return fail(RS_INVALID_ARG, "null output");
     if (n_hits) *n_hits = 0;
     return query_impl(t, d_starts, d_ends, n_r, kBarycentric, max_coll, max_stack, ref, nullptr,
@@ -744,6 +934,7 @@ int rs_query_compact(const rs_tree* t, const float* d_starts, const float* d_end
 int rs_query_stats(const rs_tree* t, const float* d_starts, const float* d_ends, int64_t n_r,
                    int mode, int max_coll, int max_stack, int ref, int64_t* visits, int64_t* mts,
                    void* stream) {
+    marks_reset();
     cudaStream_t s = S(stream);
     // outputs go to a scratch block: stats runs are diagnostics
     char* blk = nullptr;
@@ -761,6 +952,7 @@ int rs_query_stats(const rs_tree* t, const float* d_starts, const float* d_ends,
 
 int rs_sort_segments(const float* d_starts, const float* d_ends, int64_t n, float* d_out_starts,
                      float* d_out_ends, int64_t* d_perm, void* stream) {
+    marks_reset();
     if (n < 0 || n > 2147483647ll) return fail(RS_INVALID_ARG, "bad segment count");
     if (n == 0) return RS_OK;
     if (!(d_starts && d_ends && d_out_starts && d_out_ends && d_perm)) return fail(RS_INVALID_ARG, "null pointer");
@@ -778,6 +970,7 @@ int rs_baseline(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_
                 const float* d_starts, const float* d_ends, int64_t n_r, int mode,
                 int32_t* d_detected, int32_t* d_counts, int32_t* d_tri, float* d_dist,
                 float* d_points, void* stream) {
+    marks_reset();
     if (mode < 0 || mode > 2) return fail(RS_INVALID_ARG, "unknown mode %d", mode);
     if (n_t < 0 || n_r < 0 || n_t > 2147483647ll || n_r > 2147483647ll)
         return fail(RS_INVALID_ARG, "bad sizes");
@@ -863,7 +1056,6 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
         }
         return RS_OK;
     };
-    ev_record(0, s);
     rs_tree* t = nullptr;
     rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, s, &t, fork, true);
     if (rc) return rc;
@@ -891,7 +1083,7 @@ static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d
                              int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
                              int64_t* n_hits, int64_t* bad, cudaStream_t s) {
     rs_tree* t = nullptr;
-    if (tree_kind == kTreeFast && !g_buffer_path && !g_binary_fast) {
+    if (tree_kind == kTreeFast && !buffer_path() && !g_binary_fast) {
         FastOut o;
         o.flags = d_flags;
         o.c_ray = d_ray; o.c_dist = d_dist; o.c_tri = d_tri; o.c_pt = d_pt;
@@ -909,7 +1101,6 @@ static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d
         const int rc2 = t ? rs_free(t, s) : RS_OK;
         return rc ? rc : rc2;
     }
-    ev_record(0, s);
     int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
     if (rc) return rc;
     const int ref = tree_kind == kTreeReference;
@@ -963,7 +1154,7 @@ static int enqueue_device_batch_body(const float* d_verts, int64_t n_v, const in
                                 int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri,
                                 float* d_pt, const StatusDst& h_status, cudaStream_t s) {
     rs_tree* t = nullptr;
-    if (tree_kind == kTreeFast && !g_buffer_path && !g_binary_fast) {
+    if (tree_kind == kTreeFast && !buffer_path() && !g_binary_fast) {
         FastOut o;
         o.flags = d_flags;
         o.c_ray = d_ray; o.c_dist = d_dist; o.c_tri = d_tri; o.c_pt = d_pt;
@@ -979,7 +1170,6 @@ static int enqueue_device_batch_body(const float* d_verts, int64_t n_v, const in
         stage_mark(10, s);
         return rc;
     }
-    ev_record(0, s);
     int rc = build_impl(d_verts, n_v, d_tris, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
     if (rc) return rc;
     if (tree_kind == kTreeFast && !g_binary_fast) {
@@ -1017,13 +1207,12 @@ static int enqueue_device_batch_body(const float* d_verts, int64_t n_v, const in
     return rs_free(t, s);
 }
 
-static void timing_join(cudaStream_t s);
 static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t* d_tris,
                                 int64_t n_t, const float* d_starts, const float* d_ends,
                                 int64_t n_r, int mode, int tree_kind, int max_coll, int max_stack,
                                 int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri,
                                 float* d_pt, const StatusDst& h_status, cudaStream_t s) {
-    g_tpending = 0;
+    mark(0, s);
     const int rc = enqueue_device_batch_body(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
                                              tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
                                              d_tri, d_pt, h_status, s);
@@ -1034,21 +1223,34 @@ static int enqueue_device_batch(const float* d_verts, int64_t n_v, const int32_t
 struct GraphKey {
     const void* p[9];
     int64_t n_v, n_t, n_r;
-    int mode, kind, mc, ms, timing, opt_gen;
+    int mode, kind, mc, ms, timing, opt_gen, device;
     bool operator<(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) < 0; }
 };
+// One captured run_batch.  Entries are shared: a caller holds a reference
+// for the whole launch + wait + status read, so an eviction by another
+// thread only drops the cache's reference and the resources go with the
+// last user.  `run` serialises calls on the same entry (they share its
+// status word and scratch arena; identical keys also share outputs).
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     RsStatus* h_status = nullptr;  // pinned, mapped
     RsStatus* d_status = nullptr;  // its device alias
     char* arena = nullptr;         // the graph's scratch (see Arena)
-    unsigned long long stamp = 0;
+    unsigned long long stamp = 0;  // LRU clock (under g_graph_mu)
     long long kernels = 0;         // kernel nodes in the graph (for rs_kernel_launches)
+    std::vector<Mark> marks;       // timing nodes baked into the graph (events owned here)
+    std::mutex run;
+    ~GraphEntry() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (h_status) cudaFreeHost(h_status);
+        if (arena) cudaFree(arena);
+        for (auto& m : marks) cudaEventDestroy(m.ev);
+    }
 };
 static thread_local RsStatus g_last_status{};
 static std::atomic<int> g_opt_gen{0};  // bumped by rs_set_option: captured graphs bake the options in
 static std::mutex g_graph_mu;
-static std::map<GraphKey, GraphEntry> g_graphs;
+static std::map<GraphKey, std::shared_ptr<GraphEntry>> g_graphs;
 static std::set<GraphKey> g_seen;  // argument sets called once (captured on the next call)
 static unsigned long long g_graph_clock = 0;
 static const bool g_use_arena = [] {  // RS_GRAPH_ARENA=0: allocation nodes in the graph (A/B)
@@ -1060,11 +1262,72 @@ static const bool g_use_graphs = [] {
     return !(e && e[0] == '1');
 }();
 
+// Capture one argument set into a new entry (two passes: the first sizes the
+// scratch arena, the second captures from it).  Returns null on failure
+// (the caller then runs the direct launches).
+static std::shared_ptr<GraphEntry> capture_graph(const float* d_verts, int64_t n_v, const int32_t* d_tris,
+                                                 int64_t n_t, const float* d_starts, const float* d_ends,
+                                                 int64_t n_r, int mode, int tree_kind, int max_coll,
+                                                 int max_stack, int32_t* d_flags, int32_t* d_ray,
+                                                 float* d_dist, int32_t* d_tri, float* d_pt) {
+    auto e = std::make_shared<GraphEntry>();
+    if (cudaHostAlloc(reinterpret_cast<void**>(&e->h_status), sizeof(RsStatus), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_status), e->h_status, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); replay on the caller's
+    static thread_local cudaStream_t cap = nullptr;
+    if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    cudaGraph_t g = nullptr;
+    const long long k0 = rs::g_launches.load();
+    auto capture_once = [&](cudaGraph_t* out) -> int {
+        marks_reset();
+        if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return RS_CUDA_ERROR;
+        const int r = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
+                                           tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
+                                           d_tri, d_pt, StatusDst{e->h_status, e->d_status}, cap);
+        const cudaError_t ce = cudaStreamEndCapture(cap, out);
+        return r != RS_OK ? r : (ce == cudaSuccess && *out ? RS_OK : RS_CUDA_ERROR);
+    };
+    g_arena = Arena{nullptr, 0, 0, 1};
+    int erc = capture_once(&g);
+    const size_t arena_bytes = g_arena.off;
+    g_arena = Arena{};
+    if (g) cudaGraphDestroy(g);
+    g = nullptr;
+    if (erc == RS_OK && g_use_arena &&
+        cudaMalloc(reinterpret_cast<void**>(&e->arena), arena_bytes) == cudaSuccess) {
+        g_arena = Arena{e->arena, arena_bytes, 0, 2};
+        erc = capture_once(&g);
+        g_arena = Arena{};
+    } else if (erc == RS_OK) {
+        cudaGetLastError();
+        e->arena = nullptr;
+        erc = capture_once(&g);  // stream-ordered allocation nodes instead
+    }
+    e->kernels = rs::g_launches.load() - k0;
+    rs::g_launches.store(k0);  // counted when replayed
+    // the timing events recorded by the graph's nodes now belong to it
+    e->marks = g_marks;
+    g_pool.erase(g_pool.begin(), g_pool.begin() + (ptrdiff_t)g_pool_used);
+    marks_reset();
+    const bool ok = erc == RS_OK && g && cudaGraphInstantiate(&e->exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return e;
+}
+
 int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
                         const float* d_starts, const float* d_ends, int64_t n_r, int mode,
                         int tree_kind, int max_coll, int max_stack, int32_t* d_flags,
                         int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
                         int64_t* n_hits, int64_t* bad, void* stream) {
+    marks_reset();
     int rc = check_query(mode, max_coll, max_stack);
     if (rc) return rc;
     if (bad) *bad = -1;
@@ -1090,13 +1353,15 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
         key.mode = mode; key.kind = tree_kind; key.mc = max_coll; key.ms = max_stack;
         key.timing = g_timing;
         key.opt_gen = g_opt_gen.load();
-        GraphEntry* ge = nullptr;
+        CK(cudaGetDevice(&key.device));
+        std::shared_ptr<GraphEntry> ge;
         bool capture = true;
         {
             std::lock_guard<std::mutex> lk(g_graph_mu);
             auto it = g_graphs.find(key);
             if (it != g_graphs.end()) {
-                ge = &it->second;
+                ge = it->second;
+                ge->stamp = ++g_graph_clock;
             } else {
                 // capture only on an argument set's second call: a one-off
                 // call (fresh buffers every time) runs the direct launches
@@ -1109,141 +1374,93 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
             }
         }
         if (!ge && capture) {
-            GraphEntry e;
-            CK(cudaHostAlloc(reinterpret_cast<void**>(&e.h_status), sizeof(RsStatus), cudaHostAllocMapped));
-            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e.d_status), e.h_status, 0));
-            // capture on a private stream (the caller's may be the legacy
-            // default stream, which cannot be captured); replay on the caller's
-            static thread_local cudaStream_t cap = nullptr;
-            if (!cap) CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-            cudaGraph_t g = nullptr;
-            const long long k0 = rs::g_launches.load();
-            auto capture_once = [&](cudaGraph_t* out) -> int {
-                CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-                const int r = enqueue_device_batch(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode,
-                                                   tree_kind, max_coll, max_stack, d_flags, d_ray, d_dist,
-                                                   d_tri, d_pt, StatusDst{e.h_status, e.d_status}, cap);
-                const cudaError_t ce = cudaStreamEndCapture(cap, out);
-                return r != RS_OK ? r : (ce == cudaSuccess && *out ? RS_OK : RS_CUDA_ERROR);
-            };
-            // pass 1 sizes the arena (its graph is discarded), pass 2 captures from it
-            g_arena = Arena{nullptr, 0, 0, 1};
-            int erc = capture_once(&g);
-            const size_t arena_bytes = g_arena.off;
-            g_arena = Arena{};
-            if (g) cudaGraphDestroy(g);
-            g = nullptr;
-            rs::g_launches.store(k0);
-            if (erc == RS_OK && g_use_arena &&
-                cudaMalloc(reinterpret_cast<void**>(&e.arena), arena_bytes) == cudaSuccess) {
-                g_arena = Arena{e.arena, arena_bytes, 0, 2};
-                erc = capture_once(&g);
-                g_arena = Arena{};
-            } else if (erc == RS_OK) {
-                cudaGetLastError();
-                e.arena = nullptr;
-                erc = capture_once(&g);  // stream-ordered allocation nodes instead
-            }
-            e.kernels = rs::g_launches.load() - k0;
-            rs::g_launches.fetch_sub(e.kernels);  // counted when replayed
-            if (erc == RS_OK && g && cudaGraphInstantiate(&e.exec, g, 0) == cudaSuccess) {
+            ge = capture_graph(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode, tree_kind,
+                               max_coll, max_stack, d_flags, d_ray, d_dist, d_tri, d_pt);
+            if (ge) {
                 std::lock_guard<std::mutex> lk(g_graph_mu);
-                if (g_graphs.size() >= 8) {  // bounded cache: evict the least recently used
-                    auto victim = g_graphs.begin();
-                    for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
-                        if (it->second.stamp < victim->second.stamp) victim = it;
-                    cudaGraphExecDestroy(victim->second.exec);
-                    cudaFreeHost(victim->second.h_status);
-                    if (victim->second.arena) cudaFree(victim->second.arena);
-                    g_graphs.erase(victim);
+                auto it = g_graphs.find(key);
+                if (it != g_graphs.end()) {
+                    ge = it->second;  // another thread captured it meanwhile
+                } else {
+                    if (g_graphs.size() >= 8) {  // bounded cache: drop the least recently used
+                        auto victim = g_graphs.begin();
+                        for (auto v = g_graphs.begin(); v != g_graphs.end(); ++v)
+                            if (v->second->stamp < victim->second->stamp) victim = v;
+                        g_graphs.erase(victim);  // freed when its last user returns
+                    }
+                    g_graphs[key] = ge;
                 }
-                ge = &(g_graphs[key] = e);
-            } else {
-                cudaGetLastError();
-                cudaFreeHost(e.h_status);
-                if (e.arena) cudaFree(e.arena);
+                ge->stamp = ++g_graph_clock;
             }
-            if (g) cudaGraphDestroy(g);
         }
         if (ge) {
-            ge->stamp = ++g_graph_clock;
+            std::lock_guard<std::mutex> run(ge->run);
             using clk = std::chrono::steady_clock;
             const auto h0 = clk::now();
             CK(cudaGraphLaunch(ge->exec, s));
             const auto h1 = clk::now();
             rs::g_launches.fetch_add(ge->kernels);
             CK(cudaStreamSynchronize(s));
-            if (g_timing == 3) {  // host side of the call: launch and wait (ms)
-                g_host_ms[0] = std::chrono::duration<float, std::milli>(h1 - h0).count();
-                g_host_ms[1] = std::chrono::duration<float, std::milli>(clk::now() - h1).count();
-            }
+            g_host_ms[0] = std::chrono::duration<float, std::milli>(h1 - h0).count();
+            g_host_ms[1] = std::chrono::duration<float, std::milli>(clk::now() - h1).count();
             const RsStatus h = *ge->h_status;  // written by k_status_out before the sync returned
             g_last_status = h;
-            if (!h.internal) {
+            if (!ge->marks.empty()) {
+                g_tres = compute_timings(ge->marks);  // eagerly: the events belong to the graph
+                g_have_marks = true;
+            }
+            if (!h.internal && !h.dropped) {
                 if (n_hits) *n_hits = (int64_t)h.hits;
                 rc = status_code(h, bad);
                 done = true;
             }
             // internal capacity flag: fall through to the direct path, which
-            // re-queries with the binary kernels
+            // re-queries with the binary kernels; a collision-buffer overflow
+            // (candidates dropped): the direct path re-launches with a buffer
+            // of the claimed size
         }
     }
     if (!done) {
+        marks_reset();
+        mark(0, s);
         rc = run_device_direct(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode, tree_kind,
                                max_coll, max_stack, d_flags, d_ray, d_dist, d_tri, d_pt, n_hits, bad,
                                s);
-    }
-    if (g_timing && (rc == RS_OK || rc == RS_STACK_OVERFLOW)) {
-        g_build_ms = g_query_ms = 0.f;
-        if (g_timing == 1) {
-            cudaEventElapsedTime(&g_build_ms, g_ev[0], g_ev[1]);
-            cudaEventElapsedTime(&g_query_ms, g_ev[1], g_ev[2]);
-        }
-        g_hot_ms = 0.f;
-        if (g_ev[3] && g_ev[4]) cudaEventElapsedTime(&g_hot_ms, g_ev[3], g_ev[4]);
-        for (int k = 0; k < kStageEvents; ++k) {
-            g_stage_ms[k] = -1.f;
-            if (g_timing == 3 && g_ev[0] && g_ev[5 + k]) cudaEventElapsedTime(&g_stage_ms[k], g_ev[0], g_ev[5 + k]);
-        }
-        if (g_timing == 3) {  // 11, 12: host time in cudaGraphLaunch and in the wait
-            g_stage_ms[11] = g_host_ms[0];
-            g_stage_ms[12] = g_host_ms[1];
-        }
-        if (g_timing == 3 && g_ev[0] && g_ev[3] && g_ev[4]) {  // 14, 15: the traversal's start and end
-            cudaEventElapsedTime(&g_stage_ms[14], g_ev[0], g_ev[3]);
-            cudaEventElapsedTime(&g_stage_ms[15], g_ev[0], g_ev[4]);
-        }
-        g_ev_valid = true;
     }
     return rc;
 }
 
 RS_API int rs_set_timing(int enable) {
-    g_timing = enable == 2 || enable == 3 ? enable : (enable != 0 ? 1 : 0);
-    g_ev_valid = false;
+    g_timing = enable >= 0 && enable <= 3 ? enable : 1;
+    marks_reset();
     return RS_OK;
 }
 
 RS_API int rs_last_timings(float* build_ms, float* query_ms, float* hot_ms) {
-    if (!g_ev_valid) return fail(RS_INVALID_ARG, "no timed rs_run_batch_device call yet");
-    if (build_ms) *build_ms = g_build_ms;
-    if (query_ms) *query_ms = g_query_ms;
-    if (hot_ms) *hot_ms = g_hot_ms;
+    const TimingResult* r = last_timings();
+    if (!r) return fail(RS_INVALID_ARG, "no timed call yet (rs_set_timing)");
+    if (build_ms) *build_ms = r->build;
+    if (query_ms) *query_ms = r->query;
+    if (hot_ms) *hot_ms = r->hot;
+    return RS_OK;
+}
+
+RS_API int rs_last_phases(float* ms, int n) {
+    const TimingResult* r = last_timings();
+    if (!r) return fail(RS_INVALID_ARG, "no timed call yet (rs_set_timing)");
+    for (int k = 0; k < n && k < kPhaseCount; ++k) ms[k] = r->phase[k];
     return RS_OK;
 }
 
 RS_API int rs_stage_times(float* ms, int n) {
-    if (!g_ev_valid || g_timing != 3) return fail(RS_INVALID_ARG, "no stage-timed call yet (rs_set_timing(3))");
-    for (int k = 0; k < n && k < kStageEvents; ++k) ms[k] = g_stage_ms[k];
+    const TimingResult* r = last_timings();
+    if (!r || g_timing != 3) return fail(RS_INVALID_ARG, "no stage-timed call yet (rs_set_timing(3))");
+    for (int k = 0; k < n && k < kStageEvents; ++k) ms[k] = r->stage[k];
     return RS_OK;
 }
 
 RS_API long long rs_kernel_launches(void) { return g_launches.load(); }
 
-// Diagnostics: the device status words of the calling thread's last
-// graph-replayed rs_run_batch_device (bad, internal, hits, tile_counter,
-// visits, mts, cand_count, pad); builds with -DRS_TILE_STATS fill the
-// traversal counters.
 RS_API int rs_set_option(const char* name, long long value, long long* old_value) {
     if (!name) return fail(RS_INVALID_ARG, "null option name");
     if (rs::sorted_option(name, value, old_value)) return fail(RS_INVALID_ARG, "unknown option %s", name);
@@ -1253,6 +1470,10 @@ RS_API int rs_set_option(const char* name, long long value, long long* old_value
 
 RS_API const char* rs_hot_kernel(void) { return rs::hot_kernel_name(); }
 
+// Diagnostics: the device status words of the calling thread's last
+// graph-replayed rs_run_batch_device (bad, internal, hits, tile_counter,
+// visits, mts, cand_count, pad); builds with -DRS_TILE_STATS fill the
+// traversal counters.
 RS_API int rs_last_status(unsigned long long* out8) {
     std::memcpy(out8, &g_last_status, sizeof(RsStatus));
     return RS_OK;
@@ -1261,43 +1482,15 @@ RS_API int rs_last_status(unsigned long long* out8) {
 }  // extern "C"
 
 void rs::stage_mark(int k, cudaStream_t s) {
-    if (k >= 0 && k < kStageEvents) ev_record(5 + k, s);
+    if (k >= 0 && k < kStageEvents) mark(kTagStage + k, s);
 }
-
-// Timing level 2 inside a captured graph: the traversal's two event-record
-// nodes hang off side branches (a fork from the caller's stream, joined back
-// only at the end of the graph) instead of sitting in the kernel chain, where
-// each added ~6 us of node latency to every step.
 
 void rs::hot_kernel_mark(int which, cudaStream_t s) {
-    if (!(g_hot_mark_mask & (1 << which))) return;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cs);
-    if (g_timing != 2 || cs != cudaStreamCaptureStatusActive) {
-        ev_record(3 + which, s);
-        return;
-    }
-    if (!g_tstream) {
-        cudaStreamCreateWithFlags(&g_tstream, cudaStreamNonBlocking);
-        for (int k = 0; k < 2; ++k) {
-            cudaEventCreateWithFlags(&g_tfork[k], cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&g_tjoin[k], cudaEventDisableTiming);
-        }
-    }
-    // each mark gets its own branch: fork from s, record, and remember the join
-    cudaEventRecord(g_tfork[which], s);
-    cudaStreamWaitEvent(g_tstream, g_tfork[which], 0);
-    ev_record(3 + which, g_tstream);
-    cudaEventRecord(g_tjoin[which], g_tstream);
-    g_tpending |= 1 << which;
+    if (g_hot_mark_mask & (1 << which)) mark(3 + which, s);
 }
 
-// joins the timing branches back into s (before a capture ends)
-static void timing_join(cudaStream_t s) {
-    for (int k = 0; k < 2; ++k)
-        if (g_tpending & (1 << k)) cudaStreamWaitEvent(s, g_tjoin[k], 0);
-    g_tpending = 0;
-}
+// set while the host pipeline re-runs a batch with the binary kernels
+static thread_local bool g_force_binary = false;
 
 extern "C" {
 
@@ -1347,6 +1540,7 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     auto chunk_cnt = [&](int64_t k) { return bounds[k + 1] - bounds[k]; };
     const bool bary = mode == kBarycentric;
     const bool fast_tree = tree_kind == kTreeFast && !g_binary_fast;
+    const bool fast = fast_tree && !g_force_binary;
     // Barycentric rows into pinned host outputs: each chunk's compaction
     // writes its rows straight into the caller's (mapped) host arrays at the
     // running row count, so the D2H overlaps the remaining uploads instead
@@ -1354,7 +1548,7 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     int32_t *zray = nullptr, *ztri = nullptr;
     float *zdist = nullptr, *zpt = nullptr;
     bool zc = false;
-    if (bary && fast_tree && g_zero_copy && !g_buffer_path) {
+    if (bary && fast && g_zero_copy && !buffer_path()) {
         void *a = nullptr, *b = nullptr, *cc = nullptr, *d = nullptr;
         zc = cudaHostGetDevicePointer(&a, h_ray, 0) == cudaSuccess &&
              cudaHostGetDevicePointer(&b, h_dist, 0) == cudaSuccess &&
@@ -1371,8 +1565,27 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     const size_t out_b = bary ? (zc ? 256 : 4 * align256(12ull * n_r)) : 2 * align256(4ull * chunk_rays);
     const size_t tiles_b = align256(compact_scratch_bytes(chunk_rays)) * (size_t)nchunks;
     const size_t st_b = align256(sizeof(RsStatus) * (size_t)nchunks);
-    char* blk = nullptr;
-    CK(dmalloc(reinterpret_cast<void**>(&blk), mesh_b + in_b + out_b + tiles_b + st_b, s));
+    // every exit (errors included) drains the pipeline's streams and
+    // releases the device block, the tree and the per-buffer scratch
+    struct Cleanup {
+        cudaStream_t s;
+        char* blk = nullptr;
+        rs_tree* t = nullptr;
+        FastScratch fs[2];
+        ~Cleanup() {
+            cudaStreamSynchronize(g_pipe.copy);
+            cudaStreamSynchronize(g_pipe.copy2);
+            cudaStreamSynchronize(s);
+            for (auto& f : fs)
+                if (f.blk) dfree(f.blk, s);
+            if (t) rs_free(t, s);
+            if (blk) dfree(blk, s);
+            cudaStreamSynchronize(s);
+        }
+    } guard{s};
+    FastScratch* fs = guard.fs;
+    CK(dmalloc(reinterpret_cast<void**>(&guard.blk), mesh_b + in_b + out_b + tiles_b + st_b, s));
+    char* blk = guard.blk;
     Carver c{blk};
     float* dV = c.take<float>(3ull * n_v);
     int* dT = c.take<int>(3ull * n_t);
@@ -1411,15 +1624,12 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     CK(cudaStreamWaitEvent(d2h, g_pipe.ev_blk, 0));
     CK(cudaMemcpyAsync(dV, h_verts, 12ull * n_v, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dT, h_tris, 12ull * n_t, cudaMemcpyHostToDevice, s));
-    rs_tree* t = nullptr;
-    rc = build_impl(dV, n_v, dT, n_t, tree_kind, nullptr, nullptr, s, &t, nullptr, true);
-    if (rc) {
-        dfree(blk, s);
-        return rc;
-    }
+    mark(0, s);
+    rc = build_impl(dV, n_v, dT, n_t, tree_kind, nullptr, nullptr, s, &guard.t, nullptr, true);
+    if (rc) return rc;
+    rs_tree* const t = guard.t;
     const int ref = tree_kind == kTreeReference;
-    const bool fast = tree_kind == kTreeFast && !g_binary_fast;
-    FastScratch fs[2];
+    if (fast_tree && g_force_binary) max_stack = 1 << 30;  // the binary walk of a fast tree: no overflow rule
     if (fast)
         for (int b = 0; b < 2; ++b) {
             rc = fast_alloc(fs[b], chunk_rays, mode, 2 * chunk_rays + 4096, s);
@@ -1430,7 +1640,7 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     // behind: once chunk j's status has landed in pinned memory the host
     // knows its row count and queues the row copies at the running offset,
     // while the device already works on chunk j+1.
-    const bool lagged = bary && !zc && !g_buffer_path;
+    const bool lagged = bary && !zc && !buffer_path();
     if (lagged && g_pipe.hst_cap < nchunks) {
         if (g_pipe.hst) cudaFreeHost(g_pipe.hst);
         CK(cudaHostAlloc(reinterpret_cast<void**>(&g_pipe.hst), sizeof(RsStatus) * nchunks,
@@ -1476,6 +1686,7 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
             if (rc) return rc;
         } else {
             QueryArgs a = make_args(t, din[b][0], din[b][1], cnt, max_coll, max_stack, st + k);
+            if (fast_tree) a.nodes4 = nullptr;  // binary kernels over the fast tree's records
             a.ray_offset = lo;
             if (bary) {
                 // each chunk compacts into its own region; rows are concatenated on the host
@@ -1489,11 +1700,10 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
                 a.detected = dflag[b];
                 a.counts = dflag[b];
             }
-            if (launch_query(a, mode, ref != 0, bary, kstack_for(ref != 0, max_stack), false, s)) {
-                rs_free(t, stream);
-                dfree(blk, s);
-                return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
-            }
+            mark(1, s);
+            const int lq = launch_query(a, mode, ref != 0, bary, kstack_for(ref != 0, max_stack), false, s);
+            mark(2, s);
+            if (lq) return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
             CK(cudaGetLastError());
         }
         CK(cudaEventRecord(g_pipe.ev_q[b], s));
@@ -1511,12 +1721,16 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     if (lagged && (rc = retire(nchunks - 1))) return rc;
     cp = d2h;
     // statuses of every chunk; barycentric row counts come back with them
-    RsStatus* hst = new RsStatus[nchunks];
+    std::vector<RsStatus> hst_v((size_t)nchunks);
+    RsStatus* hst = hst_v.data();
     CK(cudaStreamWaitEvent(cp, g_pipe.ev_q[(nchunks - 1) & 1], 0));
     CK(cudaMemcpyAsync(hst, st, sizeof(RsStatus) * nchunks, cudaMemcpyDeviceToHost, cp));
     CK(cudaStreamSynchronize(cp));
     if (fast) {
-        for (int b = 0; b < 2; ++b) CK(dfree(fs[b].blk, s));
+        for (int b = 0; b < 2; ++b) {
+            CK(dfree(fs[b].blk, s));
+            fs[b].blk = nullptr;
+        }
         // collision-buffer overflow in a chunk: redo that chunk with a buffer
         // sized to what its traversal claimed
         for (int64_t k = 0; k < nchunks; ++k) {
@@ -1546,6 +1760,19 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
         if (hst[k].bad && (!badv || ~hst[k].bad < ~badv)) badv = hst[k].bad;
         internal |= hst[k].internal;
     }
+    if (fast && internal) {
+        // a fast-path walk exceeded its capacity (never expected: fast trees
+        // are at most 61 deep): redo the batch with the binary kernels, as
+        // the device path does (binary_query)
+        guard.~Cleanup();
+        new (&guard) Cleanup{s};
+        g_force_binary = true;
+        rc = run_batch_host_impl(h_verts, n_v, h_tris, n_t, h_starts, h_ends, n_r, mode, tree_kind,
+                                 max_coll, max_stack, chunk_rays, h_flags, h_ray, h_dist, h_tri, h_pt,
+                                 n_hits, bad, stream);
+        g_force_binary = false;
+        return rc;
+    }
     if (bary && zc) {
         for (int64_t k = 0; k < nchunks; ++k) running += hst[k].hits;  // rows already in place
     } else if (bary && lagged) {
@@ -1564,10 +1791,6 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
         }
         CK(cudaStreamSynchronize(cp));
     }
-    delete[] hst;
-    rs_free(t, stream);
-    CK(dfree(blk, s));
-    CK(cudaStreamSynchronize(s));
     if (n_hits) *n_hits = (int64_t)running;
     RsStatus agg{};
     agg.bad = badv;
@@ -1580,6 +1803,7 @@ int rs_run_batch_host(const float* h_verts, int64_t n_v, const int32_t* h_tris, 
                       int tree_kind, int max_coll, int max_stack, int64_t chunk_rays,
                       int32_t* h_flags, int32_t* h_ray, float* h_dist, int32_t* h_tri,
                       float* h_pt, int64_t* n_hits, int64_t* bad, void* stream) {
+    marks_reset();
     rs::set_batch_rays(n_r);  // chunks choose their traversal by the whole batch's density
     const int rc = run_batch_host_impl(h_verts, n_v, h_tris, n_t, h_starts, h_ends, n_r, mode, tree_kind,
                                        max_coll, max_stack, chunk_rays, h_flags, h_ray, h_dist, h_tri,

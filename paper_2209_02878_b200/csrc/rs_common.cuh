@@ -71,7 +71,7 @@ struct RsStatus {
     unsigned long long visits;    // optional stats
     unsigned long long mts;
     unsigned long long cand_count;  // collision-buffer entries claimed (may exceed capacity)
-    unsigned long long pad;
+    unsigned long long dropped;     // collision buffer overflowed: candidates dropped, re-launch
 };
 
 constexpr int kCandChunk = 128;  // collision-buffer entries claimed per warp atomic

@@ -9,6 +9,10 @@ namespace rs {
 
 // Number of kernels this library has launched (bench.py's gpu_launches).
 void count_launches(long long k);
+// Per-device launch facts (cached per device, thread-safe; rs_capi.cu).
+int device_sms();
+int occupancy(const void* kernel, int threads, size_t dynamic_smem = 0);
+void ensure_dynamic_smem(const void* kernel, int bytes);
 // Device timing of the dominant kernel (bench.py roofline): 0 before, 1 after.
 void hot_kernel_mark(int which, cudaStream_t s);
 void stage_mark(int k, cudaStream_t s);  // rs_set_timing(3) diagnostics
@@ -125,6 +129,7 @@ struct ExactArgs {
     int* best_tri;               // barycentric: winning triangle (pre-set to -1)
     unsigned long long* cand_t;  // barycentric: t key per candidate
     unsigned long long* mts;
+    unsigned long long* dropped; // set when the buffer overflowed (results incomplete)
 };
 struct CompactArgs {
     long long n_r;
@@ -201,6 +206,12 @@ void set_batch_rays(long long n);
 int sorted_option(const char* name, long long value, long long* old);
 // Fast-tree key grid: 0 isotropic, 1 per-axis, 2 auto (option "fast_keys").
 int fast_key_mode();
+// Fast-tree query path (option "fast_path"): 0 binned tile traversal
+// (default), 1 collision buffer (pair traversal -> warp-aggregated append ->
+// exact pass, re-launched with a sized buffer on overflow).
+int fast_path();
+// Initial collision-buffer capacity in entries (option "cand_cap"; 0: 2 x segments + 4096).
+long long cand_cap_override();
 // Name of the traversal kernel the last launch_sorted_trav chose.
 const char* hot_kernel_name();
 void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s);

@@ -528,12 +528,8 @@ static void go(const QueryArgs& a, bool compact, bool stats, cudaStream_t s) {
     }
     if (!REF && a.nodes4 && !g_binary_fast) {
         auto kq = stats ? k_query_quad<MODE, true> : k_query_quad<MODE, false>;
-        static int occ_q[2] = {0, 0};
-        int& oq = occ_q[stats ? 1 : 0];
-        if (!oq) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oq, kq, kQuadThreads, 0);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int oq = occupancy((const void*)kq, kQuadThreads);
+        const int sms = device_sms();
         long long want = (a.n_r + kQuadGroups - 1) / kQuadGroups;
         long long pg = (long long)sms * (oq > 0 ? oq : 1);
         kq<<<(unsigned)(want < pg ? want : pg), kQuadThreads, 0, s>>>(a);
@@ -545,12 +541,8 @@ static void go(const QueryArgs& a, bool compact, bool stats, cudaStream_t s) {
         return;
     }
     auto kern = stats ? k_query_persistent<MODE, REF, KS, true> : k_query_persistent<MODE, REF, KS, false>;
-    static int per_sm[2] = {0, 0};
-    int& occ = per_sm[stats ? 1 : 0];
-    if (!occ) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPersistThreads, 0);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int occ = occupancy((const void*)kern, kPersistThreads);
+    const int sms = device_sms();
     long long want = (a.n_r + kPersistThreads - 1) / kPersistThreads;
     long long pg = (long long)sms * (occ > 0 ? occ : 1);
     kern<<<(unsigned)(want < pg ? want : pg), kPersistThreads, 0, s>>>(a);

@@ -424,10 +424,7 @@ __global__ void __launch_bounds__(256) k_bin_count(SortedArgs a) {
     }
 }
 
-// Exclusive scan of the bin counters in two levels: k_tile_reduce sums each
-// 1024-bin tile, k_tile_scan scans the tile sums in one CTA, then k_bin_scan
-// scans each tile's bins from its tile offset.
-
+// Block-wide exclusive scan of 256 per-thread values (k_bin_scan1).
 __device__ __forceinline__ unsigned block_excl_scan_256(unsigned v, unsigned* wtot, unsigned* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned x = v;
@@ -444,48 +441,6 @@ __device__ __forceinline__ unsigned block_excl_scan_256(unsigned v, unsigned* wt
     }
     if (total) *total = all;
     return before + x - v;
-}
-
-__global__ void __launch_bounds__(256) k_tile_reduce(SortedArgs a) {
-    __shared__ unsigned wtot[8];
-    const uint4 v = *reinterpret_cast<const uint4*>(a.bins + blockIdx.x * kScanTile + threadIdx.x * 4);
-    unsigned total;
-    block_excl_scan_256(v.x + v.y + v.z + v.w, wtot, &total);
-    if (threadIdx.x == 0) a.tile_sum[blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(256) k_tile_scan(SortedArgs a) {
-    __shared__ unsigned wtot[8];
-    constexpr int per = kScanTiles / 256;
-    unsigned v[per], sum = 0;
-#pragma unroll
-    for (int k = 0; k < per; ++k) {
-        v[k] = a.tile_sum[threadIdx.x * per + k];
-        sum += v[k];
-    }
-    unsigned total;
-    unsigned run = block_excl_scan_256(sum, wtot, &total);
-#pragma unroll
-    for (int k = 0; k < per; ++k) {
-        a.tile_sum[threadIdx.x * per + k] = run;  // becomes the tile offset
-        run += v[k];
-    }
-    if (threadIdx.x == 0) *a.n_live = total;
-}
-
-__global__ void __launch_bounds__(256) k_bin_scan(SortedArgs a) {
-    __shared__ unsigned wtot[8];
-    const int tile = blockIdx.x;
-    const int base = tile * kScanTile + threadIdx.x * 4;
-    const uint4 v = *reinterpret_cast<const uint4*>(a.bins + base);
-    unsigned run = __ldg(a.tile_sum + tile) +
-                   block_excl_scan_256(v.x + v.y + v.z + v.w, wtot, nullptr);
-    uint4 o;
-    o.x = run; run += v.x;
-    o.y = run; run += v.y;
-    o.z = run; run += v.z;
-    o.w = run;
-    *reinterpret_cast<uint4*>(a.cursor + base) = o;
 }
 
 // Scatter pass: the same bins; each live segment's 32-B record goes to its
@@ -1053,6 +1008,9 @@ constexpr int kTileFCap = 256;  // walk frontier per level
 #endif
 constexpr int kCutDepth = RS_CUT_DEPTH;  // the walk starts from the depth-6 cut (7, 8 measured slower: smem vs occupancy)
 constexpr int kCutCap = 1 << kCutDepth;
+// a tile's walk seeds its leaf list and first frontier from the cut without
+// capacity checks: at most kCutCap entries each
+static_assert(kCutCap <= kTileLCap && kCutCap <= kTileFCap, "cut larger than the tile lists");
 #ifndef RS_WCAP
 #define RS_WCAP 16
 #endif
@@ -1966,15 +1924,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_wtile(Sor
 
 size_t sorted_bins() { return kBins; }
 
-static int sm_total() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
+static int sm_total() { return device_sms(); }
 
 bool sorted_wide() {
     static const bool wide = [] {
@@ -2003,6 +1953,8 @@ struct SortedOpts {
     unsigned range_max = 4096;   // tile lists from a Morton key range of at most this many leaves (0: walk only)
     unsigned warp_chunks = 4;    // warp tiles: records per warp unit / 32
     int geom = 0;                // 1: bin geometry derived once by k_seg_sample (A/B: C3/C5 -1..2%, C2 +3%)
+    int fast_path = 0;           // 0 binned tiles, 1 collision buffer (rs_trav.cu)
+    long long cand_cap = 0;      // collision buffer: initial capacity (0: 2 x segments + 4096)
 };
 static SortedOpts& opts() {
     static SortedOpts o = [] {
@@ -2029,6 +1981,9 @@ static SortedOpts& opts() {
         d.rec_ids = (int)num("RS_REC_IDS", d.rec_ids);
         d.warp_chunks = (unsigned)num("RS_WARP_CHUNKS", d.warp_chunks);
         d.geom = (int)num("RS_GEOM", d.geom);
+        const char* fp = getenv("RS_FAST_PATH");
+        if (fp && fp[0] == 'b') d.fast_path = 1;
+        d.cand_cap = num("RS_CAND_CAP", d.cand_cap);
         return d;
     }();
     return o;
@@ -2052,6 +2007,8 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "auto_tile")) { prev = o.auto_tile; if (value >= 3 && value <= 5) o.auto_tile = (int)value; }
     else if (!strcmp(name, "warp_chunks")) { prev = o.warp_chunks; if (value > 0) o.warp_chunks = (unsigned)value; }
     else if (!strcmp(name, "geom")) { prev = o.geom; if (value >= 0) o.geom = value ? 1 : 0; }
+    else if (!strcmp(name, "fast_path")) { prev = o.fast_path; if (value >= 0 && value <= 1) o.fast_path = (int)value; }
+    else if (!strcmp(name, "cand_cap")) { prev = o.cand_cap; if (value >= 0) o.cand_cap = value; }
     else return -1;
     if (old) *old = prev;
     return 0;
@@ -2059,6 +2016,8 @@ int sorted_option(const char* name, long long value, long long* old) {
 
 static int trav_variant() { return opts().trav; }
 int fast_key_mode() { return opts().fast_keys; }
+int fast_path() { return opts().fast_path; }
+long long cand_cap_override() { return opts().cand_cap; }
 static unsigned tile_min_density() { return opts().tile_density; }
 static unsigned tile_balance() { return opts().tile_balance; }
 static unsigned bin_occupancy() { return opts().bin_occ; }
@@ -2082,13 +2041,9 @@ void launch_binning(const SortedArgs& a0, cudaStream_t s, bool zero_flags) {
     k_seg_sample<<<kSampleCtas, kSampleThreads, 0, s>>>(a);
     const bool vec = ((reinterpret_cast<uintptr_t>(a.starts) | reinterpret_cast<uintptr_t>(a.ends)) & 15) == 0;
     if (vec && opts().bin_tma && a.n_r >= kStreamSegs) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_bin_count_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem);
-            cudaFuncSetAttribute(k_bin_count_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem);
-            cudaFuncSetAttribute(k_bin_scatter_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmem);
-            attr = true;
-        }
+        ensure_dynamic_smem((const void*)k_bin_count_tma<false>, (int)kStreamSmem);
+        ensure_dynamic_smem((const void*)k_bin_count_tma<true>, (int)kStreamSmem);
+        ensure_dynamic_smem((const void*)k_bin_scatter_tma, (int)kStreamSmem);
         const long long chunks = a.n_r / kStreamSegs;
         const unsigned g = (unsigned)(chunks < sms * (long long)RS_STREAM_CTAS ? chunks : sms * (long long)RS_STREAM_CTAS);
         const bool rank = opts().bin_rank;
@@ -2114,45 +2069,35 @@ void launch_binning(const SortedArgs& a0, cudaStream_t s, bool zero_flags) {
     }
     const long long want = (a.n_r + 1023) / 1024;
     const unsigned g = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
+    stage_mark(5, s);
     if (vec) k_bin_count<true><<<g, 256, 0, s>>>(a);
     else k_bin_count<false><<<g, 256, 0, s>>>(a);
+    stage_mark(6, s);
     k_bin_scan1<<<kScanTiles, 256, 0, s>>>(a);
+    stage_mark(7, s);
     if (vec) k_bin_scatter<true><<<g, 256, 0, s>>>(a);
     else k_bin_scatter<false><<<g, 256, 0, s>>>(a);
+    stage_mark(8, s);
 }
 
 template <int MODE>
 static void launch_tile(const SortedArgs& a, int sms, cudaStream_t s) {
-    static int occ[2] = {0, 0};
     const bool wide = a.nodes4 != nullptr && opts().tile_wide;
-    int& o = occ[wide];
-    if (!o) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &o, wide ? (const void*)k_trav_tile<MODE, true> : (const void*)k_trav_tile<MODE, false>,
-            kTileThreads, 0);
-        if (o < 1) o = 1;
-    }
+    const int o = occupancy(wide ? (const void*)k_trav_tile<MODE, true> : (const void*)k_trav_tile<MODE, false>,
+                            kTileThreads);
     if (wide) k_trav_tile<MODE, true><<<sms * o, kTileThreads, 0, s>>>(a);
     else k_trav_tile<MODE, false><<<sms * o, kTileThreads, 0, s>>>(a);
 }
 
 template <int MODE>
 static void launch_ptile(const SortedArgs& a, int sms, cudaStream_t s) {
-    static int occ = 0;
-    if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trav_ptile<MODE>, kTileThreads, 0);
-        if (occ < 1) occ = 1;
-    }
+    const int occ = occupancy((const void*)k_trav_ptile<MODE>, kTileThreads);
     k_trav_ptile<MODE><<<sms * occ, kTileThreads, 0, s>>>(a);
 }
 
 template <int MODE>
 static void launch_wtile(const SortedArgs& a, int sms, cudaStream_t s) {
-    static int occ = 0;
-    if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trav_wtile<MODE>, kTileThreads, 0);
-        if (occ < 1) occ = 1;
-    }
+    const int occ = occupancy((const void*)k_trav_wtile<MODE>, kTileThreads);
     k_trav_wtile<MODE><<<sms * occ, kTileThreads, 0, s>>>(a);
 }
 
@@ -2209,15 +2154,10 @@ void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t
         hot_kernel_mark(1, s);
         return;
     }
-    static int occ[3] = {0, 0, 0};
-    int& o = occ[mode];
-    if (!o) {
-        const void* k = mode == kBoolean ? (const void*)k_trav_sorted<kBoolean, false>
-                        : mode == kCount ? (const void*)k_trav_sorted<kCount, false>
-                                         : (const void*)k_trav_sorted<kBarycentric, false>;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kSortedThreads, 0);
-        if (o < 1) o = 1;
-    }
+    const int o = occupancy(mode == kBoolean ? (const void*)k_trav_sorted<kBoolean, false>
+                            : mode == kCount ? (const void*)k_trav_sorted<kCount, false>
+                                             : (const void*)k_trav_sorted<kBarycentric, false>,
+                            kSortedThreads);
     const long long wt = (a.n_r + kSortedThreads - 1) / kSortedThreads;
     const unsigned gt = (unsigned)(wt < (long long)sms * o ? wt : (long long)sms * o);
     if (variant == 1 && !stats) {

@@ -404,6 +404,10 @@ template <int MODE, bool STATS>
 __global__ void __launch_bounds__(256) k_exact(ExactArgs a) {
     const unsigned long long n = *a.cand_count < (unsigned long long)a.cand_cap
                                      ? *a.cand_count : (unsigned long long)a.cand_cap;
+    // overflow detection: the append counter ran past the buffer, so some
+    // candidates were dropped; the host re-launches with a buffer of the
+    // claimed size (rs_capi.cu fast_query / host pipeline / graph fallback)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && *a.cand_count > (unsigned long long)a.cand_cap) *a.dropped = 1;
     unsigned long long mts = 0;
     for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
         const int2 c = a.cand[i];
@@ -558,15 +562,7 @@ __global__ void __launch_bounds__(256) k_bary_dense(CompactArgs a, int* detected
 
 // ------------------------------------------------------------ host glue ---
 
-static int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
+static int sm_count() { return device_sms(); }
 
 // persistent grid: at most 16 CTAs per SM of kTravThreads, <= kTravThreads/2 groups each
 size_t trav_gstack_ints() { return (size_t)sm_count() * 16 * (kTravThreads / 2) * kTravStack; }
@@ -580,9 +576,7 @@ void launch_trav(const TravArgs& a, bool stats, cudaStream_t s) {
     }();
     auto k = lanes == 4 ? (stats ? k_trav_group<4, true> : k_trav_group<4, false>)
                         : (stats ? k_trav_pair<true> : k_trav_pair<false>);
-    static int occ[4] = {0, 0, 0, 0};
-    int& o = occ[(stats ? 1 : 0) + (lanes == 4 ? 2 : 0)];
-    if (!o) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kTravThreads, 0);
+    const int o = occupancy((const void*)k, kTravThreads);
     const long long want = (a.n_r + kTravThreads / lanes - 1) / (kTravThreads / lanes);
     const long long pg = (long long)sm_count() * (o > 0 ? (o < 16 ? o : 16) : 1);
     k<<<(unsigned)(want < pg ? want : pg), kTravThreads, 0, s>>>(a);

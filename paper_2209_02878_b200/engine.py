@@ -13,7 +13,6 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -283,16 +282,14 @@ def _run_host(mesh: Mesh, seg: SegmentBatch, config: EngineConfig, kind: str) ->
     else:
         flags = _host_empty(n, np.int32)
     n_hits, bad = C.c_int64(0), C.c_int64(-1)
-    t0 = time.perf_counter()
     st = _lib.lib().rs_run_batch_host(
         _ptr(mesh.vertices), mesh.num_vertices, _ptr(mesh.triangles), mesh.num_triangles,
         _ptr(seg.starts), _ptr(seg.ends), n, _lib.MODE_TAGS[mode], _lib.TREE_KINDS[kind],
         config.max_collisions, config.max_stack, int(config.chunk_rays),
         _ptr(flags), _ptr(ray), _ptr(dist), _ptr(tri), _ptr(pt), C.byref(n_hits), C.byref(bad),
         _stream())
-    elapsed = time.perf_counter() - t0
     _lib.check(st, bad.value, config.max_stack)
-    timings = {"query": elapsed}
+    timings = _lib.last_phases()
     if mode == MODE_BOOLEAN:
         return ResultSet(mode, n, crossing=flags, timings=timings)
     if mode == MODE_COUNT:
@@ -329,12 +326,14 @@ def run_device(mesh: Mesh, seg: SegmentBatch, config: EngineConfig, kind: str,
         config.max_collisions, config.max_stack, _ptr(flags), _ptr(ray), _ptr(dist), _ptr(tri),
         _ptr(pt), C.byref(n_hits), C.byref(bad), _stream(dev.index))
     _lib.check(st, bad.value, config.max_stack)
+    timings = _lib.last_phases()
     if mode == MODE_BOOLEAN:
-        return ResultSet(mode, n, crossing=flags)
+        return ResultSet(mode, n, crossing=flags, timings=timings)
     if mode == MODE_COUNT:
-        return ResultSet(mode, n, counts=flags)
+        return ResultSet(mode, n, counts=flags, timings=timings)
     k = n_hits.value
-    return ResultSet(mode, n, ray_index=ray[:k], distance=dist[:k], triangle_id=tri[:k], point=pt[:k])
+    return ResultSet(mode, n, ray_index=ray[:k], distance=dist[:k], triangle_id=tri[:k], point=pt[:k],
+                     timings=timings)
 
 
 def _to_device(mesh: Mesh, segments: SegmentBatch):
@@ -372,18 +371,23 @@ def run_batch(mesh: Mesh, segments: SegmentBatch, config: EngineConfig | None = 
     timings = {}
     perm = None
     if config.sort_rays:
-        t0 = time.perf_counter()
-        segments, perm = sort_segments_by_morton(segments)
-        timings["ray sort"] = time.perf_counter() - t0
+        segments, perm, timings["ray sort"] = _timed_sort(segments)
     kind = config.resolved_tree()
-    if dev:
-        t0 = time.perf_counter()
-        rs = run_device(mesh, segments, config, kind)
-        rs.timings["query"] = time.perf_counter() - t0
-    else:
-        rs = _run_host(mesh, segments, config, kind)
+    rs = run_device(mesh, segments, config, kind) if dev else _run_host(mesh, segments, config, kind)
     rs.timings.update(timings)
     return _unpermute(rs, perm)
+
+
+def _timed_sort(segments: SegmentBatch):
+    """sort_segments_by_morton with its device time ("ray sort")."""
+    import torch
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    segments, perm = sort_segments_by_morton(segments)
+    ev[1].record()
+    ev[1].synchronize()
+    return segments, perm, ev[0].elapsed_time(ev[1]) / 1e3
 
 
 def run_baseline_allpairs(mesh: Mesh, segments: SegmentBatch,
@@ -403,12 +407,9 @@ def run_baseline_allpairs(mesh: Mesh, segments: SegmentBatch,
     perm = None
     timings = {}
     if config.sort_rays:
-        t0 = time.perf_counter()
-        segments, perm = sort_segments_by_morton(segments)
-        timings["ray sort"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
+        segments, perm, timings["ray sort"] = _timed_sort(segments)
     out = b200.baseline_dense(mesh, segments, config.mode)
-    timings["query"] = time.perf_counter() - t0
+    timings.update(_lib.last_phases())
     rs = _assemble_dense(config.mode, out, n, dev)
     rs.timings = timings
     return _unpermute(rs, perm)

@@ -21,6 +21,8 @@ them):
                 with results and max_stack overflow indices
   tree_*.npz    trees for random meshes (test_backends.py:46-84 sizes)
   sortperm.npz  sort_segments_by_morton permutations (engine.py:125-147)
+  tree_dup5.npz, scene_dup.npz   equal Morton codes (test_backends.py:70-84
+                and a terrain with repeated triangles): trees + results
 """
 
 from __future__ import annotations
@@ -170,6 +172,45 @@ def tree_case(rs, n_tri, seed):
     np.savez_compressed(OUT / f"tree_{n_tri}.npz", **d)
 
 
+def dup_cases(rs):
+    """Equal Morton codes: the all-duplicate mesh of test_backends.py:70-84
+    (one tree) and a terrain whose triangles are each repeated (every code
+    appears 2-3 times): trees (the Apetrei climb's id-XOR / position
+    tie-breaks, _core.pyx:52-64, and the sort's stability, morton.py:131-146)
+    and results in every mode."""
+    from raysurf import EngineConfig, Mesh, SegmentBatch, run_baseline_allpairs, run_batch
+    from raysurf.oracle import generate_scene
+
+    rng = np.random.default_rng(56)
+    verts = rng.uniform(-1, 1, size=(6, 3)).astype(np.float32)
+    tris = np.array([[0, 1, 2], [1, 2, 3], [2, 3, 4], [0, 2, 4], [1, 3, 5]], dtype=np.int32)
+    mesh = Mesh.from_arrays(np.tile(verts[:1], (6, 1)) * 0 + verts[:1], tris)
+    d = {"vertices": mesh.vertices, "triangles": mesh.triangles}
+    d.update(_tree_arrays(rs, mesh))
+    assert len(set(d["sorted_codes"].tolist())) == 1
+    np.savez_compressed(OUT / "tree_dup5.npz", **d)
+
+    sc = generate_scene(1500, 8000, 0.5, seed=2023)
+    T = sc.mesh.triangles
+    pick = np.random.default_rng(3).permutation(T.shape[0])
+    # every triangle twice, a third of them three times; shuffled ids
+    T2 = np.concatenate([T, T[pick], T[pick[: T.shape[0] // 3]]])
+    T2 = T2[np.random.default_rng(4).permutation(T2.shape[0])]
+    mesh = Mesh.from_arrays(sc.mesh.vertices, T2)
+    batch = SegmentBatch.from_arrays(sc.segments.starts, sc.segments.ends)
+    d = {"vertices": mesh.vertices, "triangles": mesh.triangles, "starts": batch.starts,
+         "ends": batch.ends, "expected": sc.expected_crossings}
+    d.update(_tree_arrays(rs, mesh))
+    assert len(np.unique(d["sorted_codes"])) < mesh.num_triangles
+    for m in MODES:
+        d.update(_result_arrays(f"batch_{m}", run_batch(mesh, batch, EngineConfig(mode=m))))
+        d.update(_result_arrays(f"base_{m}", run_baseline_allpairs(mesh, batch, EngineConfig(mode=m))))
+        for cap in (4, 8):
+            d.update(_result_arrays(f"cap{cap}_{m}", run_batch(mesh, batch, EngineConfig(mode=m, max_collisions=cap))))
+    np.savez_compressed(OUT / "scene_dup.npz", **d)
+    print("wrote dup cases")
+
+
 def layered_case(rs):
     """Small C4 analogue: 3 z-offset copies of a scene, stretched crossers, count mode."""
     from raysurf import EngineConfig, Mesh, SegmentBatch, run_batch
@@ -223,6 +264,9 @@ def main():
     if sys.argv[1:] == ["sortperm"]:
         sortperm_case(rs)
         return
+    if sys.argv[1:] == ["dup"]:
+        dup_cases(rs)
+        return
     from raysurf import morton
 
     # morton known answers straight from the reference (test_morton.py:33-74)
@@ -247,6 +291,7 @@ def main():
         tree_case(rs, n, n)
     layered_case(rs)
     sortperm_case(rs)
+    dup_cases(rs)
 
 
 if __name__ == "__main__":

@@ -15,10 +15,10 @@ TREE_FIELDS = (
     "internal_visit", "leaf_bounds", "leaf_triangle_id", "leaf_range_left",
     "leaf_range_right", "sorted_triangle_ids",
 )
-SCENES = ("c1", "s19", "s77", "full", "none")
+SCENES = ("c1", "s19", "s77", "full", "none", "dup")  # dup: every triangle repeated (equal Morton codes)
 SOUPS = ("17", "20")
 OVERFLOWS = ("ovf21", "ovf31", "ovfshort")
-TREE_SIZES = (1, 2, 3, 7, 8, 100, 5000)
+TREE_SIZES = (1, 2, 3, 7, 8, 100, 5000, "dup5")  # dup5: all codes equal (test_backends.py:70-84)
 
 
 def load(name: str) -> dict:

@@ -105,6 +105,10 @@ def test_cli_defaults_flags_and_report(tmp_path):
     assert r.returncode == 0, r.stderr
     assert f"rays     : {fx['starts'].shape[0]}" in r.stdout
     assert "phase timings (ms):" in r.stdout
+    # the reference's phase report (io_cli.py:52-61,254-263), every phase timed on device
+    for phase in ("ray sort", "ray boxes", "quantization", "encoding", "sorting", "reset",
+                  "construct", "query"):
+        assert f"  {phase:<12} " in r.stdout, (phase, r.stdout)
     assert np.array_equal(io_cli.read_count_results(tmp_path), expected(fx, "batch", "count")["counts"])
     # byte-determinism across repeats (test_io_cli.py)
     first = (tmp_path / io_cli.RESULT_FILE_COUNT).read_bytes()

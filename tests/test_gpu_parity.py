@@ -6,6 +6,7 @@ bit-exact as well (f64 Moller-Trumbore in the reference op order, no FMA).
 """
 
 import contextlib
+import ctypes as C
 from pathlib import Path
 
 import numpy as np
@@ -67,6 +68,32 @@ def test_fast_tree_matches_oracle(n):
     got = b200.DeviceTree(rs.Mesh.from_arrays(V, T), kind="fast").download()
     for f in TREE_FIELDS:
         assert np.array_equal(getattr(got, f), want[f]), f
+
+
+def test_duplicate_code_scene_trees_and_results():
+    """Runs of equal Morton codes (every triangle repeated): the device sort's
+    stability and the climb's id-XOR / position tie-breaks (_core.pyx:52-64)
+    against the reference's own tree, all 12 fields; the fast tree against
+    the oracle; results through both trees with resume (caps 4/8)."""
+    fx = load("scene_dup")
+    V, T = fx["vertices"], fx["triangles"]
+    mesh = rs.Mesh.from_arrays(V, T)
+    for tree in (b200.build_tree(mesh, fx["sorted_codes"], fx["sorted_ids"])[0],
+                 b200.DeviceTree(mesh, kind="reference").download()):
+        for f in TREE_FIELDS:
+            assert np.array_equal(getattr(tree, f), fx[f"tree_{f}"]), f
+    codes, ids = O.sorted_keys(V, T, "fast", 10)
+    assert len(np.unique(codes)) < len(codes)
+    want = O.build_tree(V, T, codes, ids)
+    got = b200.DeviceTree(mesh, kind="fast").download()
+    for f in TREE_FIELDS:
+        assert np.array_equal(getattr(got, f), want[f]), f
+    batch = rs.SegmentBatch.from_arrays(fx["starts"], fx["ends"])
+    for mode in MODES:
+        for tree in ("fast", "reference"):
+            for cap in (4, 8):
+                r = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree=tree, max_collisions=cap))
+                assert_result_fields(result_dict(r), expected(fx, f"cap{cap}", mode), f"dup {mode} {tree} {cap}")
 
 
 def test_large_tree_matches_oracle():
@@ -201,6 +228,40 @@ def test_tile_knobs_bitwise(name, mode, knobs):
             stack.enter_context(_lib.option(k, v))
         got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
     assert_result_fields(result_dict(got), want, f"{name} {mode} {knobs}")
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+@pytest.mark.parametrize("cap", [0, 64], ids=["sized", "overflow"])
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ("c1", "soup:17", "layered", "dup"))
+def test_collision_buffer_path(name, mode, cap, device):
+    """north_star (3), the collision-buffer manager (option fast_path=1): the
+    pair traversal appends (segment, leaf) candidates warp-aggregated into a
+    pre-sized device buffer, the exact pass reads it back; an overflowing
+    buffer (cand_cap=64 entries) is detected (the append counter runs past
+    the end, k_exact flags `dropped`) and the query re-launched with a
+    buffer of the claimed size -- on the host pipeline per chunk, on device
+    inputs from the graph replay's status.  Results stay bit-identical."""
+    fx = load(name if name == "layered" else
+              (f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}"))
+    mesh, batch = mesh_batch(fx, device)
+    want = expected(fx, "cap32" if name == "layered" else "batch", mode)
+    with _lib.option("fast_path", 1), _lib.option("cand_cap", cap):
+        for rep in range(3 if device else 1):  # direct, graph capture, graph replay
+            got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
+            assert_result_fields(result_dict(got), want, f"{name} {mode} buffer cap={cap} rep {rep}")
+        if cap and device:
+            st = (C.c_ulonglong * 8)()
+            _lib.lib().rs_last_status(st)
+            assert st[6] > cap and st[7] == 1, list(st)  # cand_count claimed past the end, dropped
+        dt = b200.DeviceTree(rs.Mesh.from_arrays(fx["vertices"], fx["triangles"]), kind="fast")
+        dense = dt.query_dense(fx["starts"], fx["ends"], mode, 32, 64, ref_semantics=False)
+        key = {"boolean": "detected", "count": "counts", "barycentric": "detected"}[mode]
+        flags = _np(dense[key])
+        if mode == "barycentric":
+            assert np.array_equal(np.nonzero(flags)[0], want["ray_index"])
+        else:
+            assert np.array_equal(flags, want["crossing" if mode == "boolean" else "counts"])
 
 
 def test_lean_build_matches_full_build():
@@ -367,6 +428,36 @@ def test_host_pipeline_pageable_outputs(chunk):
     assert_result_fields(got, expected(fx, "batch", "barycentric"), f"pageable chunk {chunk}")
 
 
+PHASES = ("ray boxes", "quantization", "encoding", "sorting", "reset", "construct", "query")
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+def test_timings_phase_keys(device):
+    """ResultSet.timings carries the reference's phase keys (engine.py:238-288)
+    measured with device events, on host inputs (chunked pipeline), device
+    inputs (direct launches, then a captured graph) and with sort_rays; the
+    plugin's build_tree returns real reset/construct times."""
+    sc = rs.generate_scene(3000, 200_000, 0.5, seed=8)
+    mesh, batch = sc.mesh, sc.segments
+    if device:
+        mesh = rs.Mesh.from_arrays(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.triangles).cuda())
+        batch = rs.SegmentBatch.from_arrays(torch.from_numpy(batch.starts).cuda(), torch.from_numpy(batch.ends).cuda())
+    for mode in MODES:
+        for rep in range(3):  # direct, capture, replay
+            r = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode))
+            assert set(r.timings) == set(PHASES), (mode, rep, r.timings)
+            assert all(v >= 0 for v in r.timings.values()) and r.timings["query"] > 0, r.timings
+            assert r.timings["encoding"] == 0.0  # fused into the quantization kernel
+        r = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, sort_rays=True))
+        assert set(r.timings) == set(PHASES) | {"ray sort"}, r.timings
+        r = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="reference"))
+        assert {"quantization", "sorting", "reset", "construct", "query"} <= set(r.timings), r.timings
+    fx = load("tree_5000")
+    _, reset_s, construct_s = b200.build_tree(rs.Mesh.from_arrays(fx["vertices"], fx["triangles"]),
+                                              fx["sorted_codes"], fx["sorted_ids"])
+    assert reset_s > 0 and construct_s > 0
+
+
 # ----------------------------------------------- full-size, property-based --
 
 @pytest.mark.parametrize("mode", MODES)
@@ -396,6 +487,84 @@ def test_c2_full_size_ground_truth(mode):
         assert np.array_equal(got.triangle_id[pos], want["triangle_id"])
         assert np.array_equal(got.point[pos], want["point"])
         assert np.array_equal(got.distance[pos], want["distance"])
+
+
+@pytest.fixture(scope="module")
+def c4_scene():
+    return rs.layered_scene(rs.generate_scene(29_284, 10_000_000, 0.5, seed=2022), layers=7)
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+@pytest.mark.parametrize("cap", (32, 8))
+def test_c4_full_size_ground_truth(c4_scene, cap, device):
+    """BASELINE configs[3] at full size: 7 stacked copies of the C2 terrain
+    (204,988 triangles) x 10M stretched segments, count mode at
+    max_collisions 32 and 8 (8 forces the reference's buffer resumption:
+    14 candidates per crossing segment).  Ground truth (7 per crossing
+    segment, 0 otherwise) for every segment, boolean and barycentric
+    consistency, plus a bitwise oracle check on a 200k sample."""
+    sc = c4_scene
+    mesh, batch = sc.mesh, sc.segments
+    if device:
+        mesh = rs.Mesh.from_arrays(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.triangles).cuda())
+        batch = rs.SegmentBatch.from_arrays(torch.from_numpy(batch.starts).cuda(), torch.from_numpy(batch.ends).cuda())
+    truth = sc.expected_crossings.astype(np.int32)
+    assert set(np.unique(truth).tolist()) == {0, 7}
+    got = rs.run_batch(mesh, batch, rs.EngineConfig(mode="count", max_collisions=cap))
+    assert np.array_equal(_np(got.counts), truth)
+    flags = rs.run_batch(mesh, batch, rs.EngineConfig(mode="boolean", max_collisions=cap))
+    assert np.array_equal(_np(flags.crossing), (truth > 0).astype(np.int32))
+    if not device:
+        bary = rs.run_batch(mesh, batch, rs.EngineConfig(mode="barycentric", max_collisions=cap))
+        assert np.array_equal(bary.ray_index, np.nonzero(truth)[0])
+    idx = np.random.default_rng(cap).choice(sc.segments.count, 200_000, replace=False)
+    idx.sort()
+    s, e = sc.segments.starts[idx], sc.segments.ends[idx]
+    for mode in MODES:
+        want = O.run_batch(sc.mesh.vertices, sc.mesh.triangles, s, e, mode=mode, max_coll=cap)
+        sub = rs.run_batch(sc.mesh, rs.SegmentBatch.from_arrays(s, e),
+                           rs.EngineConfig(mode=mode, max_collisions=cap))
+        assert_result_fields(result_dict(sub), want, f"C4 sample {mode} cap{cap}")
+        if mode == "barycentric" and not device:
+            pos = np.searchsorted(bary.ray_index, idx[want["ray_index"]])
+            for f in ("triangle_id", "point", "distance"):
+                assert np.array_equal(getattr(bary, f)[pos], want[f]), f
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+def test_c5_shard_ground_truth(device):
+    """BASELINE configs[4]'s mesh at full size (2,000,000 triangles, 1,002,001
+    vertices) with a 2M-segment shard of its distribution: every mode
+    against the generator's ground truth, plus a bitwise oracle check on a
+    100k sample (distance/point included)."""
+    sc = rs.generate_scene(2_000_000, 2_000_000, 0.5, seed=2022)
+    mesh, batch = sc.mesh, sc.segments
+    if device:
+        mesh = rs.Mesh.from_arrays(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.triangles).cuda())
+        batch = rs.SegmentBatch.from_arrays(torch.from_numpy(batch.starts).cuda(), torch.from_numpy(batch.ends).cuda())
+    truth = sc.expected_crossings.astype(np.int32)
+    res = {}
+    for mode in MODES:
+        r = res[mode] = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode))
+        if mode == "boolean":
+            assert np.array_equal(_np(r.crossing), truth)
+        elif mode == "count":
+            assert np.array_equal(_np(r.counts), truth)
+        else:
+            assert np.array_equal(_np(r.ray_index), np.nonzero(truth)[0])
+    idx = np.random.default_rng(5).choice(sc.segments.count, 100_000, replace=False)
+    idx.sort()
+    s, e = sc.segments.starts[idx], sc.segments.ends[idx]
+    for mode in MODES:
+        want = O.run_batch(sc.mesh.vertices, sc.mesh.triangles, s, e, mode=mode)
+        if mode == "barycentric":
+            full = res[mode]
+            pos = np.searchsorted(_np(full.ray_index), idx[want["ray_index"]])
+            for f in ("triangle_id", "point", "distance"):
+                assert np.array_equal(_np(getattr(full, f))[pos], want[f]), f
+        else:
+            key = "crossing" if mode == "boolean" else "counts"
+            assert np.array_equal(_np(getattr(res[mode], key))[idx], want[key])
 
 
 @pytest.mark.parametrize("mode", MODES)

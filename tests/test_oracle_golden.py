@@ -39,6 +39,25 @@ def test_tree_bit_identical(n):
         assert np.array_equal(tree[f], fx[f"tree_{f}"]), f
 
 
+def test_duplicate_code_scene_tree():
+    """scene_dup: every triangle repeated, so runs of equal Morton codes --
+    the sort's (code, id) order and the climb's id-XOR / position tie-breaks
+    (_core.pyx:52-64)."""
+    fx = load("scene_dup")
+    V, T = fx["vertices"], fx["triangles"]
+    codes, ids = O.sorted_keys(V, T)
+    assert len(np.unique(codes)) < len(codes)
+    assert np.array_equal(codes, fx["sorted_codes"]) and np.array_equal(ids, fx["sorted_ids"])
+    tree = O.build_tree(V, T, codes, ids)
+    for f in TREE_FIELDS:
+        assert np.array_equal(tree[f], fx[f"tree_{f}"]), f
+    args = (V, T, fx["starts"], fx["ends"])
+    for mode in MODES:
+        for cap in (4, 8):
+            got = O.run_batch(*args, mode=mode, max_coll=cap)
+            assert_result_fields(got, expected(fx, f"cap{cap}", mode), f"dup cap{cap} {mode}")
+
+
 @pytest.mark.parametrize("name", SCENES)
 @pytest.mark.parametrize("mode", MODES)
 def test_scene_results(name, mode):
