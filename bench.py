@@ -1,21 +1,34 @@
 #!/usr/bin/env python
-"""Headline benchmark: Mrays/s of run_batch (boolean mode, 10M segments x
-29,284-triangle terrain = BASELINE.json configs[1]) on N B200s.
+"""Headline benchmark: Mrays/s of run_batch on N B200s.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c3|c4|c5] [--no-cpu-baseline]
+                    [--config c2|c3|c4|c5] [--scaling weak|strong] [--no-cpu-baseline]
+
+Configs (BASELINE.json configs[1..4]; configs[0] is a parity-test case):
+  c2  boolean, 10M segments x 29,284-tri terrain        (the headline, default)
+  c3  barycentric, same inputs
+  c4  count, 10M long segments x 7 stacked layers (204,988 tris)
+  c5  boolean, 1B segments x 2M-tri terrain, sharded across the ranks; the
+      segments are generated on each rank's GPU (rs_generate_segments) --
+      24 GB would not come through PCIe from a numpy generator
 
 One step = one full run_batch on device-resident inputs: BVH build over the
-mesh (keys, sort, climb) + traversal/exact test of every segment + status
-read-back (TraversalStackOverflow check), exactly what a caller of
-`run_batch` gets.  Multi-GPU (torchrun, one rank per GPU): weak scaling, each
-rank runs its own full 10M-segment batch against its own replica of the mesh;
-no collective on the data path; value = all ranks' segments / max-over-ranks
-time.  Rank 0 prints one JSON line.
+mesh (keys, sort, climb) + traversal/exact test of every segment (+ ordered
+compaction for barycentric) + status read-back, i.e. exactly what a caller
+of `run_batch` gets.  Inputs (240 MB per 10M segments) are larger than L2.
 
-`--impl reference` times the reference's own CPU implementation
-(oracle/ref_engine.py over the reference's compiled _core kernel) on the
-host's cores, same config/metric; rank 0 only.
+Multi-GPU (torchrun, one rank per GPU, mesh and BVH replicated, segments
+sharded by contiguous ranges, no collective on the data path): c2-c4 scale
+weakly by default (each rank its own 10M-segment batch; --scaling strong
+splits the 10M), c5 strongly (the 1B job is split).  value = all ranks'
+segments / max-over-ranks device time.  The result gather to rank 0 (NCCL)
+is timed separately after the timed region and reported as "gather".
+
+`--impl reference` times the reference's own CPU implementation (the
+reference package's run_batch with its compiled Cython kernel, built from
+/root/reference into oracle/_ref by oracle/Makefile) on all host cores, on
+the same config, every step the full workload when that fits the time
+budget (c2/c3: yes), else a stated prefix sample; rank 0 only.
 """
 
 from __future__ import annotations
@@ -36,14 +49,30 @@ REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 METRIC = "Mrays/sec (boolean mode, 10M rays x 30k tris) at 1/2/4/8 B200 vs host-CPU ref"
-CONFIGS = {
-    # name: (n_tri, n_rays, mode, layers, description)
-    "c2": (29_284, 10_000_000, "boolean", 1, "boolean, 10M segments x 29,284-tri terrain (BASELINE configs[1])"),
-    "c3": (29_284, 10_000_000, "barycentric", 1, "barycentric, 10M x 29,284 (configs[2])"),
-    "c4": (29_284, 10_000_000, "count", 7, "count, 10M long segments x 7-layer 204,988 tris (configs[3])"),
-    "c5": (2_000_000, 10_000_000, "boolean", 1, "boolean, 10M-segment shard x 2M tris (configs[4] per-GPU shard)"),
-}
 SEED = 2022
+
+
+class Cfg:
+    def __init__(self, name, n_tri, n_rays, mode, layers, scaling, desc, units):
+        self.name, self.n_tri, self.n_rays, self.mode = name, n_tri, n_rays, mode
+        self.layers, self.scaling, self.desc = layers, scaling, desc
+        # SURVEY.md 8(d) algorithmic units per segment (reference-tree counts):
+        # B_ray compulsory HBM bytes, W32 FP32 lane-ops (12 x internal
+        # visits), W64 FP64 ops (55 x exact tests)
+        self.b_ray, self.w32, self.w64 = units
+
+
+CONFIGS = {
+    "c2": Cfg("c2", 29_284, 10_000_000, "boolean", 1, "weak",
+              "boolean, 10M segments x 29,284-tri terrain (BASELINE configs[1])", (28, 404, 41)),
+    "c3": Cfg("c3", 29_284, 10_000_000, "barycentric", 1, "weak",
+              "barycentric, 10M x 29,284 (configs[2])", (36, 404, 55)),
+    "c4": Cfg("c4", 29_284, 10_000_000, "count", 7, "weak",
+              "count, 10M long segments x 7-layer 204,988 tris (configs[3])", (28, 881, 385)),
+    "c5": Cfg("c5", 2_000_000, 1_000_000_000, "boolean", 1, "strong",
+              "boolean, 1B segments x 2M-tri terrain, sharded across the GPUs (configs[4])",
+              (28, 1939, 41)),
+}
 
 
 def dist_env():
@@ -51,22 +80,74 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def make_scene(cfg):
+def make_scene(cfg: Cfg, n_rays=None):
     import paper_2209_02878_b200 as rs
 
-    n_tri, n_rays, _, layers, _ = CONFIGS[cfg]
-    sc = rs.generate_scene(n_tri, n_rays, 0.5, seed=SEED)
-    if layers > 1:
-        sc = rs.layered_scene(sc, layers=layers)
+    sc = rs.generate_scene(cfg.n_tri, cfg.n_rays if n_rays is None else n_rays, 0.5, seed=SEED)
+    if cfg.layers > 1:
+        sc = rs.layered_scene(sc, layers=cfg.layers)
     return sc
 
 
-def measured_peaks():
+def peaks():
+    """HBM GB/s and FP32/FP64 op rates of this GPU.  HBM from the driver's
+    MEASURED_PEAKS.json (burst copy); FP32/FP64 from the SM count x lanes x
+    the measured max SM clock (B200: 128 FP32 lanes, 64 FP64 lanes per SM)."""
     p = REPO / "MEASURED_PEAKS.json"
+    hbm, mhz, kind = 6650.0, 1965.0, "fallback (B200_PROFILING.md)"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        hbm, mhz, kind = float(d["hbm_gbs"]), float(d.get("sm_max_mhz", mhz)), "measured"
+    sms = 148
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            sms = torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        pass
+    return {"hbm_gbs": hbm, "fp32_tops": sms * 128 * mhz * 1e6 / 1e12,
+            "fp64_tops": sms * 64 * mhz * 1e6 / 1e12, "kind": kind, "sms": sms, "mhz": mhz}
+
+
+def roofline(cfg: Cfg, rays_per_s_kernel: float, rays_per_s_step: float, kernel: str):
+    """ceiling = min(HBM/B_ray, FP32/W32, FP64/W64); the
+    binding resource is the label, `achieved`/`peak` are in its unit for the
+    dominant kernel, and every resource's fraction is listed."""
+    pk = peaks()
+    ceilings = {"hbm": pk["hbm_gbs"] * 1e9 / cfg.b_ray,
+                "fp32": pk["fp32_tops"] * 1e12 / cfg.w32,
+                "fp64": pk["fp64_tops"] * 1e12 / cfg.w64}
+    bound = min(ceilings, key=ceilings.get)
+    per_unit = {"hbm": (cfg.b_ray / 1e9, pk["hbm_gbs"], "GB/s"),
+                "fp32": (cfg.w32 / 1e12, pk["fp32_tops"], "Tlane-op/s"),
+                "fp64": (cfg.w64 / 1e12, pk["fp64_tops"], "Tflop/s")}
+    res = {}
+    for r, (scale, peak, unit) in per_unit.items():
+        a = rays_per_s_kernel * scale
+        res[r] = {"achieved": round(a, 3), "peak": round(peak, 1), "unit": unit,
+                  "frac": round(a / peak, 4)}
+    scale, peak, unit = per_unit[bound]
+    traffic = None
+    tf = REPO / "profiles" / f"traffic_{cfg.name}.json"
+    tinfo = None
+    if tf.exists():
+        tinfo = json.loads(tf.read_text())
+        if tinfo.get("kernel") == kernel:
+            traffic = tinfo.get("dram_bytes_per_launch")
+    return {
+        "bound": bound, "achieved": res[bound]["achieved"], "peak": res[bound]["peak"], "unit": unit,
+        "frac": res[bound]["frac"], "traffic": traffic, "kernel": kernel,
+        "ceiling_grays": round(ceilings[bound] / 1e9, 2),
+        "kernel_grays": round(rays_per_s_kernel / 1e9, 3),
+        "step_frac": round(rays_per_s_step / ceilings[bound], 4),
+        "resources": res,
+        "step_dram_bytes": tinfo.get("step_dram_bytes") if tinfo else None,
+        "units": {"B_ray": cfg.b_ray, "W32": cfg.w32, "W64": cfg.w64,
+                  "source": "SURVEY.md 8(d), reference-tree visit/test counts"},
+        "peaks": pk["kind"] + "; FP32/FP64 = SMs x lanes x max SM clock",
+        "traffic_source": tinfo.get("source") if tinfo else None,
+    }
 
 
 class ClockSampler:
@@ -124,64 +205,136 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_reference(cfg, steps, warmup, sc=None):
-    """Reference CPU run_batch on this host; returns (Mrays/s, info)."""
+# --------------------------------------------------------------- reference --
+
+def _ref_runner():
+    """run_batch of the reference package itself (oracle/_ref/refpkg: the
+    reference's Python sources + its _core.pyx compiled by oracle/Makefile),
+    called through its public API; else the restated orchestration over the
+    compiled kernel, else the C port."""
+    refsrc = REPO / "oracle" / "_ref" / "refpkg" / "src"
+    if (refsrc / "raysurf").is_dir():
+        sys.path.insert(0, str(refsrc))
+        import raysurf
+
+        if "compiled" in raysurf.available_backends():
+            def run(V, T, s, e, mode, workers):
+                return raysurf.run_batch(raysurf.Mesh.from_arrays(V, T),
+                                         raysurf.SegmentBatch.from_arrays(s, e),
+                                         raysurf.EngineConfig(mode=mode, workers=workers,
+                                                              backend="compiled"))
+            return run, "reference", "raysurf.run_batch (reference package, compiled backend)"
     from oracle import ref_engine
 
+    def run(V, T, s, e, mode, workers):
+        return ref_engine.run_batch(V, T, s, e, mode, workers=workers)
+    return run, ref_engine.kind(), "oracle/ref_engine.py over the reference kernel"
+
+
+def cpu_inputs(cfg: Cfg, n_max: int, sc=None):
+    """Host mesh + the first n_max segments of the config's batch."""
+    if cfg.name == "c5":
+        from oracle import gen_oracle
+        import paper_2209_02878_b200 as rs
+
+        mesh = sc.mesh if sc is not None else rs.generate_scene(cfg.n_tri, 0, 0.5, seed=SEED).mesh
+        s, e, _ = gen_oracle.generate_segments(mesh.vertices, mesh.triangles, n_max, seed=SEED)
+        return mesh.vertices, mesh.triangles, s, e
     sc = sc or make_scene(cfg)
-    mode = CONFIGS[cfg][2]
-    V, T = sc.mesh.vertices, sc.mesh.triangles
-    s, e = sc.segments.starts, sc.segments.ends
+    return (sc.mesh.vertices, sc.mesh.triangles, sc.segments.starts[:n_max], sc.segments.ends[:n_max])
+
+
+def cpu_reference(cfg: Cfg, steps: int, warmup: int, budget_s: float, sc=None,
+                  sample_cap: int = 10_000_000):
+    """Time the reference on this host.  Every step runs the full config's
+    batch when (steps + warmup) of them fit `budget_s`; otherwise a prefix of
+    min(full, `sample_cap`) segments (c5: a 10M-segment shard of the 1B job,
+    rows from the same generator as the GPU arm's), with fewer steps (>= 2)
+    when even that overruns.  For a sample, the full config's rate is also
+    extrapolated linearly from the reference's own phase timings (fixed
+    build phases once + per-segment query cost x the full count).
+    Returns (Mrays/s, info)."""
+    run, kind, how = _ref_runner()
     workers = os.cpu_count() or 1
-    # bounded sample: keep the whole leg within ~30 s of CPU time
+    n_full = cfg.n_rays
+    probe_n = min(n_full, 1_000_000)
+    V, T, s, e = cpu_inputs(cfg, probe_n, sc)
     t0 = time.perf_counter()
-    ref_engine.run_batch(V, T, s[:200_000], e[:200_000], mode, workers=workers)
-    per_ray = (time.perf_counter() - t0) / 200_000
-    n = s.shape[0]
-    budget = 30.0 / max(1, steps + warmup)
-    if per_ray * n > budget:
-        n = max(100_000, int(budget / per_ray))
-    s, e = s[:n], e[:n]
+    run(V, T, s, e, cfg.mode, workers)
+    t_probe = time.perf_counter() - t0
+    # the probe's time counted as per-segment cost (its build included):
+    # a conservative estimate of a step
+    est = lambda k: t_probe * max(1.0, k / probe_n)  # noqa: E731
+    n = n_full if est(n_full) * (steps + warmup) <= budget_s else min(n_full, sample_cap)
+    if est(n) * (steps + warmup) > budget_s:
+        steps = max(2, int(budget_s / est(n)) - warmup)
+    if n != probe_n:
+        V, T, s, e = cpu_inputs(cfg, n, sc)
     for _ in range(warmup):
-        ref_engine.run_batch(V, T, s, e, mode, workers=workers)
-    times = []
+        run(V, T, s, e, cfg.mode, workers)
+    times, phases = [], []
     for _ in range(steps):
         t0 = time.perf_counter()
-        ref_engine.run_batch(V, T, s, e, mode, workers=workers)
+        r = run(V, T, s, e, cfg.mode, workers)
         times.append(time.perf_counter() - t0)
-    best = min(times)
-    info = {"cores": workers, "kind": ref_engine.kind(),
-            "sample": f"first {n} of the {CONFIGS[cfg][1]} segments of config {cfg}, "
-                      f"full mesh, best of {steps} run_batch calls (workers={workers})",
-            "ms_per_step": 1e3 * float(np.mean(times))}
+        phases.append(getattr(r, "timings", None) or {})
+    k = int(np.argmin(times))
+    best = times[k]
+    info = {"cores": workers, "kind": kind, "n": n, "same_config": n == n_full, "steps": steps,
+            "sample": (f"{'all' if n == n_full else 'first'} {n} of the {n_full} segments of config "
+                       f"{cfg.name}, full mesh, best of {steps} run_batch calls (workers={workers}; {how})"),
+            "ms_per_step": 1e3 * float(np.mean(times)), "ms_best": 1e3 * best,
+            "phases_s": {p: round(v, 4) for p, v in phases[k].items()}}
+    if n != n_full and "query" in phases[k]:
+        per_seg = (phases[k]["query"] + phases[k].get("ray boxes", 0.0)) / n
+        fixed = max(0.0, best - per_seg * n)
+        info["extrapolated_full_config"] = {
+            "value": round(n_full / (fixed + per_seg * n_full) / 1e6, 4), "unit": "Mrays/s",
+            "how": f"fixed phases {fixed:.3f} s once + (query + ray boxes) {per_seg * 1e9:.1f} ns/segment "
+                   f"x {n_full} segments, from the reference's ResultSet.timings of the best step"}
     try:
-        model = [l for l in open("/proc/cpuinfo") if l.startswith("model name")][0].split(":")[1].strip()
+        model = [ln for ln in open("/proc/cpuinfo") if ln.startswith("model name")][0].split(":")[1].strip()
         info["cpu"] = model
     except Exception:
         pass
     return n / best / 1e6, info
 
 
+def config_dict(cfg: Cfg, world: int, scaling: str, n_per_rank: int):
+    return {"workload": cfg.desc, "mode": cfg.mode, "n_triangles": cfg.n_tri * cfg.layers,
+            "segments_total": n_per_rank * world if scaling == "weak"
+            else cfg.n_rays, "segments_per_gpu": n_per_rank,
+            "l2": "inputs larger than L2 (24 B/segment)",
+            "parallelism": f"segment shards x{world}, mesh/BVH replicated"}
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg = args.config
-    value, info = cpu_reference(cfg, args.steps, args.warmup)
+    cfg = CONFIGS[args.config]
+    value, info = cpu_reference(cfg, args.steps, args.warmup, budget_s=float(os.environ.get(
+        "RS_REF_BUDGET_S", "240")))
+    scaling = args.scaling or cfg.scaling
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Mrays/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": info["steps"], "warmup": args.warmup,
         "ms_per_step": round(info["ms_per_step"], 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 boxes / f64 exact test",
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32 boxes / f64 exact test",
         "data": "synthetic (generate_scene seed 2022)",
-        "config": {"workload": CONFIGS[cfg][4], "mode": CONFIGS[cfg][2]},
+        "config": config_dict(cfg, 1, scaling, info["n"]),
         "cpu_baseline": {"value": round(value, 4), "unit": "Mrays/s", "cores": info["cores"],
-                         "kind": info["kind"], "sample": info["sample"]},
+                         "kind": info["kind"], "sample": info["sample"],
+                         "same_config": info["same_config"], "cpu": info.get("cpu"),
+                         "phases_s": info["phases_s"],
+                         "extrapolated_full_config": info.get("extrapolated_full_config")},
         "e2e": {"value": round(value, 4), "unit": "Mrays/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
+
+# -------------------------------------------------------------------- ours --
 
 def main():
     ap = argparse.ArgumentParser()
@@ -190,13 +343,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--config", default="c2", choices=tuple(CONFIGS))
+    ap.add_argument("--scaling", default=None, choices=("weak", "strong"))
+    ap.add_argument("--rays", type=int, default=0, help="override the config's total segment count")
     ap.add_argument("--tree", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--presort", action="store_true",
-                    help="experiment: Morton-order the segments on the host before upload")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.rays:
+        CONFIGS[args.config].n_rays = args.rays
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -205,27 +360,38 @@ def main():
 
     import paper_2209_02878_b200 as rs
     from paper_2209_02878_b200 import _lib
+    from paper_2209_02878_b200.parallel import shard_range
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = args.config
-    n_tri, n_rays, mode, layers, desc = CONFIGS[cfg]
-    sc = make_scene(cfg)
-    mesh_h, seg_h = sc.mesh, sc.segments
-    if args.presort:
-        seg_h, perm = rs.sort_segments_by_morton(seg_h)
-        sc.expected_crossings = sc.expected_crossings[perm]
+    cfg = CONFIGS[args.config]
+    scaling = args.scaling or cfg.scaling
+    mode = cfg.mode
     dev = torch.device("cuda", local)
-    mesh_d = rs.Mesh.from_arrays(torch.from_numpy(mesh_h.vertices).to(dev),
-                                 torch.from_numpy(mesh_h.triangles).to(dev))
-    seg_d = rs.SegmentBatch.from_arrays(torch.from_numpy(seg_h.starts).to(dev),
-                                        torch.from_numpy(seg_h.ends).to(dev))
+    generated = cfg.name == "c5"
+    sc = None
+    if generated:
+        mesh_h = rs.generate_scene(cfg.n_tri, 0, 0.5, seed=SEED).mesh
+        lo, hi = shard_range(cfg.n_rays, rank, world) if scaling == "strong" else \
+            (rank * cfg.n_rays, (rank + 1) * cfg.n_rays)
+        mesh_d = rs.Mesh.from_arrays(torch.from_numpy(mesh_h.vertices).to(dev),
+                                     torch.from_numpy(mesh_h.triangles).to(dev))
+        seg_d, truth_d = rs.scene.generate_segments_device(mesh_d, hi - lo, 0.5, seed=SEED, first=lo,
+                                                           device=dev)
+    else:
+        sc = make_scene(cfg)
+        mesh_h, seg_h = sc.mesh, sc.segments
+        lo, hi = shard_range(cfg.n_rays, rank, world) if scaling == "strong" else (0, cfg.n_rays)
+        mesh_d = rs.Mesh.from_arrays(torch.from_numpy(mesh_h.vertices).to(dev),
+                                     torch.from_numpy(mesh_h.triangles).to(dev))
+        seg_d = rs.SegmentBatch.from_arrays(torch.from_numpy(seg_h.starts[lo:hi]).to(dev),
+                                            torch.from_numpy(seg_h.ends[lo:hi]).to(dev))
+        truth_d = torch.from_numpy(sc.expected_crossings[lo:hi]).to(dev)
     n = seg_d.count
     config = rs.EngineConfig(mode=mode, tree=args.tree)
     kind = config.resolved_tree()
-    out = {}
     if mode == "barycentric":
         out = {"ray": torch.empty(n, dtype=torch.int32, device=dev),
                "dist": torch.empty(n, dtype=torch.float32, device=dev),
@@ -246,19 +412,16 @@ def main():
     for _ in range(args.warmup):
         res = step()
     # correctness gate on the benchmarked output: generated ground truth
-    truth = sc.expected_crossings
-    if os.environ.get("RS_BENCH_NOCHECK"):  # timing experiments on deliberately wrong builds only
-        truth = None
-    if truth is None:
-        pass
-    elif mode == "boolean":
-        assert np.array_equal(res.crossing.cpu().numpy(), truth.astype(np.int32))
-    elif mode == "count":
-        assert np.array_equal(res.counts.cpu().numpy(), truth.astype(np.int32))
-    else:
-        assert np.array_equal(res.ray_index.cpu().numpy(), np.nonzero(truth)[0])
+    if not os.environ.get("RS_BENCH_NOCHECK"):  # timing experiments on deliberately wrong builds only
+        if mode == "boolean":
+            assert torch.equal(res.crossing, truth_d.to(torch.int32))
+        elif mode == "count":
+            assert torch.equal(res.counts, truth_d.to(torch.int32))
+        else:
+            assert torch.equal(res.ray_index.to(torch.int64),
+                               torch.nonzero(truth_d).flatten())
 
-    build_ms, query_ms, hot_ms = [], [], []
+    hot_ms = []
     bms, qms, hms = C.c_float(), C.c_float(), C.c_float()
     stream = torch.cuda.current_stream()
     if world > 1:
@@ -275,8 +438,6 @@ def main():
             step()
             if timing_level:
                 lib.rs_last_timings(C.byref(bms), C.byref(qms), C.byref(hms))
-                build_ms.append(bms.value)
-                query_ms.append(qms.value)
                 hot_ms.append(hms.value)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -284,31 +445,19 @@ def main():
         time.sleep(0.05)
     launches = lib.rs_kernel_launches() - launches0
     hot_kernel = lib.rs_hot_kernel().decode()
-    if timing_level != 1:
-        # the build/query split: a few extra steps with the phase events on
-        # (outside the timed region)
-        lib.rs_set_timing(1)
-        build_ms, query_ms = [], []
-        for _ in range(5):
-            step()
-            lib.rs_last_timings(C.byref(bms), C.byref(qms), C.byref(hms))
-            build_ms.append(bms.value)
-            query_ms.append(qms.value)
-            if not timing_level:
-                hot_ms.append(hms.value)
-        lib.rs_set_timing(0)
-    stage_ms = None
-    if os.environ.get("RS_BENCH_STAGES"):
-        # diagnostics: per-stage marks on both streams (outside the timed region)
-        lib.rs_set_timing(3)
-        arr = (C.c_float * 16)()
-        rows = []
-        for _ in range(7):
-            step()
-            lib.rs_stage_times(arr, 16)
-            rows.append(list(arr))
-        lib.rs_set_timing(0)
-        stage_ms = [round(float(np.median([r[k] for r in rows[2:]])), 4) for k in range(16)]
+    # the build/query split and the reference's phase keys: a few extra
+    # steps with the phase events on (outside the timed region)
+    lib.rs_set_timing(1)
+    build_ms, query_ms, phases = [], [], []
+    for _ in range(5):
+        r = step()
+        lib.rs_last_timings(C.byref(bms), C.byref(qms), C.byref(hms))
+        build_ms.append(bms.value)
+        query_ms.append(qms.value)
+        phases.append(r.timings)
+        if not timing_level:
+            hot_ms.append(hms.value)
+    lib.rs_set_timing(0)
     if world > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
@@ -319,77 +468,103 @@ def main():
     total_rays = n * world * args.steps
     value = total_rays / (max_ms / 1e3) / 1e6
 
-    # e2e through the public API with host (pinned) buffers
+    # result gather to rank 0 over NCCL (outside the timed region)
+    gather = None
+    if world > 1 and mode != "barycentric":
+        flat = out["flags"]
+        bufs = [torch.empty_like(flat) for _ in range(world)] if rank == 0 else None
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        dist.gather(flat, gather_list=bufs, dst=0)
+        dist.barrier()
+        g0.record(stream)
+        reps = 5
+        for _ in range(reps):
+            dist.gather(flat, gather_list=bufs, dst=0)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gt = torch.tensor([g0.elapsed_time(g1) / reps], dtype=torch.float64, device=dev)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather = {"ms": round(float(gt.item()), 4), "bytes_to_rank0": 4 * n * (world - 1),
+                  "how": "dist.gather (NCCL) of every rank's int32 flags to rank 0, timed after "
+                         "the timed region, max over ranks"}
+
+    # e2e through the public API with host buffers (pinned, then pageable)
     e2e = None
     if not args.no_e2e:
-        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+        if generated:  # a 10M-segment sample of the generated batch, copied to the host
+            m = min(n, 10_000_000)
+            s_host, e_host = seg_d.starts[:m].cpu().numpy(), seg_d.ends[:m].cpu().numpy()
+            e2e_note = f"sample: first {m} of this rank's {n} generated segments"
+        else:
+            m = n
+            s_host, e_host = seg_h.starts[lo:hi], seg_h.ends[lo:hi]
+            e2e_note = "the whole per-rank batch"
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
         mesh_p = rs.Mesh.from_arrays(pin(mesh_h.vertices), pin(mesh_h.triangles))
-        seg_p = rs.SegmentBatch.from_arrays(pin(seg_h.starts), pin(seg_h.ends))
-        if os.environ.get("RS_E2E_CHUNK"):  # pipeline chunk experiments
-            import dataclasses
-            config = dataclasses.replace(config, chunk_rays=int(os.environ["RS_E2E_CHUNK"]))
-        for _ in range(2):
-            r = rs.run_batch(mesh_p, seg_p, config)
-        ts = []
-        for _ in range(max(3, args.steps // 4)):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = rs.run_batch(mesh_p, seg_p, config)
-            ts.append(time.perf_counter() - t0)
-        e2e_t = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        h2d = 24 * n + 12 * mesh_h.num_vertices + 12 * mesh_h.num_triangles
-        d2h = 4 * n if mode != "barycentric" else 24 * r.num_crossing()
-        e2e = {"value": round(n * world / e2e_t.item() / 1e6, 3), "unit": "Mrays/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": round(1e3 * e2e_t.item(), 3),
-               "path": "run_batch(numpy pinned) -> rs_run_batch_host: chunked H2D/query/D2H"}
+        seg_p = rs.SegmentBatch.from_arrays(pin(s_host), pin(e_host))
+        seg_pg = rs.SegmentBatch.from_arrays(np.array(s_host), np.array(e_host))
 
-    # roofline of the dominant kernel (the traversal): SURVEY 8(d) compulsory
-    # bytes per segment x segments per launch / its CUDA-event duration
-    b_ray = 24 + (4 if mode != "barycentric" else 24 * 0.5)
+        def e2e_time(mesh_x, seg_x, reps):
+            for _ in range(2):
+                r = rs.run_batch(mesh_x, seg_x, config)
+            ts = []
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                r = rs.run_batch(mesh_x, seg_x, config)
+                ts.append(time.perf_counter() - t0)
+            tt = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return tt.item(), r
+
+        t_pin, r = e2e_time(mesh_p, seg_p, max(3, min(args.steps // 4, 25)))
+        t_pg, _ = e2e_time(mesh_h, seg_pg, 3)
+        h2d = 24 * m + 12 * mesh_h.num_vertices + 12 * mesh_h.num_triangles
+        d2h = 4 * m if mode != "barycentric" else 24 * r.num_crossing()
+        e2e = {"value": round(m * world / t_pin / 1e6, 3), "unit": "Mrays/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(1e3 * t_pin, 3),
+               "pageable_value": round(m * world / t_pg / 1e6, 3),
+               "pageable_ms_per_step": round(1e3 * t_pg, 3),
+               "path": "run_batch(numpy, pinned) -> rs_run_batch_host: chunked H2D/query/D2H; "
+                       "pageable_*: the same call on plain numpy arrays",
+               "segments": e2e_note}
+
     q_ms = float(np.mean(query_ms))
     h_ms = float(np.mean(hot_ms)) if hot_ms and min(hot_ms) > 0 else q_ms
-    achieved = b_ray * n / (h_ms / 1e3) / 1e9
-    peak, peak_kind = measured_peaks()
-    traffic = None
-    tf = REPO / "profiles" / f"traffic_{cfg}.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    phase_keys = sorted({k for p in phases for k in p})
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mrays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 boxes / f64 exact test", "data": "synthetic (generate_scene seed 2022, "
-        "same generator and draws as the reference)",
-        "config": {"workload": desc, "mode": mode, "n_triangles": mesh_h.num_triangles,
-                   "segments_per_gpu": n, "tree": kind, "l2": "inputs (240 MB) larger than L2",
-                   "parallelism": f"ray shards x{world}, mesh/BVH replicated"},
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "f32 boxes / f64 exact test",
+        "data": ("synthetic: generate_scene(2M tris, seed 2022) mesh; segments generated on device "
+                 "(rs_generate_segments: the reference generator's distribution, Philox keyed by "
+                 "(seed, global row))") if generated else
+                "synthetic (generate_scene seed 2022, same generator and draws as the reference)",
+        "config": config_dict(cfg, world, scaling, n),
+        "tree": kind,
         "phase_ms": {"build": round(float(np.mean(build_ms)), 4), "query": round(q_ms, 4),
-                     "source": "traversal_kernel: CUDA events in the timed region; build/query: "
-                               "5 instrumented steps after it",
-                     "traversal_kernel": round(h_ms, 4)},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": hot_kernel, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_segment": b_ray},
+                     "traversal_kernel": round(h_ms, 4),
+                     "reference_phases": {k: round(1e3 * float(np.mean([p.get(k, 0.0) for p in phases])), 4)
+                                          for k in phase_keys},
+                     "source": "traversal_kernel: CUDA events in the timed region; the rest: "
+                               "5 instrumented steps after it"},
+        "roofline": roofline(cfg, n / (h_ms / 1e3), value * 1e6 / world, hot_kernel),
         "gpu_launches": int(launches),
         "clocks": clocks.summary(t_start, t_end + 0.02),
     }
-    if stage_ms is not None:
-        line["phase_ms"]["stages"] = stage_ms
+    if gather:
+        line["gather"] = gather
     if e2e:
         line["e2e"] = e2e
-    if os.environ.get("RS_DEBUG_STATUS"):
-        st = (C.c_ulonglong * 8)()
-        lib.rs_last_status(st)
-        line["debug_status"] = dict(zip(["bad", "internal", "hits", "tile_counter", "visits", "mts",
-                                         "cand_count", "pad"], [int(x) for x in st]))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, info = cpu_reference(cfg, 2, 1, sc=sc)
+        v, info = cpu_reference(cfg, 2, 1, budget_s=30.0, sc=sc if not generated else None)
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "Mrays/s", "cores": info["cores"],
-                                "kind": info["kind"], "sample": info["sample"]}
+                                "kind": info["kind"], "sample": info["sample"], "cpu": info.get("cpu"),
+                                "extrapolated_full_config": info.get("extrapolated_full_config")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

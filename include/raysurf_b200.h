@@ -125,6 +125,21 @@ RS_API int rs_query_stats(const rs_tree *tree, const float *d_starts, const floa
 RS_API int rs_sort_segments(const float *d_starts, const float *d_ends, int64_t n,
                             float *d_out_starts, float *d_out_ends, int64_t *d_perm, void *stream);
 
+/* Synthetic terrain segments generated on device (BASELINE configs[4]: 1B
+ * segments cannot come through PCIe from the reference's numpy generator,
+ * raysurf/oracle.py:167-274).  Restates that generator's distribution
+ * (oracle.py:228-271) with a Philox-4x32-10 stream keyed by (seed, global
+ * segment index): rows [first, first + n) of the batch are written to
+ * d_starts/d_ends (n,3) f32, and d_flags (n,) u8 (may be NULL) receives the
+ * ground truth (1 = crosses the terrain exactly once, 0 = misses).  Any
+ * sharding of a batch yields the same rows.  The mesh is a generate_scene
+ * height field: z_lo/z_hi its vertex z range, x_hi/y_hi = grid extent + 1.
+ * Stream-ordered; does not synchronise. */
+RS_API int rs_generate_segments(const float *d_verts, const int32_t *d_tris, int64_t n_t,
+                                double z_lo, double z_hi, double x_hi, double y_hi,
+                                double crossing_fraction, uint64_t seed, int64_t first, int64_t n,
+                                float *d_starts, float *d_ends, uint8_t *d_flags, void *stream);
+
 /* All-pairs baseline (no BVH), device arrays, dense outputs as rs_query. */
 RS_API int rs_baseline(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
                 const float *d_starts, const float *d_ends, int64_t n_r, int mode,

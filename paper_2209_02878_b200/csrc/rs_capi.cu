@@ -676,9 +676,12 @@ struct FastScratch {
 // buffer -> exact pass; default 0: the binned tile traversal.
 static bool buffer_path() { return rs::fast_path() == 1; }
 
-static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cudaStream_t s) {
+// `sized`: a re-launch with the capacity the overflowing launch claimed (the
+// cand_cap test override applies to first launches only).
+static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cudaStream_t s,
+                      bool sized = false) {
     if (!buffer_path()) cap = kCandChunk;  // the sorted path has no collision buffer
-    else if (rs::cand_cap_override() > 0) cap = rs::cand_cap_override();
+    else if (rs::cand_cap_override() > 0 && !sized) cap = rs::cand_cap_override();
     cap = ((cap + kCandChunk - 1) / kCandChunk) * kCandChunk;
     const bool bary = mode == kBarycentric;
     size_t total = 256;
@@ -813,7 +816,7 @@ static int fast_query(const rs_tree* t, const float* d_s, const float* d_e, int6
     FastScratch f;
     long long cap = 2ll * n_r + 4096;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        int rc = fast_alloc(f, n_r, mode, cap, s);
+        int rc = fast_alloc(f, n_r, mode, cap, s, attempt > 0);
         if (rc) return rc;
         rc = fast_launch(t, d_s, d_e, n_r, mode, o, f, stats, s);
         if (!rc) rc = read_status(f.st, s, h);
@@ -1116,6 +1119,101 @@ static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d
     return rc ? rc : rc2;
 }
 
+// Batches above kDeviceChunk segments (BASELINE configs[4]: 1B segments per
+// job, up to 1B / n_gpus per rank) are processed as one build and a loop of
+// chunk queries on the caller's stream: the scratch (32-B records, keys,
+// bins) is sized for one chunk and reused, each chunk leaves its status in
+// its own slot, the barycentric rows of consecutive chunks compact through
+// one device row counter (ascending ray index across the whole batch), and
+// every chunk chooses its traversal kernel by the whole batch's density
+// (set_batch_rays).  One synchronisation at the end.
+// Option "device_chunk" (multiple of 1024) lowers it for tests.
+static std::atomic<long long> g_device_chunk{1ll << 27};
+
+static int run_device_chunked(const float* d_verts, int64_t n_v, const int32_t* d_tris,
+                              int64_t n_t, const float* d_starts, const float* d_ends, int64_t n_r,
+                              int mode, int32_t* d_flags, int32_t* d_ray, float* d_dist,
+                              int32_t* d_tri, float* d_pt, int64_t* n_hits, int64_t* bad,
+                              cudaStream_t s) {
+    const int64_t kDeviceChunk = g_device_chunk.load();
+    const int64_t nchunks = (n_r + kDeviceChunk - 1) / kDeviceChunk;
+    const bool bary = mode == kBarycentric;
+    rs_tree* t = nullptr;
+    int rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, s, &t, nullptr, true);
+    if (rc) return rc;
+    struct Guard {
+        rs_tree* t;
+        char* blk = nullptr;
+        FastScratch f;
+        cudaStream_t s;
+        ~Guard() {
+            if (f.blk) dfree(f.blk, s);
+            if (blk) dfree(blk, s);
+            if (t) rs_free(t, s);
+        }
+    } g{t, nullptr, {}, s};
+    const size_t st_bytes = align256(sizeof(RsStatus) * nchunks);
+    CK(dmalloc(reinterpret_cast<void**>(&g.blk), st_bytes + 256, s));
+    CK(cudaMemsetAsync(g.blk, 0, st_bytes + 256, s));
+    RsStatus* st = reinterpret_cast<RsStatus*>(g.blk);
+    unsigned long long* rows = reinterpret_cast<unsigned long long*>(g.blk + st_bytes);
+    rc = fast_alloc(g.f, std::min(n_r, kDeviceChunk), mode, 2 * kDeviceChunk + 4096, s);
+    if (rc) return rc;
+    rs::set_batch_rays(n_r);
+    ev_record(1, s);
+    for (int64_t k = 0; k < nchunks && !rc; ++k) {
+        const int64_t lo = k * kDeviceChunk, cnt = std::min(kDeviceChunk, n_r - lo);
+        g.f.st = st + k;
+        FastOut o;
+        o.ray_offset = lo;
+        if (bary) {
+            o.c_ray = d_ray; o.c_dist = d_dist; o.c_tri = d_tri; o.c_pt = d_pt;
+            o.row_base = rows;
+        } else {
+            o.flags = d_flags + lo;
+        }
+        rc = fast_bin(t, d_starts + 3 * lo, d_ends + 3 * lo, cnt, mode, o, g.f, s);
+        if (!rc) rc = fast_trav(t, d_starts + 3 * lo, d_ends + 3 * lo, cnt, mode, o, g.f, false, s,
+                                false, false);
+    }
+    ev_record(2, s);
+    rs::set_batch_rays(0);
+    if (rc) return rc;
+    std::vector<RsStatus> h((size_t)nchunks);
+    CK(cudaMemcpyAsync(h.data(), st, sizeof(RsStatus) * nchunks, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    unsigned long long hits = 0, internal = 0;
+    for (const RsStatus& x : h) {
+        hits += x.hits;
+        internal |= x.internal;
+    }
+    if (internal) {
+        // a fast-path walk exceeded its capacity (never expected): the whole
+        // batch again with the binary kernels, chunk by chunk
+        hits = 0;
+        CK(cudaMemsetAsync(rows, 0, sizeof(unsigned long long), s));
+        for (int64_t k = 0; k < nchunks; ++k) {
+            const int64_t lo = k * kDeviceChunk, cnt = std::min(kDeviceChunk, n_r - lo);
+            FastOut o;
+            o.ray_offset = lo;
+            if (bary) {
+                o.c_ray = d_ray + hits; o.c_dist = d_dist + hits; o.c_tri = d_tri + hits;
+                o.c_pt = d_pt + 3 * hits;
+            } else {
+                o.flags = d_flags + lo;
+            }
+            RsStatus hb{};
+            rc = binary_query(t, d_starts + 3 * lo, d_ends + 3 * lo, cnt, mode, o, &hb, s);
+            if (rc) return rc;
+            if (hb.internal) return fail(RS_INTERNAL, "internal traversal capacity exceeded");
+            hits += hb.hits;
+        }
+    }
+    if (n_hits) *n_hits = (int64_t)hits;
+    if (bad) *bad = -1;
+    return RS_OK;
+}
+
 // The status words go to mapped pinned host memory from a one-warp kernel:
 // a D2H copy node at the end of the graph cost ~11 us of copy-engine latency
 // per call, the kernel's PCIe writes ~2 us.
@@ -1339,6 +1437,9 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
     if (tree_kind != kTreeReference && tree_kind != kTreeFast)
         return fail(RS_INVALID_ARG, "unknown tree kind %d", tree_kind);
     cudaStream_t s = S(stream);
+    if (n_r > g_device_chunk.load() && tree_kind == kTreeFast && !buffer_path() && !g_binary_fast)
+        return run_device_chunked(d_verts, n_v, d_tris, n_t, d_starts, d_ends, n_r, mode, d_flags,
+                                  d_ray, d_dist, d_tri, d_pt, n_hits, bad, s);
     bool done = false;
     if (g_use_graphs) {
         // The whole step (about 20 launches, memsets and stream-ordered
@@ -1430,6 +1531,19 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
     return rc;
 }
 
+RS_API int rs_generate_segments(const float* d_verts, const int32_t* d_tris, int64_t n_t,
+                                double z_lo, double z_hi, double x_hi, double y_hi,
+                                double frac, uint64_t seed, int64_t first, int64_t n,
+                                float* d_starts, float* d_ends, uint8_t* d_flags, void* stream) {
+    if (n < 0 || first < 0 || n_t < 1 || !(frac >= 0.0 && frac <= 1.0))
+        return fail(RS_INVALID_ARG, "invalid generator arguments");
+    if (n && (!d_verts || !d_tris || !d_starts || !d_ends)) return fail(RS_INVALID_ARG, "null array");
+    launch_generate(d_verts, d_tris, n_t, z_lo, z_hi, x_hi, y_hi, frac, seed, first, n, d_starts,
+                    d_ends, d_flags, S(stream));
+    CK(cudaGetLastError());
+    return RS_OK;
+}
+
 RS_API int rs_set_timing(int enable) {
     g_timing = enable >= 0 && enable <= 3 ? enable : 1;
     marks_reset();
@@ -1463,6 +1577,11 @@ RS_API long long rs_kernel_launches(void) { return g_launches.load(); }
 
 RS_API int rs_set_option(const char* name, long long value, long long* old_value) {
     if (!name) return fail(RS_INVALID_ARG, "null option name");
+    if (!strcmp(name, "device_chunk")) {
+        if (old_value) *old_value = g_device_chunk.load();
+        if (value > 0) g_device_chunk.store(((value + 1023) / 1024) * 1024);
+        return RS_OK;
+    }
     if (rs::sorted_option(name, value, old_value)) return fail(RS_INVALID_ARG, "unknown option %s", name);
     g_opt_gen.fetch_add(1);
     return RS_OK;

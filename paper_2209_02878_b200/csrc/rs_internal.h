@@ -220,6 +220,13 @@ void launch_bary_compact(const CompactArgs& a, cudaStream_t s);  // also advance
 void launch_bary_dense(const CompactArgs& a, int* detected, int* tri, float* dist, float* points,
                        cudaStream_t s);
 
+// Synthetic terrain segments on device (rs_gen.cu): the reference
+// generator's distribution (oracle.py:228-271) from a counter-based RNG.
+void launch_generate(const float* V, const int* T, long long n_t, double z_lo, double z_hi,
+                     double x_hi, double y_hi, double frac, unsigned long long seed,
+                     long long first, long long n, float* S, float* E, unsigned char* flags,
+                     cudaStream_t s);
+
 struct BaselineArgs {
     const float* V;
     const int* T;

@@ -137,3 +137,54 @@ def layered_scene(scene: SyntheticScene, layers: int = 7, dz: float = 8.0) -> Sy
     exp = scene.expected_crossings.astype(np.int32) * layers
     return SyntheticScene(mesh=Mesh.from_arrays(verts, tris),
                           segments=SegmentBatch.from_arrays(s, e), expected_crossings=exp)
+
+
+def _terrain_extent(vertices) -> tuple[float, float, float, float]:
+    """(z_lo, z_hi, x_hi, y_hi) of a generate_scene height field: the f32
+    vertex z range (oracle.py:213-214) and the grid extent + 1 that bounds
+    the misses' xy draws (oracle.py:256-257)."""
+    import torch
+
+    v = vertices if isinstance(vertices, torch.Tensor) else torch.from_numpy(np.asarray(vertices))
+    lo = v.amin(dim=0).cpu().numpy()
+    hi = v.amax(dim=0).cpu().numpy()
+    return float(lo[2]), float(hi[2]), float(hi[0]) + 1.0, float(hi[1]) + 1.0
+
+
+def generate_segments_device(mesh: Mesh, num_rays: int, crossing_fraction: float = 0.5,
+                             seed: int = 2022, first: int = 0, device=None,
+                             out: tuple | None = None):
+    """Rows [first, first + num_rays) of a synthetic segment batch over a
+    generate_scene terrain, generated on the GPU (rs_generate_segments): the
+    reference generator's distribution (oracle.py:228-271) from a Philox
+    stream keyed by (seed, global row), so every sharding of a batch sees the
+    same rows.  Returns (SegmentBatch of CUDA tensors, ground-truth flags u8
+    CUDA tensor).  This is how BASELINE configs[4]'s 1B segments are made:
+    24 GB that would otherwise cross PCIe from a numpy generator.
+    `out` = (starts, ends, flags) preallocated CUDA tensors (flags may be None)."""
+    import torch
+
+    from . import _lib
+
+    if not 0.0 <= crossing_fraction <= 1.0:
+        raise ValidationError("crossing fraction must be within [0, 1]")
+    if num_rays < 0 or first < 0:
+        raise ValidationError("num_rays and first must be non-negative")
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    dev_v = torch.as_tensor(np.asarray(mesh.vertices) if not isinstance(mesh.vertices, torch.Tensor)
+                            else mesh.vertices).to(device).contiguous()
+    dev_t = torch.as_tensor(np.asarray(mesh.triangles) if not isinstance(mesh.triangles, torch.Tensor)
+                            else mesh.triangles).to(device).contiguous()
+    z_lo, z_hi, x_hi, y_hi = _terrain_extent(dev_v)
+    if out is None:
+        starts = torch.empty((num_rays, 3), dtype=torch.float32, device=device)
+        ends = torch.empty((num_rays, 3), dtype=torch.float32, device=device)
+        flags = torch.empty(num_rays, dtype=torch.uint8, device=device)
+    else:
+        starts, ends, flags = out
+    stream = torch.cuda.current_stream(device).cuda_stream
+    _lib.check(_lib.lib().rs_generate_segments(
+        dev_v.data_ptr(), dev_t.data_ptr(), dev_t.shape[0], z_lo, z_hi, x_hi, y_hi,
+        float(crossing_fraction), int(seed), int(first), int(num_rays), starts.data_ptr(),
+        ends.data_ptr(), flags.data_ptr() if flags is not None else None, stream))
+    return SegmentBatch(starts, ends), flags

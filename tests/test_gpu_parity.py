@@ -737,3 +737,21 @@ def test_chunked_host_batch_keeps_the_batch_traversal():
         r = rs.run_batch(sc.mesh, sc.segments, rs.EngineConfig(mode=mode))
         assert _lib.lib().rs_hot_kernel().decode() == "k_trav_tile"
         assert np.array_equal(_np(r.crossing if mode == "boolean" else r.counts), truth), mode
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ("c1", "s19", "dup", "layered"))
+def test_device_chunked_batches(name, mode):
+    """Batches above the device chunk size (2^27 segments by default; BASELINE
+    configs[4]'s 1B-segment job) run as one build and a loop of chunk
+    queries; lowered here to 1024 so the golden scenes take that path: every
+    chunk's rows land at their global offsets, barycentric rows compact
+    across chunks in ascending ray order."""
+    fx = load(name if name == "layered" else
+              (f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}"))
+    mesh, batch = mesh_batch(fx, True)
+    want = expected(fx, "cap32" if name == "layered" else "batch", mode)
+    with _lib.option("device_chunk", 1024):
+        for _ in range(2):
+            got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
+            assert_result_fields(result_dict(got), want, f"{name} {mode} chunked")

@@ -1,9 +1,13 @@
-"""Multi-process sharding logic (world_size 2, gloo, CPU).
+"""Multi-process sharding logic (world_size 2, gloo).
 
-The per-rank compute is the C oracle here (no GPU in the build container),
+On CPU the per-rank compute is the C oracle (no GPU in the build container),
 so this exercises exactly the host-side parts of the multi-GPU path: the
-contiguous shard split, the variable-length all_gather and the barycentric
-ray-index rebasing/concatenation."""
+contiguous shard split, the gather to rank 0 (or to every rank), the
+barycentric ray-index rebasing/concatenation, and the error agreement (one
+rank's TraversalStackOverflow / ValidationError raised on every rank with
+the batch-global segment index, instead of a hang in the gather).  The GPU
+variants run the real CUDA run_batch on each rank (both ranks share one
+device here), on numpy inputs and on CUDA-tensor inputs."""
 
 import os
 import socket
@@ -17,6 +21,8 @@ import paper_2209_02878_b200 as rs
 from paper_2209_02878_b200.parallel import run_batch_sharded, shard_range
 from golden_io import MODES, assert_result_fields, expected, load
 
+FIELDS = ("crossing", "counts", "ray_index", "distance", "triangle_id", "point")
+
 
 def _oracle_local(mesh, segs, cfg):
     from oracle import oracle as O
@@ -25,22 +31,58 @@ def _oracle_local(mesh, segs, cfg):
     return rs.ResultSet(cfg.mode, segs.count, **{k: v for k, v in d.items() if k != "mode"})
 
 
-def _worker(rank, world, port, name, q, gpu=False):
+def _np(x):
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+def _worker(rank, world, port, name, q, kind, gather):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         fx = load(name)
-        mesh = rs.Mesh.from_arrays(fx["vertices"], fx["triangles"])
-        segs = rs.SegmentBatch.from_arrays(fx["starts"], fx["ends"])
+        V, T, s, e = fx["vertices"], fx["triangles"], fx["starts"], fx["ends"]
+        if kind == "gpu_device":
+            import torch
+
+            V, T, s, e = (torch.from_numpy(a).cuda() for a in (V, T, s, e))
+        mesh = rs.Mesh.from_arrays(V, T)
+        segs = rs.SegmentBatch.from_arrays(s, e)
         out = {}
         for mode in MODES:
-            r = run_batch_sharded(mesh, segs, rs.EngineConfig(mode=mode),
-                                  local_run=None if gpu else _oracle_local)
-            out[mode] = {f: np.asarray(getattr(r, f)) for f in
-                         ("crossing", "counts", "ray_index", "distance", "triangle_id", "point")
-                         if getattr(r, f) is not None}
+            r = run_batch_sharded(mesh, segs, rs.EngineConfig(mode=mode), gather=gather,
+                                  local_run=_oracle_local if kind == "cpu" else None)
+            out[mode] = {f: _np(getattr(r, f)) for f in FIELDS if getattr(r, f) is not None}
+            out[mode]["num_rays"] = r.num_rays
         q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _failing_worker(rank, world, port, q, failing_rank, exc):
+    """`failing_rank`'s local run raises `exc`; every rank must raise."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fx = load("scene_s19")
+        mesh = rs.Mesh.from_arrays(fx["vertices"], fx["triangles"])
+        segs = rs.SegmentBatch.from_arrays(fx["starts"], fx["ends"])
+
+        def local(m, part, cfg):
+            if rank == failing_rank or failing_rank < 0:
+                if exc == "overflow":
+                    raise rs.TraversalStackOverflow("overflow", segment_index=3 + rank)
+                raise rs.ValidationError("bad shard")
+            return _oracle_local(m, part, cfg)
+
+        try:
+            run_batch_sharded(mesh, segs, rs.EngineConfig(), local_run=local)
+            q.put((rank, ("ok", None)))
+        except rs.TraversalStackOverflow as e:
+            q.put((rank, ("overflow", e.segment_index)))
+        except rs.ValidationError:
+            q.put((rank, ("validation", None)))
     finally:
         dist.destroy_process_group()
 
@@ -51,19 +93,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_shard_ranges_partition():
-    for n in (0, 1, 7, 10_000_001):
-        for w in (1, 2, 3, 8):
-            r = [shard_range(n, k, w) for k in range(w)]
-            assert r[0][0] == 0 and r[-1][1] == n
-            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
-
-
-def _run_two_ranks(name, gpu):
+def _spawn(target, args_of_rank, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q, gpu)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port) + args_of_rank(q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in procs)
@@ -73,22 +107,63 @@ def _run_two_ranks(name, gpu):
     return res
 
 
-@pytest.mark.parametrize("name", ["scene_s19", "soup_17"])
-def test_two_rank_gloo_matches_reference(name):
-    res = _run_two_ranks(name, gpu=False)
-    fx = load(name)
+def test_shard_ranges_partition():
+    for n in (0, 1, 7, 10_000_001):
+        for w in (1, 2, 3, 8):
+            r = [shard_range(n, k, w) for k in range(w)]
+            assert r[0][0] == 0 and r[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+
+
+def _check(res, fx, gather):
+    n = fx["starts"].shape[0]
     for rank in (0, 1):
         for mode in MODES:
-            assert_result_fields(res[rank][mode], expected(fx, "batch", mode), f"rank {rank} {mode}")
+            got = res[rank][mode]
+            if gather == "all" or rank == 0:
+                assert got["num_rays"] == n
+                assert_result_fields(got, expected(fx, "batch", mode), f"rank {rank} {mode}")
+            else:  # rank 1 keeps its own shard (global ray indices)
+                lo, hi = shard_range(n, 1, 2)
+                want = expected(fx, "batch", mode)
+                assert got["num_rays"] == hi - lo
+                if mode == "barycentric":
+                    keep = (want["ray_index"] >= lo) & (want["ray_index"] < hi)
+                    assert np.array_equal(got["ray_index"], want["ray_index"][keep])
+                    assert np.array_equal(got["point"], want["point"][keep])
+                else:
+                    key = "crossing" if mode == "boolean" else "counts"
+                    assert np.array_equal(got[key], want[key][lo:hi])
+
+
+@pytest.mark.parametrize("gather", ["rank0", "all"])
+@pytest.mark.parametrize("name", ["scene_s19", "soup_17"])
+def test_two_rank_gloo_matches_reference(name, gather):
+    res = _spawn(_worker, lambda q: (name, q, "cpu", gather))
+    _check(res, load(name), gather)
+
+
+@pytest.mark.parametrize("failing_rank,exc,want", [
+    (1, "overflow", ("overflow", None)),     # rank 1's local index 4 -> global lo + 4
+    (-1, "overflow", ("overflow", 3)),       # both ranks: the batch-global minimum (rank 0's 3)
+    (0, "validation", ("validation", None)),
+])
+def test_error_agreement(failing_rank, exc, want):
+    res = _spawn(_failing_worker, lambda q: (q, failing_rank, exc))
+    n = load("scene_s19")["starts"].shape[0]
+    lo1 = shard_range(n, 1, 2)[0]
+    for rank in (0, 1):
+        kind, idx = res[rank]
+        assert kind == want[0], (rank, res)
+        if kind == "overflow":
+            assert idx == (want[1] if want[1] is not None else lo1 + 4), (rank, res)
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["gpu", "gpu_device"])
 @pytest.mark.parametrize("name", ["scene_c1", "soup_20"])
-def test_two_rank_sharded_gpu_matches_reference(name):
+def test_two_rank_sharded_gpu_matches_reference(name, kind):
     """Both ranks run the real CUDA run_batch on their shard (sharing one
-    GPU here), gather over gloo, and every rank holds the reference result."""
-    res = _run_two_ranks(name, gpu=True)
-    fx = load(name)
-    for rank in (0, 1):
-        for mode in MODES:
-            assert_result_fields(res[rank][mode], expected(fx, "batch", mode), f"gpu rank {rank} {mode}")
+    GPU here) on numpy or CUDA-tensor inputs, gather to rank 0 over gloo."""
+    res = _spawn(_worker, lambda q: (name, q, kind, "rank0"))
+    _check(res, load(name), "rank0")
