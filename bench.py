@@ -556,6 +556,11 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks.summary(t_start, t_end + 0.02),
     }
+    if os.environ.get("RS_DEBUG_STATUS"):
+        st = (C.c_ulonglong * 8)()
+        lib.rs_last_status(st)
+        line["debug_status"] = dict(zip(["bad", "internal", "hits", "tile_counter", "visits", "mts",
+                                         "cand_count", "dropped"], [int(x) for x in st]))
     if gather:
         line["gather"] = gather
     if e2e:

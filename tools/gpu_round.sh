@@ -61,7 +61,15 @@ for w in $WHAT; do
         arg=""; [ $tool = racecheck ] && arg=small
         timeout 1200 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize.py $arg > "$OUT/sanitize_$tool.txt" 2>&1
         echo "rc=$?" >> "$OUT/sanitize_$tool.txt"; done;;
-    bench_all) for c in c2 c3 c4 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --steps ${RS_ALL_STEPS:-10} > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
+    traffic) for c in ${RS_CFGS:-c2 c3 c4 c5}; do
+        timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+          --clock-control none --csv --log-file "$OUT/traffic_$c.csv" python bench.py --config $c --steps 2 \
+          --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/traffic_$c.log" 2>&1
+        python tools/traffic.py "$OUT/traffic_$c.csv" $c --out "$OUT/traffic_$c.json" >> "$OUT/traffic_$c.log" 2>&1; done;;
+    fullhot) for c in ${RS_CFGS:-c2}; do
+        timeout 900 ncu --set full --clock-control none --import-source on -k regex:${RS_HOT:-k_trav_tile} -s 3 -c 1 \
+          -o "$OUT/full_$c" python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/full_$c.log" 2>&1; done;;
+    bench_all) for c in c2 c3 c4 c5; do timeout 900 python bench.py --config $c --steps ${RS_ALL_STEPS:-10} > "$OUT/bench_$c.json" 2>> "$OUT/bench.err"; done;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_bench.log" 2>&1
