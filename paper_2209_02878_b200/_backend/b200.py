@@ -180,6 +180,25 @@ def _device_tree_for(mesh, tree: BvhTree) -> DeviceTree:
     return dt
 
 
+def _as_host_error(exc: Exception) -> Exception:
+    """The error in the calling package's own classes: registered inside the
+    reference (`raysurf._backend`), its engine and tests catch
+    raysurf.exceptions.TraversalStackOverflow / ValidationError
+    (_compiled.py:108-112 raises those), not this package's."""
+    import sys
+
+    from .. import exceptions as ours
+
+    host = sys.modules.get("raysurf.exceptions")
+    if host is None or host is ours:
+        return exc
+    if isinstance(exc, ours.TraversalStackOverflow):
+        return host.TraversalStackOverflow(str(exc), segment_index=exc.segment_index)
+    if isinstance(exc, ours.ValidationError):
+        return host.ValidationError(str(exc))
+    return exc
+
+
 def batch_query(mesh, tree, segments, seg_boxes, mode, max_collisions, max_stack, lo, hi, out):
     """_compiled.py:72-112: rows [lo, hi) of `out`; seg_boxes are recomputed
     on device from the endpoints (engine.py:115-122 gives the same boxes)."""
@@ -194,7 +213,10 @@ def batch_query(mesh, tree, segments, seg_boxes, mode, max_collisions, max_stack
 
         if isinstance(exc, TraversalStackOverflow) and exc.segment_index is not None:
             exc.segment_index += lo
-        raise
+        host = _as_host_error(exc)
+        if host is exc:
+            raise
+        raise host from exc
     _store(out, lo, hi, mode, res)
 
 

@@ -14,7 +14,9 @@
 #include <memory>
 #include <set>
 #include <vector>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <string>
 
 #include "../../include/raysurf_b200.h"
@@ -553,8 +555,91 @@ struct Pipe {
     cudaEvent_t ev_in[2], ev_in2[2], ev_q[2], ev_out[2], ev_blk;
     RsStatus* hst = nullptr;  // pinned per-chunk statuses (barycentric row counts)
     int64_t hst_cap = 0;
+    char* stg = nullptr;      // pinned staging for pageable inputs (2 chunk slots + mesh)
+    size_t stg_cap = 0;
 };
 thread_local Pipe g_pipe;
+
+// Pageable host inputs are staged through pinned buffers: cudaMemcpyAsync
+// from pageable memory runs at ~11 GB/s (the driver's own staging, CPU and
+// DMA serialised), while several threads copying into pinned memory reach
+// ~45 GB/s and the DMA of chunk k overlaps the copy of chunk k+1.  A small
+// persistent pool (the caller takes one share of every copy).
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool();  // never destroyed: workers live for the process
+        return *p;
+    }
+    void copy(void* dst, const void* src, size_t bytes) {
+        if (bytes < (1u << 20) || workers_ == 0) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> one(call_mu_);  // one parallel copy at a time
+        const int parts = workers_ + 1;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            parts_ = parts;
+            pending_ = workers_;
+            ++gen_;
+        }
+        cv_.notify_all();
+        run_part(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+  private:
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        const char* e = getenv("RS_COPY_THREADS");
+        // B200 box (16 host threads): 2 copiers 11.2 ms, 4 9.1 ms, 8 7.0 ms
+        // per pageable 10M-segment C2 call
+        workers_ = e && *e ? atoi(e) : (int)(hw >= 16 ? 8 : (hw > 1 ? hw / 2 : 0));
+        for (int w = 0; w < workers_; ++w) std::thread([this, w] { loop(w + 1); }).detach();
+    }
+    void run_part(int k) {
+        const size_t per = ((bytes_ + parts_ - 1) / parts_ + 63) & ~size_t(63);
+        const size_t lo = per * (size_t)k;
+        if (lo < bytes_) std::memcpy(dst_ + lo, src_ + lo, std::min(per, bytes_ - lo));
+    }
+    void loop(int k) {
+        unsigned long long seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            run_part(k);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    int workers_ = 0;
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+    int parts_ = 1, pending_ = 0;
+    unsigned long long gen_ = 0;
+};
+
+bool is_pageable(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
 
 int pipe_init() {
     int dev;
@@ -1608,6 +1693,13 @@ void rs::hot_kernel_mark(int which, cudaStream_t s) {
     if (g_hot_mark_mask & (1 << which)) mark(3 + which, s);
 }
 
+// chunks of a large pageable batch (RS_STAGE_PARTS): the first chunk's
+// host copy is exposed, so staged batches use finer chunks
+static const int64_t g_stage_parts = [] {
+    const char* e = getenv("RS_STAGE_PARTS");
+    return (int64_t)(e && *e ? atoi(e) : 16);
+}();
+
 // set while the host pipeline re-runs a batch with the binary kernels
 static thread_local bool g_force_binary = false;
 
@@ -1638,7 +1730,7 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     const bool auto_chunks = chunk_rays <= 0;
     // large batches: 8 chunks (12 for barycentric, whose per-chunk row copies
     // trail the device; C3 e2e 5.70 -> 5.51 ms)
-    const int64_t big_parts = mode == kBarycentric ? 12 : 8;
+    const int64_t big_parts = mode == kBarycentric ? 12 : (is_pageable(h_starts) ? g_stage_parts : 8);
     if (auto_chunks)
         chunk_rays = n_r > (8ll << 20) ? (n_r + big_parts - 1) / big_parts
                                        : (n_r > (1 << 20) ? (n_r + 3) / 4 : n_r);
@@ -1741,8 +1833,48 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     CK(cudaEventRecord(g_pipe.ev_blk, s));
     CK(cudaStreamWaitEvent(h2d, g_pipe.ev_blk, 0));
     CK(cudaStreamWaitEvent(d2h, g_pipe.ev_blk, 0));
-    CK(cudaMemcpyAsync(dV, h_verts, 12ull * n_v, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dT, h_tris, 12ull * n_t, cudaMemcpyHostToDevice, s));
+    // pageable inputs: two pinned chunk slots (starts, ends) + the mesh
+    const bool stage_in = is_pageable(h_starts) || is_pageable(h_ends);
+    const bool stage_mesh = is_pageable(h_verts) || is_pageable(h_tris);
+    const size_t slot_b = align256(24ull * chunk_rays);
+    const size_t mesh_hb = align256(12ull * n_v) + align256(12ull * n_t);
+    float* stg_in[2] = {nullptr, nullptr};
+    if (stage_in || stage_mesh) {
+        const size_t need = (stage_in ? 2 * slot_b : 0) + (stage_mesh ? mesh_hb : 0);
+        if (g_pipe.stg_cap < need) {
+            CK(cudaStreamSynchronize(h2d));  // the old slots may still feed a copy
+            if (g_pipe.stg) cudaFreeHost(g_pipe.stg);
+            g_pipe.stg = nullptr;
+            g_pipe.stg_cap = 0;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&g_pipe.stg), need, cudaHostAllocDefault));
+            g_pipe.stg_cap = need;
+        }
+        if (stage_in) {
+            stg_in[0] = reinterpret_cast<float*>(g_pipe.stg);
+            stg_in[1] = reinterpret_cast<float*>(g_pipe.stg + slot_b);
+        }
+    }
+    const float* mesh_v = h_verts;
+    const int32_t* mesh_t = h_tris;
+    if (stage_mesh) {
+        char* m = g_pipe.stg + (stage_in ? 2 * slot_b : 0);
+        CopyPool::get().copy(m, h_verts, 12ull * n_v);
+        CopyPool::get().copy(m + align256(12ull * n_v), h_tris, 12ull * n_t);
+        mesh_v = reinterpret_cast<const float*>(m);
+        mesh_t = reinterpret_cast<const int32_t*>(m + align256(12ull * n_v));
+    }
+    // chunk k's rows into slot k & 1 (its previous upload must have landed)
+    auto stage_chunk = [&](int64_t k) -> int {
+        const int b = (int)(k & 1);
+        if (k >= 2) CK(cudaEventSynchronize(g_pipe.ev_in[b]));
+        const int64_t lo = chunk_lo(k), cnt = chunk_cnt(k);
+        CopyPool::get().copy(stg_in[b], h_starts + 3 * lo, 12ull * cnt);
+        CopyPool::get().copy(stg_in[b] + 3 * chunk_rays, h_ends + 3 * lo, 12ull * cnt);
+        return RS_OK;
+    };
+    if (stage_in && (rc = stage_chunk(0))) return rc;
+    CK(cudaMemcpyAsync(dV, mesh_v, 12ull * n_v, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dT, mesh_t, 12ull * n_t, cudaMemcpyHostToDevice, s));
     mark(0, s);
     rc = build_impl(dV, n_v, dT, n_t, tree_kind, nullptr, nullptr, s, &guard.t, nullptr, true);
     if (rc) return rc;
@@ -1784,8 +1916,10 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
         const int64_t lo = chunk_lo(k);
         const int64_t cnt = chunk_cnt(k);
         if (k >= 2) CK(cudaStreamWaitEvent(h2d, g_pipe.ev_q[b], 0));  // input buffer b free again
-        CK(cudaMemcpyAsync(din[b][0], h_starts + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
-        CK(cudaMemcpyAsync(din[b][1], h_ends + 3 * lo, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
+        const float* src_s = stage_in ? stg_in[b] : h_starts + 3 * lo;
+        const float* src_e = stage_in ? stg_in[b] + 3 * chunk_rays : h_ends + 3 * lo;
+        CK(cudaMemcpyAsync(din[b][0], src_s, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
+        CK(cudaMemcpyAsync(din[b][1], src_e, 12ull * cnt, cudaMemcpyHostToDevice, h2d));
         CK(cudaEventRecord(g_pipe.ev_in[b], h2d));
         CK(cudaStreamWaitEvent(s, g_pipe.ev_in[b], 0));
         if (k >= 2 && !bary) CK(cudaStreamWaitEvent(s, g_pipe.ev_out[b], 0));  // flags b read back
@@ -1836,6 +1970,8 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
             CK(cudaEventRecord(g_pipe.ev_out[b], d2h));
             if (k >= 1 && (rc = retire(k - 1))) return rc;
         }
+        // the next chunk's rows into the other pinned slot while this one uploads
+        if (stage_in && k + 1 < nchunks && (rc = stage_chunk(k + 1))) return rc;
     }
     if (lagged && (rc = retire(nchunks - 1))) return rc;
     cp = d2h;
