@@ -755,7 +755,16 @@ struct FastScratch {
     float4* rec = nullptr;
     unsigned long long* seg_key = nullptr;
     void* geom = nullptr;
+    unsigned* hitbits = nullptr;  // large boolean batches: hit bitmap (see SortedArgs::hitbits)
 };
+
+// Boolean batches from this many segments on set hit bits instead of
+// writing int32 flags at random (RS_HITBITS_MIN; C5 1B: the flags' partial
+// sectors were half the traversal's 65 GB of DRAM traffic).
+static std::atomic<long long> g_hitbits_min{[] {
+    const char* e = getenv("RS_HITBITS_MIN");
+    return e && *e ? atoll(e) : (1ll << 25);
+}()};
 
 // fast_path option 1 (or RS_FAST_PATH=buffer): pair traversal -> collision
 // buffer -> exact pass; default 0: the binned tile traversal.
@@ -776,8 +785,10 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
         total += align256(8ull * n_r) + align256(4ull * n_r) + align256(8ull * cap) +
                  align256(bary_compact_scratch(n_r));
     if (buffer_path()) total += align256(4 * trav_gstack_ints());
+    const bool bits = mode == kBoolean && !buffer_path() && n_r >= g_hitbits_min.load();
     total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r) +
-             align256(8ull * n_r) + align256(bin_geom_bytes());
+             align256(8ull * (bin_rank_on() ? n_r : 1)) + align256(bin_geom_bytes()) +
+             (bits ? align256(4ull * ((n_r + 31) / 32)) : 0);
     CK(dmalloc(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
     f.st = c.take<RsStatus>(1);
@@ -796,8 +807,9 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     f.cursor = c.take<unsigned>(sorted_bins());
     f.n_live = c.take<unsigned>(64 + 4 * 32);
     f.rec = c.take<float4>(2ull * n_r);
-    f.seg_key = c.take<unsigned long long>(n_r);
+    f.seg_key = c.take<unsigned long long>(bin_rank_on() ? n_r : 1);
     f.geom = c.take<char>(bin_geom_bytes());
+    f.hitbits = bits ? c.take<unsigned>((n_r + 31) / 32) : nullptr;
     f.cap = cap;
     return RS_OK;
 }
@@ -814,6 +826,7 @@ static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d
     a.leaf_boxes = t->ta.leaf_bounds;
     a.key_mode = t->key_mode;
     a.geom = f.geom;
+    a.hitbits = f.hitbits;
     return a;
 }
 
@@ -824,8 +837,11 @@ static int fast_presets(const float* d_s, const float* d_e, int64_t n_r, int mod
                         FastScratch& f, cudaStream_t s) {
     const bool bary = mode == kBarycentric;
     CK(cudaMemsetAsync(f.st, 0, sizeof(RsStatus), s));
-    // boolean/count outputs start at 0: zeroed by the histogram pass when it can
-    if (!bary && !binning_zeroes_flags(d_s, d_e, n_r, o.flags)) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
+    // boolean/count outputs start at 0: zeroed by the histogram pass when it
+    // can; with a hit bitmap the bitmap starts at 0 and k_expand_bits writes
+    // every flag
+    if (f.hitbits) CK(cudaMemsetAsync(f.hitbits, 0, 4ull * ((n_r + 31) / 32), s));
+    else if (!bary && !binning_zeroes_flags(d_s, d_e, n_r, o.flags)) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
     if (bary) {
         CK(cudaMemsetAsync(f.best_t, 0xFF, 8ull * n_r, s));
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
@@ -852,6 +868,7 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
                      bool first = true, bool last = true) {
     if (first) ev_record(1, s);
     launch_sorted_trav(sorted_args(t, d_s, d_e, n_r, o, f), mode, stats, s);
+    if (f.hitbits) launch_expand_bits(o.flags, f.hitbits, n_r, s);
     if (mode == kBarycentric) {
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
                        f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base};
@@ -1213,7 +1230,11 @@ static int run_device_direct(const float* d_verts, int64_t n_v, const int32_t* d
 // every chunk chooses its traversal kernel by the whole batch's density
 // (set_batch_rays).  One synchronisation at the end.
 // Option "device_chunk" (multiple of 1024) lowers it for tests.
-static std::atomic<long long> g_device_chunk{1ll << 27};
+static std::atomic<long long> g_device_chunk{[] {
+    const char* e = getenv("RS_DEVICE_CHUNK");
+    const long long v = e && *e ? atoll(e) : 0;
+    return v > 0 ? ((v + 1023) / 1024) * 1024 : (1ll << 30);
+}()};
 
 static int run_device_chunked(const float* d_verts, int64_t n_v, const int32_t* d_tris,
                               int64_t n_t, const float* d_starts, const float* d_ends, int64_t n_r,
@@ -1662,6 +1683,12 @@ RS_API long long rs_kernel_launches(void) { return g_launches.load(); }
 
 RS_API int rs_set_option(const char* name, long long value, long long* old_value) {
     if (!name) return fail(RS_INVALID_ARG, "null option name");
+    if (!strcmp(name, "hitbits_min")) {  // tests: the bitmap path on small batches
+        if (old_value) *old_value = g_hitbits_min.load();
+        if (value >= 0) g_hitbits_min.store(value);
+        g_opt_gen.fetch_add(1);
+        return RS_OK;
+    }
     if (!strcmp(name, "device_chunk")) {
         if (old_value) *old_value = g_device_chunk.load();
         if (value > 0) g_device_chunk.store(((value + 1023) / 1024) * 1024);

@@ -189,7 +189,14 @@ struct SortedArgs {
     int zero_flags;             // the histogram pass zeroes flags (instead of a preset memset)
     void* geom;                 // bin_geom_bytes(): bin geometry, written by k_seg_sample
     int geom_mode;              // 1: binning CTAs copy geom; 0: each derives it
+    // boolean batches too large for their flags to stay in L2: hits set bits
+    // here (n_r / 32 words, L2-resident) and k_expand_bits writes the int32
+    // flags afterwards in one coalesced pass, instead of one partial-sector
+    // DRAM read-modify-write per hit (null: flags written directly)
+    unsigned* hitbits;
 };
+// Writes flags[i] = bit i of hitbits for i < n (every row: no zero preset needed).
+void launch_expand_bits(int* flags, const unsigned* hitbits, long long n, cudaStream_t s);
 size_t sorted_bins();
 size_t bin_geom_bytes();
 bool sorted_wide();  // RS_SORTED_WIDE=1: 4-wide per-thread traversal (needs nodes4)
@@ -210,6 +217,8 @@ int fast_key_mode();
 // (default), 1 collision buffer (pair traversal -> warp-aggregated append ->
 // exact pass, re-launched with a sized buffer on overflow).
 int fast_path();
+// Option bin_rank (A/B): the histogram pass records each segment's slot (needs seg_key).
+bool bin_rank_on();
 // Initial collision-buffer capacity in entries (option "cand_cap"; 0: 2 x segments + 4096).
 long long cand_cap_override();
 // Name of the traversal kernel the last launch_sorted_trav chose.

@@ -33,7 +33,10 @@
 namespace rs {
 
 constexpr unsigned kFullMask = 0xffffffffu;
-constexpr int kBinBits = 21;                 // up to 2M spatial bins
+// up to 512k spatial bins: the scatter's open output lines (one 128-B line
+// per bin) stay within half of L2 (1B-segment C5: 2M bins took the scatter
+// from 13 to 17 ms; C2-C4 use 2^18-2^19 bins anyway)
+constexpr int kBinBits = 19;
 constexpr int kSampleCtas = 32;              // k_seg_sample grid
 constexpr int kSampleThreads = 128;
 constexpr int kBins = 1 << kBinBits;
@@ -847,7 +850,10 @@ __global__ void __launch_bounds__(kSortedThreads) k_trav_sorted(SortedArgs a) {
         }
         if (ovf) atomicAdd(&a.status->internal, 1ull);
         if (MODE == kBoolean) {
-            if (det) a.flags[id] = 1;
+            if (det) {
+                if (a.hitbits) atomicOr(a.hitbits + (id >> 5), 1u << (id & 31));
+                else a.flags[id] = 1;
+            }
         } else if (MODE == kCount) {
             if (nh) a.flags[id] = nh;
         } else if (btri >= 0) {
@@ -943,7 +949,10 @@ template <int MODE>
 __device__ __forceinline__ void write_result(const SortedArgs& a, int id, int det, int nh,
                                              int btri, double bt) {
     if (MODE == kBoolean) {
-        if (det) a.flags[id] = 1;
+        if (det) {
+            if (a.hitbits) atomicOr(a.hitbits + (id >> 5), 1u << (id & 31));
+            else a.flags[id] = 1;
+        }
     } else if (MODE == kCount) {
         if (nh) a.flags[id] = nh;
     } else if (btri >= 0) {
@@ -2017,6 +2026,7 @@ int sorted_option(const char* name, long long value, long long* old) {
 static int trav_variant() { return opts().trav; }
 int fast_key_mode() { return opts().fast_keys; }
 int fast_path() { return opts().fast_path; }
+bool bin_rank_on() { return opts().bin_rank != 0; }
 long long cand_cap_override() { return opts().cand_cap; }
 static unsigned tile_min_density() { return opts().tile_density; }
 static unsigned tile_balance() { return opts().tile_balance; }
@@ -2029,9 +2039,38 @@ bool binning_zeroes_flags(const float* starts, const float* ends, long long n_r,
     return flags && (al & 15) == 0 && opts().bin_tma && !opts().bin_rank && n_r >= kStreamSegs;
 }
 
+__global__ void __launch_bounds__(256) k_expand_bits(int* __restrict__ flags, const unsigned* __restrict__ bits,
+                                                    long long n) {
+    // one thread per 4 flags (one 16-B store; consecutive threads write
+    // consecutive 16 B), 8 threads share a bitmap word
+    const long long n4 = n / 4;
+    const bool vec = (reinterpret_cast<uintptr_t>(flags) & 15) == 0;
+    for (long long j = blockIdx.x * 256ll + threadIdx.x; j < n4; j += gridDim.x * 256ll) {
+        const unsigned b = __ldg(bits + (j >> 3)) >> (4 * (j & 7));
+        const int4 v = make_int4(b & 1, (b >> 1) & 1, (b >> 2) & 1, (b >> 3) & 1);
+        if (vec) {
+            reinterpret_cast<int4*>(flags)[j] = v;
+        } else {
+            flags[4 * j] = v.x; flags[4 * j + 1] = v.y; flags[4 * j + 2] = v.z; flags[4 * j + 3] = v.w;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (unsigned)(n - 4 * n4)) {
+        const long long i = 4 * n4 + threadIdx.x;
+        flags[i] = (__ldg(bits + (i >> 5)) >> (i & 31)) & 1;
+    }
+}
+
+void launch_expand_bits(int* flags, const unsigned* hitbits, long long n, cudaStream_t s) {
+    if (n <= 0) return;
+    const long long want = (n / 4 + 255) / 256 + 1;
+    const long long cap = (long long)sm_total() * 8;
+    count_launches(1);
+    k_expand_bits<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(flags, hitbits, n);
+}
+
 void launch_binning(const SortedArgs& a0, cudaStream_t s, bool zero_flags) {
     SortedArgs a = a0;
-    a.zero_flags = zero_flags && binning_zeroes_flags(a.starts, a.ends, a.n_r, a.flags);
+    a.zero_flags = zero_flags && !a.hitbits && binning_zeroes_flags(a.starts, a.ends, a.n_r, a.flags);
     a.geom_mode = opts().geom;
     a.bin_occupancy = bin_occupancy();
     a.rec_ids = opts().rec_ids;

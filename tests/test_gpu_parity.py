@@ -755,3 +755,27 @@ def test_device_chunked_batches(name, mode):
         for _ in range(2):
             got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
             assert_result_fields(result_dict(got), want, f"{name} {mode} chunked")
+
+
+@pytest.mark.parametrize("variant", ["auto", "binary", "tile"])
+@pytest.mark.parametrize("name", ("c1", "s19", "dup", "soup:17", "full"))
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+def test_hit_bitmap_path(name, variant, device):
+    """Boolean batches of >= 2^25 segments set hit bits (L2-resident) that
+    one coalesced pass expands into the int32 flags; forced on here for the
+    golden scenes, through every traversal kernel and the device-chunked
+    loop."""
+    fx = load(f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}")
+    mesh, batch = mesh_batch(fx, device)
+    want = expected(fx, "batch", "boolean")
+    with contextlib.ExitStack() as stack:
+        stack.enter_context(_lib.option("hitbits_min", 1))
+        if variant != "auto":
+            stack.enter_context(_lib.option("trav", TRAV[variant]))
+        for _ in range(2):
+            got = rs.run_batch(mesh, batch, rs.EngineConfig(mode="boolean", tree="fast"))
+            assert_result_fields(result_dict(got), want, f"{name} bitmap {variant}")
+        if device:
+            with _lib.option("device_chunk", 1024):
+                got = rs.run_batch(mesh, batch, rs.EngineConfig(mode="boolean", tree="fast"))
+            assert_result_fields(result_dict(got), want, f"{name} bitmap chunked")
