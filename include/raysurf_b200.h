@@ -146,6 +146,30 @@ RS_API int rs_baseline(const float *d_verts, int64_t n_v, const int32_t *d_tris,
                 int32_t *d_detected, int32_t *d_counts, int32_t *d_tri, float *d_dist,
                 float *d_points, void *stream);
 
+/* All-pairs barycentric with ordered compaction (engine.py:320-335 +
+ * _assemble): rows for intersecting segments only, ray index ascending;
+ * output arrays hold n_r rows, *n_hits receives the count.  Synchronises. */
+RS_API int rs_baseline_compact(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
+                               const float *d_starts, const float *d_ends, int64_t n_r,
+                               int32_t *d_ray_index, float *d_distance, int32_t *d_triangle_id,
+                               float *d_point, int64_t *n_hits, void *stream);
+
+/* compute_segment_boxes (engine.py:115-122): d_boxes (n,6) f32
+ * [xmin,xmax,ymin,ymax,zmin,zmax] per segment.  Stream-ordered. */
+RS_API int rs_segment_boxes(const float *d_starts, const float *d_ends, int64_t n, float *d_boxes,
+                            void *stream);
+
+/* sort_rays un-permutation (engine.py:191-198) on device, perm[k] = original
+ * index of sorted slot k (rs_sort_segments).  Dense rows: d_out[perm[k]] =
+ * d_in[k].  Barycentric rows (k of them, ray index = sorted slot): written
+ * to o_* ascending by original index perm[ray].  Stream-ordered. */
+RS_API int rs_unpermute_dense(const int64_t *d_perm, int64_t n, const int32_t *d_in, int32_t *d_out,
+                              void *stream);
+RS_API int rs_unpermute_rows(const int64_t *d_perm, int64_t n, const int32_t *d_ray_index,
+                             const float *d_distance, const int32_t *d_triangle_id,
+                             const float *d_point, int64_t k, int32_t *o_ray_index,
+                             float *o_distance, int32_t *o_triangle_id, float *o_point, void *stream);
+
 /* Whole run_batch on device arrays: build (tree_kind) + query (+ compaction
  * for barycentric).  boolean -> d_flags = crossing, count -> d_flags = counts;
  * barycentric -> d_ray_index/d_distance/d_triangle_id/d_point (n_r rows

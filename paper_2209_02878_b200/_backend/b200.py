@@ -236,6 +236,30 @@ def _store(out, lo, hi, mode, res):
         out[k][lo:hi] = v.cpu().numpy() if is_device_array(v) else v
 
 
+def baseline_compact(mesh, segments):
+    """All-pairs barycentric on device tensors with the ordered compaction
+    (rs_baseline_compact); returns a ResultSet of CUDA tensors."""
+    from ..engine import MODE_BARYCENTRIC, ResultSet
+
+    torch = _torch()
+    V = _dev(mesh.vertices, torch.float32)
+    T = _dev(mesh.triangles, torch.int32)
+    s = _dev(segments.starts, torch.float32)
+    e = _dev(segments.ends, torch.float32)
+    n = int(s.shape[0])
+    ray = torch.empty(n, dtype=torch.int32, device=s.device)
+    dist = torch.empty(n, dtype=torch.float32, device=s.device)
+    tri = torch.empty(n, dtype=torch.int32, device=s.device)
+    pt = torch.empty((n, 3), dtype=torch.float32, device=s.device)
+    k = C.c_int64(0)
+    _lib.check(_lib.lib().rs_baseline_compact(
+        _p(V), int(V.shape[0]), _p(T), int(T.shape[0]), _p(s), _p(e), n, _p(ray), _p(dist), _p(tri),
+        _p(pt), C.byref(k), _stream()))
+    m = k.value
+    return ResultSet(MODE_BARYCENTRIC, n, ray_index=ray[:m], distance=dist[:m], triangle_id=tri[:m],
+                     point=pt[:m])
+
+
 def baseline_dense(mesh, segments, mode: str) -> dict:
     """All-pairs on device; returns numpy rows for host inputs, tensors for
     device inputs."""

@@ -1081,11 +1081,81 @@ int rs_baseline(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_
         return fail(RS_INVALID_ARG, "bad sizes");
     (void)n_v;
     BaselineArgs a{d_verts, d_tris, (int)n_t, d_starts, d_ends, n_r, d_detected, d_counts,
-                   d_tri, d_dist, d_points};
+                   d_tri, d_dist, d_points, nullptr, nullptr};
     cudaStream_t s = S(stream);
     if (n_t > 0) launch_baseline(a, mode, s);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
+    return RS_OK;
+}
+
+int rs_baseline_compact(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
+                        const float* d_starts, const float* d_ends, int64_t n_r, int32_t* d_ray,
+                        float* d_dist, int32_t* d_tri, float* d_pt, int64_t* n_hits, void* stream) {
+    marks_reset();
+    if (n_hits) *n_hits = 0;
+    if (n_t < 0 || n_r < 0 || n_t > 2147483647ll || n_r > 2147483647ll)
+        return fail(RS_INVALID_ARG, "bad sizes");
+    if (!(d_ray && d_dist && d_tri && d_pt) && n_r > 0) return fail(RS_INVALID_ARG, "null output");
+    (void)n_v;
+    if (n_r == 0 || n_t == 0) return RS_OK;
+    cudaStream_t s = S(stream);
+    const size_t cs = bary_compact_scratch(n_r);
+    char* blk = nullptr;
+    const size_t total = align256(sizeof(RsStatus)) + align256(8ull * n_r) + align256(4ull * n_r) + align256(cs);
+    CK(dmalloc(reinterpret_cast<void**>(&blk), total, s));
+    Carver c{blk};
+    RsStatus* st = c.take<RsStatus>(1);
+    unsigned long long* best_t = c.take<unsigned long long>(n_r);
+    int* best_tri = c.take<int>(n_r);
+    unsigned long long* tiles = c.take<unsigned long long>(cs / 8);
+    CK(cudaMemsetAsync(st, 0, sizeof(RsStatus), s));
+    CK(cudaMemsetAsync(tiles, 0, cs, s));
+    BaselineArgs a{d_verts, d_tris, (int)n_t, d_starts, d_ends, n_r, nullptr, nullptr,
+                   nullptr, nullptr, nullptr, best_t, best_tri};
+    launch_baseline(a, kBarycentric, s);
+    CompactArgs ca{n_r, best_t, best_tri, d_starts, d_ends, d_ray, d_dist, d_tri, d_pt,
+                   tiles, tiles + (cs / 8 - 1), &st->hits, 0, nullptr};
+    launch_bary_compact(ca, s);
+    CK(cudaGetLastError());
+    RsStatus h;
+    int rc = read_status(st, s, &h);
+    CK(dfree(blk, s));
+    if (rc) return rc;
+    if (n_hits) *n_hits = (int64_t)h.hits;
+    return RS_OK;
+}
+
+int rs_segment_boxes(const float* d_starts, const float* d_ends, int64_t n, float* d_boxes,
+                     void* stream) {
+    if (n < 0) return fail(RS_INVALID_ARG, "negative count");
+    if (n && !(d_starts && d_ends && d_boxes)) return fail(RS_INVALID_ARG, "null array");
+    launch_segment_boxes(d_starts, d_ends, n, d_boxes, S(stream));
+    CK(cudaGetLastError());
+    return RS_OK;
+}
+
+int rs_unpermute_dense(const int64_t* d_perm, int64_t n, const int32_t* d_in, int32_t* d_out,
+                       void* stream) {
+    if (n < 0) return fail(RS_INVALID_ARG, "negative count");
+    if (n && !(d_perm && d_in && d_out)) return fail(RS_INVALID_ARG, "null array");
+    launch_unpermute_dense(reinterpret_cast<const long long*>(d_perm), n, d_in, d_out, S(stream));
+    CK(cudaGetLastError());
+    return RS_OK;
+}
+
+int rs_unpermute_rows(const int64_t* d_perm, int64_t n, const int32_t* d_ray, const float* d_dist,
+                      const int32_t* d_tri, const float* d_pt, int64_t k, int32_t* o_ray,
+                      float* o_dist, int32_t* o_tri, float* o_pt, void* stream) {
+    if (n < 0 || k < 0 || k > n) return fail(RS_INVALID_ARG, "bad sizes");
+    if (n == 0) return RS_OK;
+    cudaStream_t s = S(stream);
+    void* scratch = nullptr;
+    CK(dmalloc(&scratch, unpermute_scratch_bytes(n), s));
+    launch_unpermute_rows(reinterpret_cast<const long long*>(d_perm), n, d_ray, d_dist, d_tri, d_pt, k,
+                          o_ray, o_dist, o_tri, o_pt, scratch, s);
+    CK(cudaGetLastError());
+    CK(dfree(scratch, s));
     return RS_OK;
 }
 

@@ -147,4 +147,24 @@ void launch_generate(const float* V, const int* T, long long n_t, double z_lo, d
     count_launches(1);
 }
 
+// compute_segment_boxes (engine.py:115-122): (n,6) f32 [xmin,xmax,ymin,ymax,zmin,zmax].
+__global__ void __launch_bounds__(256) k_segment_boxes(const float* __restrict__ S, const float* __restrict__ E,
+                                                       long long n, float* __restrict__ B) {
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += gridDim.x * 256ll) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float p = __ldg(S + 3 * i + k), q = __ldg(E + 3 * i + k);
+            B[6 * i + 2 * k] = fminf(p, q);
+            B[6 * i + 2 * k + 1] = fmaxf(p, q);
+        }
+    }
+}
+
+void launch_segment_boxes(const float* S, const float* E, long long n, float* B, cudaStream_t s) {
+    if (n <= 0) return;
+    const long long want = (n + 255) / 256, cap = (long long)device_sms() * 8;
+    k_segment_boxes<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(S, E, n, B);
+    count_launches(1);
+}
+
 }  // namespace rs

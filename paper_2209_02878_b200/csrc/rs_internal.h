@@ -236,6 +236,16 @@ void launch_generate(const float* V, const int* T, long long n_t, double z_lo, d
                      long long first, long long n, float* S, float* E, unsigned char* flags,
                      cudaStream_t s);
 
+// sort_rays un-permutation (rs_trav.cu): dense rows out[perm[k]] = in[k];
+// barycentric rows re-ordered ascending by original index perm[ray[r]].
+void launch_unpermute_dense(const long long* perm, long long n, const int* in, int* out, cudaStream_t s);
+size_t unpermute_scratch_bytes(long long n);
+void launch_unpermute_rows(const long long* perm, long long n, const int* ray, const float* dist,
+                           const int* tri, const float* pt, long long k_rows, int* o_ray, float* o_dist,
+                           int* o_tri, float* o_pt, void* scratch, cudaStream_t s);
+
+void launch_segment_boxes(const float* S, const float* E, long long n, float* B, cudaStream_t s);
+
 struct BaselineArgs {
     const float* V;
     const int* T;
@@ -248,6 +258,10 @@ struct BaselineArgs {
     int* tri;
     float* dist;
     float* points;
+    // barycentric into per-segment (t key, triangle) for k_bary_compact
+    // instead of dense rows (null: dense)
+    unsigned long long* best_t;
+    int* best_tri;
 };
 void launch_baseline(const BaselineArgs& a, int mode, cudaStream_t s);
 

@@ -634,6 +634,9 @@ __global__ void __launch_bounds__(kBaseThreads) k_baseline(BaselineArgs a) {
         a.detected[i] = h.det;
     } else if (MODE == kCount) {
         a.counts[i] = h.n_hits;
+    } else if (a.best_tri) {
+        a.best_tri[i] = h.best_tri;
+        a.best_t[i] = h.best_tri >= 0 && h.best_t != 0.0 ? (unsigned long long)__double_as_longlong(h.best_t) : 0ull;
     } else {
         a.detected[i] = h.best_tri >= 0;
         a.tri[i] = h.best_tri;

@@ -598,6 +598,132 @@ void launch_exact(const ExactArgs& a, int mode, bool stats, cudaStream_t s) {
     }
 }
 
+// ---- sort_rays un-permutation on device (engine.py:191-198) ----------------
+//
+// Rows computed for Morton-sorted segments carry sorted slots; the caller
+// wants original indices, ascending.  boolean/count: out[perm[k]] = in[k].
+// barycentric: inv[perm[ray[r]]] = r over a dense n-array (-1 elsewhere), then
+// an ordered compaction of inv gathers the rows in ascending original index.
+__global__ void __launch_bounds__(256) k_unpermute_dense(const long long* __restrict__ perm, long long n,
+                                                         const int* __restrict__ in, int* __restrict__ out) {
+    for (long long k = blockIdx.x * 256ll + threadIdx.x; k < n; k += gridDim.x * 256ll) out[perm[k]] = in[k];
+}
+
+__global__ void __launch_bounds__(256) k_rows_inverse(const long long* __restrict__ perm,
+                                                      const int* __restrict__ ray, long long k_rows,
+                                                      int* __restrict__ inv) {
+    for (long long r = blockIdx.x * 256ll + threadIdx.x; r < k_rows; r += gridDim.x * 256ll)
+        inv[perm[ray[r]]] = (int)r;
+}
+
+struct GatherArgs {
+    const int* inv;
+    long long n;
+    const float* dist;
+    const int* tri;
+    const float* pt;
+    int* o_ray;
+    float* o_dist;
+    int* o_tri;
+    float* o_pt;
+    unsigned long long* tile_status;
+    unsigned long long* tile_counter;
+};
+
+// Ordered compaction of inv >= 0 (striped tiles and decoupled look-back, as
+// k_bary_compact), gathering row inv[i] to position rank(i).
+__global__ void __launch_bounds__(kCompactThreads) k_gather_compact(GatherArgs a) {
+    __shared__ unsigned s_round[kCompactItems][kCompactThreads / 32];
+    __shared__ unsigned long long s_prefix;
+    __shared__ int s_tile;
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1ull);
+    __syncthreads();
+    const long long tile = s_tile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const unsigned lt = (1u << l) - 1u;
+    const long long base = tile * kCompactTile;
+    int src[kCompactItems];
+    unsigned inwarp[kCompactItems];
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        const long long i = base + k * kCompactThreads + threadIdx.x;
+        src[k] = i < a.n ? a.inv[i] : -1;
+        const unsigned m = __ballot_sync(kFull, src[k] >= 0);
+        inwarp[k] = __popc(m & lt);
+        if (l == 0) s_round[k][w] = __popc(m);
+    }
+    __syncthreads();
+    if (w == 0) {
+        constexpr int kCells = kCompactItems * (kCompactThreads / 32);
+        unsigned v[kCells / 32], run = 0;
+#pragma unroll
+        for (int j = 0; j < kCells / 32; ++j) {
+            v[j] = (&s_round[0][0])[l * (kCells / 32) + j];
+            run += v[j];
+        }
+        unsigned x = run;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(kFull, x, o);
+            if (l >= o) x += y;
+        }
+        const unsigned agg = __shfl_sync(kFull, x, 31);
+        unsigned off = x - run;
+#pragma unroll
+        for (int j = 0; j < kCells / 32; ++j) {
+            const unsigned c = v[j];
+            (&s_round[0][0])[l * (kCells / 32) + j] = off;
+            off += c;
+        }
+        const unsigned long long excl = lookback_warp(a.tile_status, tile, agg);
+        if (l == 0) s_prefix = excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        if (src[k] < 0) continue;
+        const long long i = base + k * kCompactThreads + threadIdx.x;
+        const unsigned long long pos = s_prefix + s_round[k][w] + inwarp[k];
+        const long long r = src[k];
+        a.o_ray[pos] = (int)i;
+        a.o_dist[pos] = a.dist[r];
+        a.o_tri[pos] = a.tri[r];
+        a.o_pt[3 * pos] = a.pt[3 * r];
+        a.o_pt[3 * pos + 1] = a.pt[3 * r + 1];
+        a.o_pt[3 * pos + 2] = a.pt[3 * r + 2];
+    }
+}
+
+size_t unpermute_scratch_bytes(long long n) {
+    // inv (n ints), tile status words, tile counter
+    return ((4ull * n + 255) & ~255ull) + (size_t)((n + kCompactTile - 1) / kCompactTile) * 8 + 16;
+}
+
+void launch_unpermute_dense(const long long* perm, long long n, const int* in, int* out, cudaStream_t s) {
+    if (n <= 0) return;
+    count_launches(1);
+    const long long g = (n + 255) / 256;
+    k_unpermute_dense<<<(unsigned)(g < 4096 ? g : 4096), 256, 0, s>>>(perm, n, in, out);
+}
+
+void launch_unpermute_rows(const long long* perm, long long n, const int* ray, const float* dist,
+                           const int* tri, const float* pt, long long k_rows, int* o_ray, float* o_dist,
+                           int* o_tri, float* o_pt, void* scratch, cudaStream_t s) {
+    if (n <= 0) return;
+    int* inv = static_cast<int*>(scratch);
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(
+        static_cast<char*>(scratch) + ((4ull * n + 255) & ~255ull));
+    const long long tiles = (n + kCompactTile - 1) / kCompactTile;
+    cudaMemsetAsync(inv, 0xFF, 4ull * n, s);
+    cudaMemsetAsync(st, 0, (size_t)tiles * 8 + 16, s);
+    count_launches(2);
+    if (k_rows > 0) {
+        const long long g = (k_rows + 255) / 256;
+        k_rows_inverse<<<(unsigned)(g < 4096 ? g : 4096), 256, 0, s>>>(perm, ray, k_rows, inv);
+    }
+    GatherArgs a{inv, n, dist, tri, pt, o_ray, o_dist, o_tri, o_pt, st, st + tiles};
+    k_gather_compact<<<(unsigned)tiles, kCompactThreads, 0, s>>>(a);
+}
+
 size_t bary_compact_scratch(long long n_r) {
     return (size_t)((n_r + kCompactTile - 1) / kCompactTile) * 8 + 8;
 }

@@ -149,16 +149,17 @@ class EngineConfig:
 
 def compute_segment_boxes(segments: SegmentBatch):
     """(N_r,6) f32 segment AABBs [xmin,xmax,ymin,ymax,zmin,zmax]
-    (engine.py:115-122), on the device; kept for API parity (the query
-    kernels form the same boxes in registers).  numpy in, numpy out."""
+    (engine.py:115-122), on the device (rs_segment_boxes); kept for API
+    parity (the query kernels form the same boxes in registers).  numpy in,
+    numpy out; CUDA tensors in, CUDA tensor out."""
     import torch
 
     host = not segments.on_device
-    s = torch.from_numpy(segments.starts).cuda() if host else segments.starts
-    e = torch.from_numpy(segments.ends).cuda() if host else segments.ends
+    s = torch.from_numpy(np.ascontiguousarray(segments.starts)).cuda() if host else segments.starts
+    e = torch.from_numpy(np.ascontiguousarray(segments.ends)).cuda() if host else segments.ends
     boxes = torch.empty((s.shape[0], 6), dtype=torch.float32, device=s.device)
-    boxes[:, 0::2] = torch.minimum(s, e)
-    boxes[:, 1::2] = torch.maximum(s, e)
+    _lib.check(_lib.lib().rs_segment_boxes(_ptr(s), _ptr(e), int(s.shape[0]), _ptr(boxes),
+                                           _stream(s.device.index)))
     return boxes.cpu().numpy() if host else boxes
 
 
@@ -238,37 +239,35 @@ def _empty_result(mode: str, n: int, like_device=None) -> ResultSet:
 
 
 def _unpermute(rs: ResultSet, perm) -> ResultSet:
-    """engine.py:191-198 for permuted inputs, then re-sort compacted rows."""
+    """engine.py:191-198: results of Morton-sorted segments back in the
+    caller's order, on the device (rs_unpermute_dense / rs_unpermute_rows:
+    a scatter for the dense rows, an ordered gather-compaction for the
+    barycentric rows).  sort_rays always runs on the device (run_batch moves
+    host batches there), so `perm` is an int64 CUDA tensor."""
     if perm is None:
         return rs
-    dev = rs.mode != MODE_BARYCENTRIC and is_device_array(rs.crossing if rs.mode == MODE_BOOLEAN else rs.counts)
+    import torch
+
+    n = int(perm.shape[0])
+    lib = _lib.lib()
     if rs.mode in (MODE_BOOLEAN, MODE_COUNT):
         key = "crossing" if rs.mode == MODE_BOOLEAN else "counts"
         vals = getattr(rs, key)
-        if dev:
-            import torch
-
-            out = torch.empty_like(vals)
-            out[perm if torch.is_tensor(perm) else torch.from_numpy(perm).to(vals.device)] = vals
-        else:
-            out = np.empty_like(vals)
-            out[perm] = vals
+        out = torch.empty_like(vals)
+        _lib.check(lib.rs_unpermute_dense(_ptr(perm), n, _ptr(vals), _ptr(out), _stream(vals.device.index)))
         setattr(rs, key, out)
         return rs
-    ri = rs.ray_index
-    if is_device_array(ri):
-        import torch
-
-        pt = perm if torch.is_tensor(perm) else torch.from_numpy(perm).to(ri.device)
-        orig = pt[ri.long()]
-        order = torch.argsort(orig)
-        rs.ray_index = orig[order].to(torch.int32)
-        rs.distance, rs.triangle_id, rs.point = rs.distance[order], rs.triangle_id[order], rs.point[order]
-    else:
-        orig = perm[ri]
-        order = np.argsort(orig, kind="stable")
-        rs.ray_index = orig[order].astype(np.int32)
-        rs.distance, rs.triangle_id, rs.point = rs.distance[order], rs.triangle_id[order], rs.point[order]
+    k = int(rs.ray_index.shape[0])
+    dev = rs.ray_index.device
+    o_ray = torch.empty(k, dtype=torch.int32, device=dev)
+    o_dist = torch.empty(k, dtype=torch.float32, device=dev)
+    o_tri = torch.empty(k, dtype=torch.int32, device=dev)
+    o_pt = torch.empty((k, 3), dtype=torch.float32, device=dev)
+    _lib.check(lib.rs_unpermute_rows(
+        _ptr(perm), n, _ptr(rs.ray_index.contiguous()), _ptr(rs.distance.contiguous()),
+        _ptr(rs.triangle_id.contiguous()), _ptr(rs.point.contiguous()), k, _ptr(o_ray), _ptr(o_dist),
+        _ptr(o_tri), _ptr(o_pt), _stream(dev.index)))
+    rs.ray_index, rs.distance, rs.triangle_id, rs.point = o_ray, o_dist, o_tri, o_pt
     return rs
 
 
@@ -408,21 +407,18 @@ def run_baseline_allpairs(mesh: Mesh, segments: SegmentBatch,
     timings = {}
     if config.sort_rays:
         segments, perm, timings["ray sort"] = _timed_sort(segments)
-    out = b200.baseline_dense(mesh, segments, config.mode)
+    if config.mode == MODE_BARYCENTRIC:  # ordered compaction on device (rs_baseline_compact)
+        rs = b200.baseline_compact(mesh, segments)
+    else:
+        rs = _assemble_dense(config.mode, b200.baseline_dense(mesh, segments, config.mode), n, dev)
     timings.update(_lib.last_phases())
-    rs = _assemble_dense(config.mode, out, n, dev)
     rs.timings = timings
     return _unpermute(rs, perm)
 
 
 def _assemble_dense(mode: str, out: dict, n: int, dev: bool) -> ResultSet:
-    """engine.py:200-215 over dense per-segment rows."""
+    """engine.py:200-215 over dense per-segment rows (boolean / count; the
+    barycentric rows come compacted from rs_baseline_compact)."""
     if mode == MODE_BOOLEAN:
         return ResultSet(mode, n, crossing=out["detected"])
-    if mode == MODE_COUNT:
-        return ResultSet(mode, n, counts=out["counts"])
-    import torch
-
-    idx = torch.nonzero(out["detected"]).flatten()
-    return ResultSet(mode, n, ray_index=idx.to(torch.int32), distance=out["dist"][idx],
-                     triangle_id=out["tri"][idx], point=out["points"][idx])
+    return ResultSet(mode, n, counts=out["counts"])

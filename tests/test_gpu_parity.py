@@ -779,3 +779,28 @@ def test_hit_bitmap_path(name, variant, device):
             with _lib.option("device_chunk", 1024):
                 got = rs.run_batch(mesh, batch, rs.EngineConfig(mode="boolean", tree="fast"))
             assert_result_fields(result_dict(got), want, f"{name} bitmap chunked")
+
+
+@pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
+def test_compute_segment_boxes(device):
+    """rs_segment_boxes == the reference's f32 min/max layout (engine.py:115-122)."""
+    fx = load("soup_17")
+    s, e = fx["starts"], fx["ends"]
+    want = np.empty((s.shape[0], 6), np.float32)
+    want[:, 0::2] = np.minimum(s, e)
+    want[:, 1::2] = np.maximum(s, e)
+    _, batch = mesh_batch(fx, device)
+    assert np.array_equal(_np(rs.compute_segment_boxes(batch)), want)
+
+
+@pytest.mark.parametrize("sort_rays", [False, True])
+@pytest.mark.parametrize("name", ("c1", "soup:17", "s19"))
+def test_baseline_barycentric_compaction(name, sort_rays):
+    """rs_baseline_compact (ordered compaction on device) and the sort_rays
+    un-permutation of its rows, against the reference's baseline rows."""
+    fx = load(f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}")
+    want = expected(fx, "batch", "barycentric")
+    for device in (False, True):
+        mesh, batch = mesh_batch(fx, device)
+        got = rs.run_baseline_allpairs(mesh, batch, rs.EngineConfig(mode="barycentric", sort_rays=sort_rays))
+        assert_result_fields(result_dict(got), want, f"{name} baseline bary sort={sort_rays}")

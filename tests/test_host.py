@@ -114,15 +114,39 @@ def test_morton_encode_known_answers():
     assert np.array_equal(O.quantize(fx["pts"], lo, hi), fx["pts_q"])
 
 
+@pytest.mark.gpu
 def test_unpermute_barycentric_rows():
+    """rs_unpermute_rows / rs_unpermute_dense (sort_rays un-permutation)."""
+    import torch
+
     from paper_2209_02878_b200.engine import ResultSet, _unpermute
 
-    perm = np.array([3, 0, 2, 1])
-    r = ResultSet("barycentric", 4, ray_index=np.array([0, 2, 3], np.int32),
-                  distance=np.array([1, 2, 3], np.float32), triangle_id=np.array([7, 8, 9], np.int32),
-                  point=np.arange(9, dtype=np.float32).reshape(3, 3))
+    cuda = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    perm = cuda(np.array([3, 0, 2, 1], np.int64))
+    r = ResultSet("barycentric", 4, ray_index=cuda(np.array([0, 2, 3], np.int32)),
+                  distance=cuda(np.array([1, 2, 3], np.float32)),
+                  triangle_id=cuda(np.array([7, 8, 9], np.int32)),
+                  point=cuda(np.arange(9, dtype=np.float32).reshape(3, 3)))
     r = _unpermute(r, perm)
     assert r.ray_index.tolist() == [1, 2, 3]
     assert r.triangle_id.tolist() == [9, 8, 7]
-    b = _unpermute(ResultSet("boolean", 4, crossing=np.array([1, 0, 0, 1], np.int32)), perm)
+    assert r.distance.tolist() == [3, 2, 1]
+    assert r.point.tolist() == [[6, 7, 8], [3, 4, 5], [0, 1, 2]]
+    b = _unpermute(ResultSet("boolean", 4, crossing=cuda(np.array([1, 0, 0, 1], np.int32))), perm)
     assert b.crossing.tolist() == [0, 1, 0, 1]
+    # a large random permutation against numpy
+    rng = np.random.default_rng(5)
+    n = 300_000
+    pm = rng.permutation(n).astype(np.int64)
+    rows = np.sort(rng.choice(n, 100_000, replace=False)).astype(np.int32)
+    dist = rng.random(rows.size).astype(np.float32)
+    tri = rng.integers(0, 1000, rows.size).astype(np.int32)
+    pt = rng.random((rows.size, 3)).astype(np.float32)
+    r = _unpermute(ResultSet("barycentric", n, ray_index=cuda(rows), distance=cuda(dist),
+                             triangle_id=cuda(tri), point=cuda(pt)), cuda(pm))
+    orig = pm[rows]
+    order = np.argsort(orig, kind="stable")
+    assert np.array_equal(r.ray_index.cpu().numpy(), orig[order])
+    assert np.array_equal(r.distance.cpu().numpy(), dist[order])
+    assert np.array_equal(r.triangle_id.cpu().numpy(), tri[order])
+    assert np.array_equal(r.point.cpu().numpy(), pt[order])
