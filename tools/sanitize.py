@@ -7,7 +7,12 @@ host inputs, and through a captured graph:
   binning:    k_seg_sample, k_bin_count_tma, k_bin_scan1, k_bin_scatter
   traversal:  k_trav_tile (dense batch), k_trav_sorted_bin (sparse batch),
               k_query_dense (reference semantics)
-  output:     k_bary_compact, k_status_out, k_baseline
+  output:     k_bary_compact, k_status_out, k_baseline (dense and compacted)
+  round 2:    k_generate (device segments), k_expand_bits (hit bitmap of
+              large boolean batches, forced on small ones via hitbits_min),
+              the device-chunked loop (device_chunk), k_unpermute_dense /
+              k_rows_inverse / k_gather_compact (sort_rays on device),
+              k_segment_boxes, inside_closed_surface (count mode)
 Exits non-zero if any result differs from the generator's ground truth.
 
 usage: compute-sanitizer --tool memcheck python tools/sanitize.py [small]
@@ -63,5 +68,32 @@ truth = sc.expected_crossings.astype(np.int32)
 for mode in rs.MODES:
     check(rs.run_baseline_allpairs(sc.mesh, sc.segments, rs.EngineConfig(mode=mode)), truth, mode, f"baseline {mode}")
     check(rs.run_batch(sc.mesh, sc.segments, rs.EngineConfig(mode=mode, sort_rays=True)), truth, mode, f"sort_rays {mode}")
+from paper_2209_02878_b200 import _lib
+
+# device generator + hit bitmap + device-chunked loop
+mesh = rs.generate_scene(2000, 0, 0.5, seed=2022).mesh
+dmesh = rs.Mesh.from_arrays(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.triangles).cuda())
+segs, flags = rs.generate_segments_device(dmesh, 40_000 if small else 200_000, 0.5, seed=9, first=123)
+truth = flags.cpu().numpy().astype(np.int32)
+with _lib.option("hitbits_min", 1):
+    check(rs.run_batch(dmesh, segs, rs.EngineConfig(mode="boolean")), truth, "boolean", "bitmap")
+    with _lib.option("device_chunk", 8192):
+        check(rs.run_batch(dmesh, segs, rs.EngineConfig(mode="boolean")), truth, "boolean", "chunked bitmap")
+with _lib.option("device_chunk", 8192):
+    for mode in ("count", "barycentric"):
+        check(rs.run_batch(dmesh, segs, rs.EngineConfig(mode=mode)), truth, mode, f"chunked {mode}")
+# sort_rays on device tensors (un-permutation kernels), segment boxes
+for mode in rs.MODES:
+    check(rs.run_batch(dmesh, segs, rs.EngineConfig(mode=mode, sort_rays=True)), truth, mode, f"dev sort_rays {mode}")
+    check(rs.run_baseline_allpairs(dmesh, rs.SegmentBatch(segs.starts[:3000], segs.ends[:3000]),
+                                   rs.EngineConfig(mode=mode, sort_rays=True)), truth[:3000], mode,
+          f"dev baseline sort_rays {mode}")
+rs.compute_segment_boxes(segs)
+# odd parity on a closed cube
+v = np.array([[x, y, z] for x in (-0.5, 0.5) for y in (-0.5, 0.5) for z in (-0.5, 0.5)], np.float32)
+quads = [(0, 1, 3, 2), (4, 6, 7, 5), (0, 4, 5, 1), (2, 3, 7, 6), (0, 2, 6, 4), (1, 5, 7, 3)]
+t = np.array([tri for a, b, c, d in quads for tri in ((a, b, c), (a, c, d))], np.int32)
+pts = np.array([[0, 0, 0], [2, 0, 0]], np.float32)
+assert rs.inside_closed_surface(pts, rs.Mesh.from_arrays(v, t)).tolist() == [True, False]
 torch.cuda.synchronize()
 print("sanitize workload ok")
