@@ -94,6 +94,9 @@ struct rs_tree {
     const unsigned long long* codes = nullptr;
     unsigned long long* code_samples = nullptr;
     int sample_stride = 0, n_samples = 0, key_mode = 0;
+    // leaf index by triangle id (barycentric compaction's t recompute);
+    // allocated by the first barycentric fast query, freed with the tree
+    int* leaf_of = nullptr;
 };
 
 namespace {
@@ -720,6 +723,7 @@ int rs_tree_download(const rs_tree* t, float* ib, int32_t* cl, int32_t* cr, int3
 int rs_free(rs_tree* t, void* stream) {
     if (!t) return RS_OK;
     if (t->scratch) dfree(t->scratch, S(stream));
+    if (t->leaf_of) dfree(t->leaf_of, S(stream));
     cudaError_t e = dfree(t->block, S(stream));
     delete t;
     if (e != cudaSuccess) return fail(RS_CUDA_ERROR, "cudaFreeAsync: %s", cudaGetErrorString(e));
@@ -781,8 +785,12 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     size_t total = 256;
     total += align256(sizeof(RsStatus));
     total += align256(8ull * cap) + align256(4ull * (cap / kCandChunk + 1));
+    // barycentric: the sorted path keeps only the winning triangle per
+    // segment (the compaction recomputes t); the collision-buffer path's
+    // atomicMin needs the t keys
+    const bool keys = bary && buffer_path();
     if (bary)
-        total += align256(8ull * n_r) + align256(4ull * n_r) + align256(8ull * cap) +
+        total += (keys ? align256(8ull * n_r) : 0) + align256(4ull * n_r) + align256(8ull * cap) +
                  align256(bary_compact_scratch(n_r));
     if (buffer_path()) total += align256(4 * trav_gstack_ints());
     const bool bits = mode == kBoolean && !buffer_path() && n_r >= g_hitbits_min.load();
@@ -795,7 +803,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     f.cand = c.take<int2>(cap);
     f.chunk_fill = c.take<int>(cap / kCandChunk + 1);
     if (bary) {
-        f.best_t = c.take<unsigned long long>(n_r);
+        f.best_t = keys ? c.take<unsigned long long>(n_r) : nullptr;
         f.best_tri = c.take<int>(n_r);
         f.cand_t = c.take<unsigned long long>(cap);
         f.tiles = c.take<unsigned long long>(bary_compact_scratch(n_r) / 8);
@@ -843,7 +851,7 @@ static int fast_presets(const float* d_s, const float* d_e, int64_t n_r, int mod
     if (f.hitbits) CK(cudaMemsetAsync(f.hitbits, 0, 4ull * ((n_r + 31) / 32), s));
     else if (!bary && !binning_zeroes_flags(d_s, d_e, n_r, o.flags)) CK(cudaMemsetAsync(o.flags, 0, 4ull * n_r, s));
     if (bary) {
-        CK(cudaMemsetAsync(f.best_t, 0xFF, 8ull * n_r, s));
+        if (f.best_t) CK(cudaMemsetAsync(f.best_t, 0xFF, 8ull * n_r, s));
         CK(cudaMemsetAsync(f.best_tri, 0xFF, 4ull * n_r, s));
         CK(cudaMemsetAsync(f.tiles, 0, f.tiles_bytes, s));
     }
@@ -870,8 +878,12 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
     launch_sorted_trav(sorted_args(t, d_s, d_e, n_r, o, f), mode, stats, s);
     if (f.hitbits) launch_expand_bits(o.flags, f.hitbits, n_r, s);
     if (mode == kBarycentric) {
+        if (!f.best_t) {  // the compaction recomputes t from the winning leaf
+            if (!t->leaf_of) CK(dmalloc(reinterpret_cast<void**>(&const_cast<rs_tree*>(t)->leaf_of), 4ull * t->n, s));
+            launch_leaf_inverse(t->leaves, (int)t->n, t->leaf_of, s);
+        }
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
-                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base};
+                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base, t->leaves, t->leaf_of};
         if (o.c_ray) launch_bary_compact(ca, s);
         else launch_bary_dense(ca, o.det, o.tri, o.dist, o.pts, s);
     }

@@ -146,7 +146,14 @@ struct CompactArgs {
     unsigned long long* n_hits;
     long long ray_offset;
     unsigned long long* row_base;  // optional: rows land at *row_base + rank, then *row_base += hits
+    // best_t == null (sorted fast path): t is recomputed for each hit row
+    // from its winning triangle -- leaves[leaf_of[tri]] -- with the same f64
+    // test, instead of being stored per segment by the traversal
+    const RsLeaf* leaves;
+    const int* leaf_of;
 };
+// leaf_of[leaves[k].id] = k for the n leaves (the compaction's t recompute).
+void launch_leaf_inverse(const RsLeaf* leaves, int n, int* leaf_of, cudaStream_t s);
 void launch_trav(const TravArgs& a, bool stats, cudaStream_t s);
 
 // Coherent fast path (rs_sorted.cu): root cull + counting sort into spatial

@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(kSortedThreads) k_trav_sorted(SortedArgs a) {
         } else if (MODE == kCount) {
             if (nh) a.flags[id] = nh;
         } else if (btri >= 0) {
-            a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
+            if (a.best_t) a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
             a.best_tri[id] = btri;
         }
     }
@@ -956,7 +956,7 @@ __device__ __forceinline__ void write_result(const SortedArgs& a, int id, int de
     } else if (MODE == kCount) {
         if (nh) a.flags[id] = nh;
     } else if (btri >= 0) {
-        a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
+        if (a.best_t) a.best_t[id] = bt == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(bt);
         a.best_tri[id] = btri;
     }
 }

@@ -457,6 +457,35 @@ __global__ void __launch_bounds__(256) k_tiebreak(ExactArgs a) {
 // at their final ascending positions with point/distance computed from the
 // winning t in reference op order (_core.pyx:330-348).
 constexpr int kCompactThreads = 256;
+
+// The winning hit's t: stored by the traversal (best_t), or recomputed from
+// the winning triangle's leaf record with the same f64 test (identical
+// operands and op order as the traversal's mt_hit_pre, so the same t).
+__device__ __forceinline__ double win_t(const CompactArgs& a, long long i, int tri, double sx,
+                                        double sy, double sz, double dx, double dy, double dz) {
+    if (a.best_t) {
+        const unsigned long long key = a.best_t[i];
+        return key == 0ull ? 0.0 : __longlong_as_double((long long)key);
+    }
+    const RsLeaf* L = a.leaves + __ldg(a.leaf_of + tri);
+    const float4 p0 = __ldg(&L->p0), p1 = __ldg(&L->p1), p2 = __ldg(&L->p2);
+    double t = 0.0;
+    mt_hit(p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, p2.x, sx, sy, sz, dx, dy, dz, &t);
+    return t;
+}
+
+__global__ void __launch_bounds__(256) k_leaf_inverse(const RsLeaf* __restrict__ leaves, int n,
+                                                      int* __restrict__ leaf_of) {
+    for (int k = blockIdx.x * 256 + threadIdx.x; k < n; k += gridDim.x * 256)
+        leaf_of[__float_as_int(__ldg(&leaves[k].p2.y))] = k;
+}
+
+void launch_leaf_inverse(const RsLeaf* leaves, int n, int* leaf_of, cudaStream_t s) {
+    if (n <= 0) return;
+    count_launches(1);
+    const int g = (n + 255) / 256;
+    k_leaf_inverse<<<g < 2048 ? g : 2048, 256, 0, s>>>(leaves, n, leaf_of);
+}
 constexpr int kCompactItems = 16;
 constexpr int kCompactTile = kCompactThreads * kCompactItems;
 
@@ -520,14 +549,14 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
         if (tri[k] < 0) continue;
         const long long i = base + k * kCompactThreads + threadIdx.x;
         const unsigned long long pos = tb + s_round[k][w] + inwarp[k];
-        const unsigned long long key = a.best_t[i];
-        const double t = key == 0ull ? 0.0 : __longlong_as_double((long long)key);
         const float* s = a.starts + 3 * i;
         const float* e = a.ends + 3 * i;
         const double sx = s[0], sy = s[1], sz = s[2];
+        const double dx = __dsub_rn((double)e[0], sx), dy = __dsub_rn((double)e[1], sy),
+                     dz = __dsub_rn((double)e[2], sz);
+        const double t = win_t(a, i, tri[k], sx, sy, sz, dx, dy, dz);
         float px, py, pz, d;
-        hit_point(sx, sy, sz, __dsub_rn((double)e[0], sx), __dsub_rn((double)e[1], sy),
-                  __dsub_rn((double)e[2], sz), t, &px, &py, &pz, &d);
+        hit_point(sx, sy, sz, dx, dy, dz, t, &px, &py, &pz, &d);
         a.ray[pos] = (int)(i + a.ray_offset);
         a.dist[pos] = d;
         a.tri[pos] = tri[k];
@@ -544,13 +573,13 @@ __global__ void __launch_bounds__(256) k_bary_dense(CompactArgs a, int* detected
     const int tri = a.best_tri[i];
     float px = 0.f, py = 0.f, pz = 0.f, d = 0.f;
     if (tri >= 0) {
-        const unsigned long long k = a.best_t[i];
-        const double t = k == 0ull ? 0.0 : __longlong_as_double((long long)k);
         const float* s = a.starts + 3 * i;
         const float* e = a.ends + 3 * i;
         const double sx = s[0], sy = s[1], sz = s[2];
-        hit_point(sx, sy, sz, __dsub_rn((double)e[0], sx), __dsub_rn((double)e[1], sy),
-                  __dsub_rn((double)e[2], sz), t, &px, &py, &pz, &d);
+        const double dx = __dsub_rn((double)e[0], sx), dy = __dsub_rn((double)e[1], sy),
+                     dz = __dsub_rn((double)e[2], sz);
+        const double t = win_t(a, i, tri, sx, sy, sz, dx, dy, dz);
+        hit_point(sx, sy, sz, dx, dy, dz, t, &px, &py, &pz, &d);
     }
     detected[i] = tri >= 0;
     tri_out[i] = tri;
