@@ -458,6 +458,19 @@ def main():
         if not timing_level:
             hot_ms.append(hms.value)
     lib.rs_set_timing(0)
+    stage_ms = None
+    if os.environ.get("RS_BENCH_STAGES"):
+        # diagnostics: per-stage marks on both streams (outside the timed
+        # region; include/raysurf_b200.h rs_stage_times lists the marks)
+        lib.rs_set_timing(3)
+        arr = (C.c_float * 16)()
+        rows = []
+        for _ in range(7):
+            step()
+            lib.rs_stage_times(arr, 16)
+            rows.append(list(arr))
+        lib.rs_set_timing(0)
+        stage_ms = [round(float(np.median([r[k] for r in rows[2:]])), 4) for k in range(16)]
     if world > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
@@ -556,6 +569,8 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks.summary(t_start, t_end + 0.02),
     }
+    if stage_ms is not None:
+        line["phase_ms"]["stages"] = stage_ms
     if os.environ.get("RS_DEBUG_STATUS"):
         st = (C.c_ulonglong * 8)()
         lib.rs_last_status(st)

@@ -754,4 +754,12 @@ void launch_code_samples(const unsigned long long* codes, int n, int stride,
     k_code_samples<<<(m + 255) / 256, 256, 0, s>>>(codes, n, stride, samples, m);
 }
 
+// The build's kernels (captured graphs give them the highest node priority,
+// rs_capi.cu capture_graph).
+bool is_build_kernel(const void* f) {
+    return f == (const void*)k_prep || f == (const void*)k_keys || f == (const void*)k_sort_hist ||
+           f == (const void*)k_onesweep || f == (const void*)k_climb_lean || f == (const void*)k_climb ||
+           f == (const void*)k_code_samples;
+}
+
 }  // namespace rs

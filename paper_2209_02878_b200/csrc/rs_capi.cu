@@ -1172,8 +1172,9 @@ int rs_unpermute_rows(const int64_t* d_perm, int64_t n, const int32_t* d_ray, co
 }
 
 struct Fork {
-    cudaStream_t aux = nullptr;
-    cudaEvent_t prep = nullptr, bin = nullptr, bin2 = nullptr;
+    cudaStream_t aux = nullptr;  // binning (default priority)
+    cudaStream_t hp = nullptr;   // the build, at the highest stream priority
+    cudaEvent_t prep = nullptr, bin = nullptr, bin2 = nullptr, start = nullptr, built = nullptr;
 };
 static thread_local Fork g_fork;
 
@@ -1183,8 +1184,21 @@ static int fork_init() {
     CK(cudaEventCreateWithFlags(&g_fork.prep, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g_fork.bin, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g_fork.bin2, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g_fork.start, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g_fork.built, cudaEventDisableTiming));
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&g_fork.hp, cudaStreamNonBlocking, hi));
     return RS_OK;
 }
+
+// The build runs on a high-priority stream beside the binning: its small,
+// latency-bound kernels (keys, 4 sort passes, climb) otherwise queue behind
+// the bandwidth-bound binning CTAs for SM slots (RS_BUILD_PRIO=0: A/B).
+static const bool g_build_prio = [] {
+    const char* e = getenv("RS_BUILD_PRIO");
+    return !(e && e[0] == '0');
+}();
 
 // RS_PIPELINE_PARTS=2: large batches are binned and traversed in two halves,
 // so the second half's binning (memory-bound) overlaps the first half's
@@ -1216,8 +1230,14 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
     const int64_t n1 = two ? ((n_r / 2 + 1023) / 1024) * 1024 : n_r, n2 = n_r - n1;
     FastOut o1 = o, o2 = o;
     FastScratch f2;
+    cudaStream_t bs = s;  // the build's stream
+    if (g_build_prio) {
+        bs = g_fork.hp;
+        CK(cudaEventRecord(g_fork.start, s));
+        CK(cudaStreamWaitEvent(bs, g_fork.start, 0));
+    }
     auto fork = [&](rs_tree* t) -> int {
-        CK(cudaEventRecord(g_fork.prep, s));
+        CK(cudaEventRecord(g_fork.prep, bs));
         CK(cudaStreamWaitEvent(aux, g_fork.prep, 0));
         int r = fast_alloc(f, n1, mode, 2ll * n1 + 4096, aux);
         if (r) return r;
@@ -1244,8 +1264,12 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
         return RS_OK;
     };
     rs_tree* t = nullptr;
-    rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, s, &t, fork, true);
+    rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, bs, &t, fork, true);
     if (rc) return rc;
+    if (bs != s) {
+        CK(cudaEventRecord(g_fork.built, bs));
+        CK(cudaStreamWaitEvent(s, g_fork.built, 0));
+    }
     CK(cudaStreamWaitEvent(s, g_fork.bin, 0));
     if (!two) {
         rc = fast_trav(t, d_starts, d_ends, n_r, mode, o1, f, false, s);
@@ -1599,7 +1623,30 @@ static std::shared_ptr<GraphEntry> capture_graph(const float* d_verts, int64_t n
     e->marks = g_marks;
     g_pool.erase(g_pool.begin(), g_pool.begin() + (ptrdiff_t)g_pool_used);
     marks_reset();
-    const bool ok = erc == RS_OK && g && cudaGraphInstantiate(&e->exec, g, 0) == cudaSuccess;
+    // the build's kernel nodes at the highest priority: the binning's CTAs
+    // otherwise hold the SMs the latency-bound build kernels need (the
+    // graph runs with per-node priorities)
+    if (erc == RS_OK && g && g_build_prio) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(g, nodes.data(), &nn);
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp{};
+            if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess || !rs::is_build_kernel(kp.func)) continue;
+            cudaKernelNodeAttrValue v{};
+            v.priority = hi;
+            cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v);
+        }
+        cudaGetLastError();
+    }
+    const bool ok = erc == RS_OK && g &&
+                    cudaGraphInstantiate(&e->exec, g, g_build_prio ? cudaGraphInstantiateFlagUseNodePriority : 0) ==
+                        cudaSuccess;
     if (g) cudaGraphDestroy(g);
     if (!ok) {
         cudaGetLastError();

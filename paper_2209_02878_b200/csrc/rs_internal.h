@@ -35,6 +35,8 @@ struct TreeArrays {
     int* parent;         // (2n,) parent internal node by node ref (root: -1)
 };
 
+bool is_build_kernel(const void* f);
+
 void launch_prep(const float* V, const int* T, int n, double* cent, RsHeader* hdr,
                  const TreeArrays& ta, bool centroids, cudaStream_t s, bool lean = false);
 // Query-only climb: RsNode/RsLeaf records and the root, no SoA fields.
