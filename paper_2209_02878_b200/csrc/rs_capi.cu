@@ -757,7 +757,6 @@ struct FastScratch {
     int* gstack = nullptr;
     unsigned *bins = nullptr, *cursor = nullptr, *n_live = nullptr;
     float4* rec = nullptr;
-    unsigned long long* seg_key = nullptr;
     void* geom = nullptr;
     unsigned* hitbits = nullptr;  // large boolean batches: hit bitmap (see SortedArgs::hitbits)
 };
@@ -795,7 +794,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     if (buffer_path()) total += align256(4 * trav_gstack_ints());
     const bool bits = mode == kBoolean && !buffer_path() && n_r >= g_hitbits_min.load();
     total += 3 * align256(4 * sorted_bins()) + align256(4 * (64 + 4 * 32)) + align256(32ull * n_r) +
-             align256(8ull * (bin_rank_on() ? n_r : 1)) + align256(bin_geom_bytes()) +
+             align256(bin_geom_bytes()) +
              (bits ? align256(4ull * ((n_r + 31) / 32)) : 0);
     CK(dmalloc(reinterpret_cast<void**>(&f.blk), total, s));
     Carver c{f.blk};
@@ -815,7 +814,6 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
     f.cursor = c.take<unsigned>(sorted_bins());
     f.n_live = c.take<unsigned>(64 + 4 * 32);
     f.rec = c.take<float4>(2ull * n_r);
-    f.seg_key = c.take<unsigned long long>(bin_rank_on() ? n_r : 1);
     f.geom = c.take<char>(bin_geom_bytes());
     f.hitbits = bits ? c.take<unsigned>((n_r + 31) / 32) : nullptr;
     f.cap = cap;
@@ -825,7 +823,7 @@ static int fast_alloc(FastScratch& f, int64_t n_r, int mode, long long cap, cuda
 static SortedArgs sorted_args(const rs_tree* t, const float* d_s, const float* d_e, int64_t n_r,
                               const FastOut& o, FastScratch& f) {
     SortedArgs a{t->nodes4, t->nodes, t->leaves, t->hdr, (int)(t->n - 1), d_s, d_e, n_r,
-                      f.bins, f.cursor, f.n_live, reinterpret_cast<float*>(f.n_live + 64), f.bins + sorted_bins(), f.rec, f.seg_key, o.flags,
+                      f.bins, f.cursor, f.n_live, reinterpret_cast<float*>(f.n_live + 64), f.bins + sorted_bins(), f.rec, o.flags,
                       f.best_t, f.best_tri, f.st};
     a.codes = t->codes;
     a.code_samples = t->code_samples;

@@ -175,13 +175,11 @@ struct SortedArgs {
     float* seg_stats;    // k_seg_sample: per-CTA (sum of box sides x/y/z, live count)
     unsigned* tile_sum;  // sorted_bins()/1024 per-tile counts (zeroed) -> tile offsets
     float4* rec;         // n_r x 32-B records (start, id, end)
-    unsigned long long* seg_key;  // n_r: bin << 32 | rank within bin (~0: dead), from the histogram pass
     int* flags;                  // boolean / count output (pre-zeroed)
     unsigned long long* best_t;  // barycentric (pre-set ~0)
     int* best_tri;               // barycentric (pre-set -1)
     RsStatus* status;
     unsigned bin_occupancy;  // binning: target live segments per bin (set at launch)
-    int rec_ids;             // rec holds 4-B segment ids instead of 32-B records (set at launch)
     unsigned tile_area;  // tile traversal: target triangles' worth of records per tile (set at launch)
     unsigned tile_depth; // tile traversal: records per tile <= tile_depth / depth complexity (0: off)
     // Morton-range candidate lists (fast lean trees; codes == nullptr disables)
@@ -193,7 +191,6 @@ struct SortedArgs {
     unsigned range_max;                      // scan at most this many leaves, else walk
     int key_mode;                            // keys' grid: 0 isotropic, 1 per-axis
     unsigned tile_balance;      // tile traversal: at least this many tiles per CTA
-    unsigned warp_chunks;       // warp tiles: 32-record chunks per warp unit
     unsigned tile_min_density;  // tile traversal only above this many records per triangle
     int zero_flags;             // the histogram pass zeroes flags (instead of a preset memset)
     void* geom;                 // bin_geom_bytes(): bin geometry, written by k_seg_sample
@@ -226,8 +223,6 @@ int fast_key_mode();
 // (default), 1 collision buffer (pair traversal -> warp-aggregated append ->
 // exact pass, re-launched with a sized buffer on overflow).
 int fast_path();
-// Option bin_rank (A/B): the histogram pass records each segment's slot (needs seg_key).
-bool bin_rank_on();
 // Initial collision-buffer capacity in entries (option "cand_cap"; 0: 2 x segments + 4096).
 long long cand_cap_override();
 // Name of the traversal kernel the last launch_sorted_trav chose.

@@ -73,29 +73,18 @@ __device__ __forceinline__ void st_rec(float4* dst, const float s[3], int id, co
                  : "memory");
 }
 
-// Sorted-order segment access.  Records mode (default): the scatter wrote
-// each live segment's 32-B record (start, id, end).  Ids mode (rec_ids=1,
-// A/B): the scatter writes only the 4-B segment id and the traversal reads
-// the rows from the caller's arrays; measured 3.7x slower traversal on C2
-// (the gathered rows miss L1 and are re-read from DRAM) for a 7% faster
-// scatter.
+// Sorted-order segment access: the scatter wrote each live segment's 32-B
+// record (start, id, end).  (Writing only 4-B segment ids and gathering the
+// rows in the traversal measured 3.7x slower on C2: the gathered rows miss
+// L1 and are re-read from DRAM.)
 __device__ __forceinline__ void get_rec(const SortedArgs& a, unsigned idx, float4& r0, float4& r1) {
-    if (a.rec_ids) {
-        const int id = __ldg(reinterpret_cast<const int*>(a.rec) + idx);
-        const float* S = a.starts + 3ll * id;
-        const float* E = a.ends + 3ll * id;
-        r0 = make_float4(__ldg(S), __ldg(S + 1), __ldg(S + 2), __int_as_float(id));
-        r1 = make_float4(__ldg(E), __ldg(E + 1), __ldg(E + 2), 0.f);
-    } else {
-        r0 = a.rec[2ull * idx];
-        r1 = a.rec[2ull * idx + 1];
-    }
+    r0 = a.rec[2ull * idx];
+    r1 = a.rec[2ull * idx + 1];
 }
 
 __device__ __forceinline__ void put_rec(const SortedArgs& a, unsigned pos, const float s[3], int id,
                                         const float e[3]) {
-    if (a.rec_ids) reinterpret_cast<int*>(a.rec)[pos] = id;
-    else st_rec(a.rec + 2ull * pos, s, id, e);
+    st_rec(a.rec + 2ull * pos, s, id, e);
 }
 
 __device__ __forceinline__ unsigned spread3(unsigned v) {  // bit i -> bit 3i (i < 10)
@@ -656,14 +645,13 @@ __device__ __forceinline__ void stream_segments(const SortedArgs& a, Body&& body
     }
 }
 
-template <bool RANK>
 __global__ void __launch_bounds__(kStreamThreads) k_bin_count_tma(SortedArgs a) {
     RootInfo ri;
     const BinLut* lut;
     root_info(a, ri, lut);
     const int lane = threadIdx.x & 31;
     stream_segments(a, [&](float (&s)[4][3], float (&e)[4][3], int cnt, long long q) {
-        if (!RANK && a.zero_flags) {  // the boolean/count outputs' zero preset, fused
+        if (a.zero_flags) {  // the boolean/count outputs' zero preset, fused
             if (cnt == 4) {
                 *reinterpret_cast<int4*>(a.flags + 4 * q) = make_int4(0, 0, 0, 0);
             } else {
@@ -674,106 +662,15 @@ __global__ void __launch_bounds__(kStreamThreads) k_bin_count_tma(SortedArgs a) 
 #pragma unroll
         for (int j = 0; j < 4; ++j) bin[j] = j < cnt ? seg_bin(s[j], e[j], ri, lut) : -1;
         const unsigned act = __activemask();
-        unsigned rank[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int up = __shfl_up_sync(act, bin[j], 1);
-            rank[j] = 0;
             if (__any_sync(act, lane > 0 && bin[j] >= 0 && up == bin[j])) {
                 const unsigned peers = __match_any_sync(act, bin[j]);
-                const int leader = __ffs(peers) - 1;
-                unsigned r = 0;
-                if (bin[j] >= 0 && leader == lane) {
-                    if (RANK) r = atomicAdd(a.bins + bin[j], __popc(peers));
-                    else atomicAdd(a.bins + bin[j], __popc(peers));
-                }
-                if (RANK) rank[j] = __shfl_sync(peers, r, leader) + __popc(peers & ((1u << lane) - 1u));
+                if (bin[j] >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(a.bins + bin[j], __popc(peers));
             } else if (bin[j] >= 0) {
-                if (RANK) rank[j] = atomicAdd(a.bins + bin[j], 1u);
-                else atomicAdd(a.bins + bin[j], 1u);
+                atomicAdd(a.bins + bin[j], 1u);
             }
-        }
-        if (RANK) {
-            // the histogram pass already knows each segment's slot within its
-            // bin: the scatter then needs no atomics
-            if (cnt == 4) {
-                ulonglong2* k2 = reinterpret_cast<ulonglong2*>(a.seg_key + 4 * q);
-                auto key = [&](int j) {
-                    return bin[j] >= 0 ? ((unsigned long long)bin[j] << 32) | rank[j] : ~0ull;
-                };
-                k2[0] = make_ulonglong2(key(0), key(1));
-                k2[1] = make_ulonglong2(key(2), key(3));
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (j < cnt)
-                        a.seg_key[4 * q + j] = bin[j] >= 0 ? ((unsigned long long)bin[j] << 32) | rank[j] : ~0ull;
-            }
-        }
-    });
-}
-
-// Scatter from the histogram pass's (bin, rank): slot = cursor[bin] + rank.
-// No atomics and no key arithmetic: the segment rows, the keys and the
-// cursors are independent loads.
-__global__ void __launch_bounds__(256) k_bin_place(SortedArgs a) {
-    const long long nq = (a.n_r + 3) / 4;
-    for (long long q = blockIdx.x * 256ll + threadIdx.x; q < nq; q += gridDim.x * 256ll) {
-        float s[4][3], e[4][3];
-        const int cnt = load4<true>(a.starts, a.ends, q, a.n_r, s, e);
-        unsigned long long k[4];
-        if (cnt == 4) {
-            const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(a.seg_key + 4 * q);
-            const ulonglong2 x = __ldg(k2), y = __ldg(k2 + 1);
-            k[0] = x.x; k[1] = x.y; k[2] = y.x; k[3] = y.y;
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) k[j] = j < cnt ? __ldg(a.seg_key + 4 * q + j) : ~0ull;
-        }
-        unsigned pos[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            pos[j] = k[j] != ~0ull ? __ldg(a.cursor + (unsigned)(k[j] >> 32)) + (unsigned)k[j] : 0u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (k[j] != ~0ull) put_rec(a, pos[j], s[j], (int)(4 * q + j), e[j]);
-    }
-}
-
-__global__ void __launch_bounds__(kStreamThreads) k_bin_scatter_tma(SortedArgs a) {
-    RootInfo ri;
-    const BinLut* lut;
-    root_info(a, ri, lut);
-    const int lane = threadIdx.x & 31;
-    stream_segments(a, [&](float (&s)[4][3], float (&e)[4][3], int cnt, long long q) {
-        int bin[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bin[j] = j < cnt ? seg_bin(s[j], e[j], ri, lut) : -1;
-        const unsigned act = __activemask();
-        bool dup = false;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int up = __shfl_up_sync(act, bin[j], 1);
-            dup |= lane > 0 && bin[j] >= 0 && up == bin[j];
-        }
-        unsigned pos[4];
-        if (__any_sync(act, dup)) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const unsigned peers = __match_any_sync(act, bin[j]);
-                const int leader = __ffs(peers) - 1;
-                unsigned p = 0;
-                if (bin[j] >= 0 && leader == lane) p = atomicAdd(a.cursor + bin[j], __popc(peers));
-                pos[j] = __shfl_sync(peers, p, leader) + __popc(peers & ((1u << lane) - 1u));
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) pos[j] = bin[j] >= 0 ? atomicAdd(a.cursor + bin[j], 1u) : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (bin[j] < 0) continue;
-            put_rec(a, pos[j], s[j], (int)(4 * q + j), e[j]);
         }
     });
 }
@@ -1567,368 +1464,6 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
     }
 }
 
-// ---- warp tiles ----------------------------------------------------------
-//
-// Same idea as k_trav_tile with the work unit shrunk to one warp: each warp
-// takes a.warp_chunks x 32 consecutive records, walks the tree (from the
-// CTA's shared cut) with their union box into its own candidate list, and
-// runs process_chunk over its records.  Only warp-level synchronisation:
-// no CTA barrier, so a warp waiting on its walk's node loads never holds up
-// the others (the CTA-tile kernel spent a quarter of its stall samples in
-// __syncthreads).
-constexpr int kWtLCap = 128;
-constexpr int kWtFCap = 64;
-
-struct WarpTile {
-    float4 lxy[kWtLCap];
-    float2 lz[kWtLCap];
-    int lid[kWtLCap];
-    int front[2][kWtFCap];
-    WarpCand wc;
-    unsigned char slot[kWCap][32];
-};
-struct WTileSmem {
-    float4 cxy[kCutCap];
-    float2 cz[kCutCap];
-    int cref[kCutCap];
-    int ncut;
-    WarpTile w[kTileThreads / 32];
-};
-
-// (K: one instantiation per calling kernel; ptxas 12.9 crashes on a
-// __noinline__ function shared by several kernels)
-template <int MODE, int K>
-__device__ __noinline__ void wtile_fallback(const SortedArgs& a, const RsSlot* nodes, int root,
-                                            float4 r0, float4 r1, int& det, int& nh, int& btri,
-                                            double& bt) {
-    bool ovf = false;
-    trav_one<MODE>(nodes, a.leaves, a.n_int, root, r0, r1, det, nh, btri, bt, ovf);
-    if (ovf) atomicAdd(&a.status->internal, 1ull);
-}
-
-// One warp: union box of records [beg, end), then a breadth-first walk from
-// the CTA's cut (ballot-compacted levels, warp-level synchronisation only)
-// collecting every leaf that overlaps it into (lxy, lz, lid).  Returns the
-// leaf count; ovf is set when the list or a level exceeds its capacity.
-// One warp: the union box of records [beg, end).
-__device__ __forceinline__ void warp_union(const SortedArgs& a, unsigned beg, unsigned end, float u[6]) {
-    const int lane = threadIdx.x & 31;
-    u[0] = u[2] = u[4] = INFINITY;
-    u[1] = u[3] = u[5] = -INFINITY;
-    for (unsigned idx = beg + lane; idx < end; idx += 32) {
-        float4 r0, r1;
-        get_rec(a, idx, r0, r1);
-        u[0] = fminf(u[0], fminf(r0.x, r1.x)); u[1] = fmaxf(u[1], fmaxf(r0.x, r1.x));
-        u[2] = fminf(u[2], fminf(r0.y, r1.y)); u[3] = fmaxf(u[3], fmaxf(r0.y, r1.y));
-        u[4] = fminf(u[4], fminf(r0.z, r1.z)); u[5] = fmaxf(u[5], fmaxf(r0.z, r1.z));
-    }
-#pragma unroll
-    for (int k = 0; k < 6; k += 2) {
-        u[k] = wred_min(u[k]);
-        u[k + 1] = wred_max(u[k + 1]);
-    }
-}
-
-
-// One warp: the candidate list of union box u from its Morton key range
-// (see k_trav_tile); -1 when the range holds more than a.range_max leaves.
-__device__ __forceinline__ int warp_range(const SortedArgs& a, const float u[6], float4* lxy,
-                                          float2* lz, int* lid, int lcap, bool& ovf) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    double plo[3], phi[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const double sz = (double)__uint_as_float(__ldg(&a.hdr->tsize[k]));
-        const double l = (double)u[2 * k], h = (double)u[2 * k + 1];
-        plo[k] = l - sz - 1e-9 * (fabs(l) + sz + 1.0);
-        phi[k] = h + sz + 1e-9 * (fabs(h) + sz + 1.0);
-    }
-    const int i0 = warp_bound(a, range_key(a, plo), false);
-    const int i1 = warp_bound(a, range_key(a, phi), true);
-    if (i1 - i0 > (int)a.range_max) return -1;
-    int nl = 0;
-    for (int b = i0; b < i1; b += 32) {
-        const int i = b + lane;
-        bool hit = false;
-        float4 xy;
-        float2 z;
-        if (i < i1) {
-            const float2* lb = reinterpret_cast<const float2*>(a.leaf_boxes + 6ll * i);
-            const float2 x = __ldg(lb), y = __ldg(lb + 1);
-            z = __ldg(lb + 2);
-            xy = make_float4(x.x, x.y, y.x, y.y);
-            hit = box_ov(u, xy, z);
-        }
-        const unsigned m = __ballot_sync(kFullMask, hit);
-        if (hit) {
-            const int k = nl + __popc(m & lt);
-            if (k < lcap) {
-                lxy[k] = xy;
-                lz[k] = z;
-                lid[k] = i;
-            }
-        }
-        nl += __popc(m);
-    }
-    ovf = nl > lcap;
-    __syncwarp();
-    return nl;
-}
-
-template <class CUT>
-__device__ __forceinline__ int warp_walk_u(const SortedArgs& a, const CUT& cut, int ncut,
-                                           const RsSlot* nodes, const float u[6], float4* lxy,
-                                           float2* lz, int* lid, int lcap, int (*front)[kWtFCap],
-                                           int fcap, bool& ovf) {
-    const int n_int = a.n_int;
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    int nl = 0, nf = 0;
-    for (int i0 = 0; i0 < ncut; i0 += 32) {
-        const int i = i0 + lane;
-        const int ref = i < ncut ? cut.cref[i] : -1;
-        const bool hit = i < ncut && box_ov(u, cut.cxy[i], cut.cz[i]);
-        const bool leaf = ref >= n_int;
-        const unsigned ml = __ballot_sync(kFullMask, hit && leaf);
-        const unsigned mi = __ballot_sync(kFullMask, hit && !leaf);
-        if (hit && leaf) {
-            const int k = nl + __popc(ml & lt);
-            if (k < lcap) {
-                lxy[k] = cut.cxy[i];
-                lz[k] = cut.cz[i];
-                lid[k] = ref - n_int;
-            }
-        }
-        if (hit && !leaf) {
-            const int k = nf + __popc(mi & lt);
-            if (k < fcap) front[0][k] = ref;
-        }
-        nl += __popc(ml);
-        nf += __popc(mi);
-    }
-    ovf = nl > lcap || nf > fcap;
-    int cur = 0;
-    while (nf > 0 && !ovf) {
-        __syncwarp();
-        int nn = 0;
-        for (int i0 = 0; i0 < nf; i0 += 32) {
-            const int i = i0 + lane;
-            bool oa = false, ob = false;
-            int ca = -1, cb = -1;
-            float f0[8], f1[8];
-            if (i < nf) {
-                const int node = front[cur][i];
-                ld_slot(nodes + 2 * node, f0);
-                ld_slot(nodes + 2 * node + 1, f1);
-                ca = __float_as_int(f1[4]);
-                cb = __float_as_int(f1[5]);
-                oa = (u[0] <= f0[1]) & (u[1] >= f0[0]) & (u[2] <= f0[3]) & (u[3] >= f0[2]) &
-                     (u[4] <= f0[5]) & (u[5] >= f0[4]);
-                ob = (u[0] <= f0[7]) & (u[1] >= f0[6]) & (u[2] <= f1[1]) & (u[3] >= f1[0]) &
-                     (u[4] <= f1[3]) & (u[5] >= f1[2]);
-            }
-            const bool la = oa && ca >= n_int, ia = oa && ca < n_int;
-            const bool lb = ob && cb >= n_int, ib = ob && cb < n_int;
-            const unsigned mla = __ballot_sync(kFullMask, la), mlb = __ballot_sync(kFullMask, lb);
-            const unsigned mia = __ballot_sync(kFullMask, ia), mib = __ballot_sync(kFullMask, ib);
-            if (la) {
-                const int k = nl + __popc(mla & lt);
-                if (k < lcap) {
-                    lxy[k] = make_float4(f0[0], f0[1], f0[2], f0[3]);
-                    lz[k] = make_float2(f0[4], f0[5]);
-                    lid[k] = ca - n_int;
-                }
-            }
-            if (lb) {
-                const int k = nl + __popc(mla) + __popc(mlb & lt);
-                if (k < lcap) {
-                    lxy[k] = make_float4(f0[6], f0[7], f1[0], f1[1]);
-                    lz[k] = make_float2(f1[2], f1[3]);
-                    lid[k] = cb - n_int;
-                }
-            }
-            if (ia) {
-                const int k = nn + __popc(mia & lt);
-                if (k < fcap) front[cur ^ 1][k] = ca;
-            }
-            if (ib) {
-                const int k = nn + __popc(mia) + __popc(mib & lt);
-                if (k < fcap) front[cur ^ 1][k] = cb;
-            }
-            nl += __popc(mla) + __popc(mlb);
-            nn += __popc(mia) + __popc(mib);
-        }
-        nf = nn;
-        cur ^= 1;
-        ovf = nl > lcap || nf > fcap;
-    }
-    __syncwarp();
-    return nl;
-}
-
-template <class CUT>
-__device__ __forceinline__ int warp_walk(const SortedArgs& a, const CUT& cut, int ncut,
-                                         const RsSlot* nodes, unsigned beg, unsigned end,
-                                         float4* lxy, float2* lz, int* lid, int lcap,
-                                         int (*front)[kWtFCap], int fcap, bool& ovf) {
-    float u[6];
-    warp_union(a, beg, end, u);
-    return warp_walk_u(a, cut, ncut, nodes, u, lxy, lz, lid, lcap, front, fcap, ovf);
-}
-
-// ---- pipelined tiles -------------------------------------------------------
-//
-// The CTA-tile scheme with the walk taken off the critical path: warp 0
-// walks the tree for the NEXT tile (warp_walk into the other half of a
-// double-buffered candidate list) while every warp, warp 0 included once its
-// walk is done, claims 32-record chunks of the current tile.  One CTA barrier
-// per tile instead of one per walk level.
-constexpr int kPtLCap = 192;
-
-struct PTileSmem {
-    float4 cxy[kCutCap];
-    float2 cz[kCutCap];
-    int cref[kCutCap];
-    int ncut;
-    float4 lxy[2][kPtLCap];
-    float2 lz[2][kPtLCap];
-    int lid[2][kPtLCap];
-    int front[2][kWtFCap];
-    WarpCand wc[kTileThreads / 32];
-    unsigned char slot[kTileThreads / 32][kWCap][32];
-    int nl[2];
-    int ovf[2];
-    unsigned tile[2];
-    unsigned chunk[2];
-};
-
-template <int MODE>
-__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_ptile(SortedArgs a) {
-    __shared__ PTileSmem sm;
-    const unsigned n_live = *a.n_live;
-    const int n_int = a.n_int;
-    const int root = __ldg(&a.hdr->root);
-    const RsSlot* const nodes = reinterpret_cast<const RsSlot*>(a.nodes);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned T = (unsigned)((unsigned long long)a.tile_area * n_live / (unsigned)(n_int + 1));
-    const unsigned per = a.tile_balance * gridDim.x;
-    const unsigned bal = (n_live + per - 1) / per;
-    T = T < bal ? T : bal;
-    T = (T + 31) / 32 * 32;
-    T = T < 64 ? 64 : (T > 16384 ? 16384 : T);
-    const unsigned n_tiles = (n_live + T - 1) / T;
-    unsigned* ctr = reinterpret_cast<unsigned*>(&a.status->tile_counter);
-    build_cut(sm, nodes, n_int, root);
-    __syncthreads();
-    const int ncut = sm.ncut;
-    auto produce = [&](int buf) {  // warp 0
-        unsigned tl = 0;
-        if (lane == 0) tl = atomicAdd(ctr, 1u);
-        tl = __shfl_sync(kFullMask, tl, 0);
-        int nl = 0;
-        bool ovf = false;
-        if (tl < n_tiles) {
-            const unsigned beg = tl * T, end = beg + T < n_live ? beg + T : n_live;
-            nl = warp_walk(a, sm, ncut, nodes, beg, end, sm.lxy[buf], sm.lz[buf], sm.lid[buf],
-                           kPtLCap, sm.front, kWtFCap, ovf);
-        }
-        if (lane == 0) {
-            sm.tile[buf] = tl;
-            sm.chunk[buf] = 0;
-            sm.nl[buf] = nl;
-            sm.ovf[buf] = ovf;
-        }
-    };
-    if (warp == 0) produce(0);
-    __syncthreads();
-    for (int k = 0;; ++k) {
-        const int cur = k & 1;
-        const unsigned tile = sm.tile[cur];
-        if (tile >= n_tiles) break;
-        const bool fallback = sm.ovf[cur] != 0;
-        const int nl = sm.nl[cur];
-        if (warp == 0) produce(cur ^ 1);
-        const unsigned beg = tile * T, end = beg + T < n_live ? beg + T : n_live;
-        const unsigned nchunks = (end - beg + 31) / 32;
-        for (;;) {
-            unsigned c = 0;
-            if (lane == 0) c = atomicAdd(&sm.chunk[cur], 1u);
-            c = __shfl_sync(kFullMask, c, 0);
-            if (c >= nchunks) break;
-            const unsigned idx = beg + 32 * c + lane;
-            const bool valid = idx < end;
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-            if (valid) get_rec(a, idx, r0, r1);
-            int det = 0, nh = 0, btri = -1;
-            double bt = 0.0;
-            if (fallback) {
-                if (valid) wtile_fallback<MODE, 1>(a, nodes, root, r0, r1, det, nh, btri, bt);
-            } else {
-                process_chunk<MODE>(a, r0, r1, valid, sm.lxy[cur], sm.lz[cur], sm.lid[cur], nl,
-                                    sm.wc[warp], sm.slot[warp], det, nh, btri, bt);
-            }
-            if (valid) write_result<MODE>(a, __float_as_int(r0.w), det, nh, btri, bt);
-        }
-        __syncthreads();  // tile done, next tile's list ready
-    }
-}
-
-
-template <int MODE>
-__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_wtile(SortedArgs a) {
-    __shared__ WTileSmem sm;
-    const unsigned n_live = *a.n_live;
-    const int n_int = a.n_int;
-    const int root = __ldg(&a.hdr->root);
-    const RsSlot* const nodes = reinterpret_cast<const RsSlot*>(a.nodes);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    build_cut(sm, nodes, n_int, root);
-    __syncthreads();
-    const int ncut = sm.ncut;
-    WarpTile& wt = sm.w[warp];
-    const unsigned U = 32u * a.warp_chunks;
-    const unsigned n_units = (n_live + U - 1) / U;
-    unsigned* ctr = reinterpret_cast<unsigned*>(&a.status->tile_counter);
-    for (;;) {
-        unsigned unit = 0;
-        if (lane == 0) unit = atomicAdd(ctr, 1u);
-        unit = __shfl_sync(kFullMask, unit, 0);
-        if (unit >= n_units) break;
-        const unsigned beg = unit * U;
-        const unsigned end = beg + U < n_live ? beg + U : n_live;
-        bool ovf = false;
-        float u[6];
-        warp_union(a, beg, end, u);
-        int nl = a.codes ? warp_range(a, u, wt.lxy, wt.lz, wt.lid, kWtLCap, ovf) : -1;
-        if (nl < 0)
-            nl = warp_walk_u(a, sm, ncut, nodes, u, wt.lxy, wt.lz, wt.lid, kWtLCap, wt.front, kWtFCap, ovf);
-        __syncwarp();
-#ifdef RS_TILE_STATS
-        if (lane == 0) {
-            atomicAdd(&a.status->visits, (unsigned long long)nl);
-            if (ovf) atomicAdd(&a.status->cand_count, 1ull);
-        }
-#endif
-        for (unsigned base = beg; base < end; base += 32) {
-            const unsigned idx = base + lane;
-            const bool valid = idx < end;
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-            if (valid) get_rec(a, idx, r0, r1);
-            int det = 0, nh = 0, btri = -1;
-            double bt = 0.0;
-            if (ovf) {
-                if (valid) wtile_fallback<MODE, 0>(a, nodes, root, r0, r1, det, nh, btri, bt);
-            } else {
-                process_chunk<MODE>(a, r0, r1, valid, wt.lxy, wt.lz, wt.lid, nl, wt.wc, wt.slot, det,
-                                    nh, btri, bt);
-            }
-            if (valid) write_result<MODE>(a, __float_as_int(r0.w), det, nh, btri, bt);
-        }
-        __syncwarp();
-    }
-}
-
 // ------------------------------------------------------------ host glue ---
 
 size_t sorted_bins() { return kBins; }
@@ -1955,12 +1490,8 @@ struct SortedOpts {
     unsigned bin_occ = 16;       // target live segments per spatial bin
     int bin_tma = 1;             // binning passes stream through TMA bulk copies
     int tile_wide = 0;           // tile walk over the collapsed 4-wide nodes (A/B: no gain on C2)
-    int bin_rank = 0;            // histogram pass records slots; scatter without atomics (A/B: slower)
-    int rec_ids = 0;             // scatter writes segment ids, not 32-B records (A/B: traversal gathers thrash L1)
-    int auto_tile = 3;           // auto's dense variant: 3 CTA tiles, 4 warp tiles
     int fast_keys = 0;           // fast-tree key grid: 0 isotropic, 1 per-axis, 2 auto
     unsigned range_max = 4096;   // tile lists from a Morton key range of at most this many leaves (0: walk only)
-    unsigned warp_chunks = 4;    // warp tiles: records per warp unit / 32
     int geom = 0;                // 1: bin geometry derived once by k_seg_sample (A/B: C3/C5 -1..2%, C2 +3%)
     int fast_path = 0;           // 0 binned tiles, 1 collision buffer (rs_trav.cu)
     long long cand_cap = 0;      // collision buffer: initial capacity (0: 2 x segments + 4096)
@@ -1983,12 +1514,8 @@ static SortedOpts& opts() {
         d.bin_occ = (unsigned)num("RS_BIN_OCC", d.bin_occ);
         d.bin_tma = (int)num("RS_BIN_TMA", d.bin_tma);
         d.tile_wide = (int)num("RS_TILE_WIDE", d.tile_wide);
-        d.auto_tile = (int)num("RS_AUTO_TILE", d.auto_tile);
         d.fast_keys = (int)num("RS_FAST_KEYS", d.fast_keys);
         d.range_max = (unsigned)num("RS_RANGE_MAX", d.range_max);
-        d.bin_rank = (int)num("RS_BIN_RANK", d.bin_rank);
-        d.rec_ids = (int)num("RS_REC_IDS", d.rec_ids);
-        d.warp_chunks = (unsigned)num("RS_WARP_CHUNKS", d.warp_chunks);
         d.geom = (int)num("RS_GEOM", d.geom);
         const char* fp = getenv("RS_FAST_PATH");
         if (fp && fp[0] == 'b') d.fast_path = 1;
@@ -2009,12 +1536,8 @@ int sorted_option(const char* name, long long value, long long* old) {
     else if (!strcmp(name, "bin_occupancy")) { prev = o.bin_occ; if (value > 0) o.bin_occ = (unsigned)value; }
     else if (!strcmp(name, "bin_tma")) { prev = o.bin_tma; if (value >= 0) o.bin_tma = (int)value; }
     else if (!strcmp(name, "tile_wide")) { prev = o.tile_wide; if (value >= 0) o.tile_wide = (int)value; }
-    else if (!strcmp(name, "rec_ids")) { prev = o.rec_ids; if (value >= 0) o.rec_ids = (int)value; }
-    else if (!strcmp(name, "bin_rank")) { prev = o.bin_rank; if (value >= 0) o.bin_rank = (int)value; }
     else if (!strcmp(name, "range_max")) { prev = o.range_max; if (value >= 0) o.range_max = (unsigned)value; }
     else if (!strcmp(name, "fast_keys")) { prev = o.fast_keys; if (value >= 0 && value <= 2) o.fast_keys = (int)value; }
-    else if (!strcmp(name, "auto_tile")) { prev = o.auto_tile; if (value >= 3 && value <= 5) o.auto_tile = (int)value; }
-    else if (!strcmp(name, "warp_chunks")) { prev = o.warp_chunks; if (value > 0) o.warp_chunks = (unsigned)value; }
     else if (!strcmp(name, "geom")) { prev = o.geom; if (value >= 0) o.geom = value ? 1 : 0; }
     else if (!strcmp(name, "fast_path")) { prev = o.fast_path; if (value >= 0 && value <= 1) o.fast_path = (int)value; }
     else if (!strcmp(name, "cand_cap")) { prev = o.cand_cap; if (value >= 0) o.cand_cap = value; }
@@ -2026,7 +1549,6 @@ int sorted_option(const char* name, long long value, long long* old) {
 static int trav_variant() { return opts().trav; }
 int fast_key_mode() { return opts().fast_keys; }
 int fast_path() { return opts().fast_path; }
-bool bin_rank_on() { return opts().bin_rank != 0; }
 long long cand_cap_override() { return opts().cand_cap; }
 static unsigned tile_min_density() { return opts().tile_density; }
 static unsigned tile_balance() { return opts().tile_balance; }
@@ -2036,7 +1558,7 @@ static unsigned tile_area() { return opts().tile_area; }
 bool binning_zeroes_flags(const float* starts, const float* ends, long long n_r, const int* flags) {
     const uintptr_t al = reinterpret_cast<uintptr_t>(starts) | reinterpret_cast<uintptr_t>(ends) |
                          reinterpret_cast<uintptr_t>(flags);
-    return flags && (al & 15) == 0 && opts().bin_tma && !opts().bin_rank && n_r >= kStreamSegs;
+    return flags && (al & 15) == 0 && opts().bin_tma && n_r >= kStreamSegs;
 }
 
 __global__ void __launch_bounds__(256) k_expand_bits(int* __restrict__ flags, const unsigned* __restrict__ bits,
@@ -2073,36 +1595,25 @@ void launch_binning(const SortedArgs& a0, cudaStream_t s, bool zero_flags) {
     a.zero_flags = zero_flags && !a.hitbits && binning_zeroes_flags(a.starts, a.ends, a.n_r, a.flags);
     a.geom_mode = opts().geom;
     a.bin_occupancy = bin_occupancy();
-    a.rec_ids = opts().rec_ids;
     if (a.n_r <= 0) return;
     count_launches(4);
     const int sms = sm_total();
     k_seg_sample<<<kSampleCtas, kSampleThreads, 0, s>>>(a);
     const bool vec = ((reinterpret_cast<uintptr_t>(a.starts) | reinterpret_cast<uintptr_t>(a.ends)) & 15) == 0;
     if (vec && opts().bin_tma && a.n_r >= kStreamSegs) {
-        ensure_dynamic_smem((const void*)k_bin_count_tma<false>, (int)kStreamSmem);
-        ensure_dynamic_smem((const void*)k_bin_count_tma<true>, (int)kStreamSmem);
-        ensure_dynamic_smem((const void*)k_bin_scatter_tma, (int)kStreamSmem);
+        // histogram over TMA-streamed segments; the scatter with plain
+        // loads and twice the warps (its cursor claims need the parallelism)
+        ensure_dynamic_smem((const void*)k_bin_count_tma, (int)kStreamSmem);
         const long long chunks = a.n_r / kStreamSegs;
         const unsigned g = (unsigned)(chunks < sms * (long long)RS_STREAM_CTAS ? chunks : sms * (long long)RS_STREAM_CTAS);
-        const bool rank = opts().bin_rank;
         stage_mark(5, s);
-        if (rank) k_bin_count_tma<true><<<g, kStreamThreads, kStreamSmem, s>>>(a);
-        else k_bin_count_tma<false><<<g, kStreamThreads, kStreamSmem, s>>>(a);
+        k_bin_count_tma<<<g, kStreamThreads, kStreamSmem, s>>>(a);
         stage_mark(6, s);
         k_bin_scan1<<<kScanTiles, 256, 0, s>>>(a);
         stage_mark(7, s);
-        if (rank) {
-            const long long want = (a.n_r + 1023) / 1024;
-            const unsigned g2 = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
-            k_bin_place<<<g2, 256, 0, s>>>(a);
-        } else if (opts().bin_tma & 2) {
-            k_bin_scatter_tma<<<g, kStreamThreads, kStreamSmem, s>>>(a);
-        } else {
-            const long long want = (a.n_r + 1023) / 1024;
-            const unsigned g2 = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
-            k_bin_scatter<true><<<g2, 256, 0, s>>>(a);
-        }
+        const long long want = (a.n_r + 1023) / 1024;
+        const unsigned g2 = (unsigned)(want < sms * 16ll ? want : sms * 16ll);
+        k_bin_scatter<true><<<g2, 256, 0, s>>>(a);
         stage_mark(8, s);
         return;
     }
@@ -2128,18 +1639,6 @@ static void launch_tile(const SortedArgs& a, int sms, cudaStream_t s) {
     else k_trav_tile<MODE, false><<<sms * o, kTileThreads, 0, s>>>(a);
 }
 
-template <int MODE>
-static void launch_ptile(const SortedArgs& a, int sms, cudaStream_t s) {
-    const int occ = occupancy((const void*)k_trav_ptile<MODE>, kTileThreads);
-    k_trav_ptile<MODE><<<sms * occ, kTileThreads, 0, s>>>(a);
-}
-
-template <int MODE>
-static void launch_wtile(const SortedArgs& a, int sms, cudaStream_t s) {
-    const int occ = occupancy((const void*)k_trav_wtile<MODE>, kTileThreads);
-    k_trav_wtile<MODE><<<sms * occ, kTileThreads, 0, s>>>(a);
-}
-
 static const char* g_hot_name = "";
 const char* hot_kernel_name() { return g_hot_name; }
 
@@ -2151,12 +1650,10 @@ void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t
     SortedArgs a = a0;
     a.tile_area = tile_area();
     a.tile_depth = opts().tile_depth;
-    a.rec_ids = opts().rec_ids;
     a.range_max = opts().range_max;
     if (!a.range_max) a.codes = nullptr;
     a.tile_min_density = tile_min_density();
     a.tile_balance = tile_balance();
-    a.warp_chunks = opts().warp_chunks;
     count_launches(1);
     const int sms = sm_total();
     int variant = trav_variant();
@@ -2167,25 +1664,10 @@ void launch_sorted_trav(const SortedArgs& a0, int mode, bool stats, cudaStream_t
     // in pieces)
     const long long n_density = a.n_r > g_batch_rays ? a.n_r : g_batch_rays;
     if (variant == 0)
-        variant = n_density < (long long)a.tile_min_density * (a.n_int + 1) ? 1 : opts().auto_tile;
+        variant = n_density < (long long)a.tile_min_density * (a.n_int + 1) ? 1 : 3;
     if (a.n_int == 0) variant = 1;
     hot_kernel_mark(0, s);
-    g_hot_name = variant == 5 ? "k_trav_ptile" : variant == 4 ? "k_trav_wtile" : variant == 3 ? "k_trav_tile"
-                 : variant == 1 ? "k_trav_sorted_bin" : "k_trav_sorted";
-    if (variant == 5 && !stats) {
-        if (mode == kBoolean) launch_ptile<kBoolean>(a, sms, s);
-        else if (mode == kCount) launch_ptile<kCount>(a, sms, s);
-        else launch_ptile<kBarycentric>(a, sms, s);
-        hot_kernel_mark(1, s);
-        return;
-    }
-    if (variant == 4 && !stats) {
-        if (mode == kBoolean) launch_wtile<kBoolean>(a, sms, s);
-        else if (mode == kCount) launch_wtile<kCount>(a, sms, s);
-        else launch_wtile<kBarycentric>(a, sms, s);
-        hot_kernel_mark(1, s);
-        return;
-    }
+    g_hot_name = variant == 3 ? "k_trav_tile" : variant == 1 ? "k_trav_sorted_bin" : "k_trav_sorted";
     if (variant == 3 && !stats) {
         if (mode == kBoolean) launch_tile<kBoolean>(a, sms, s);
         else if (mode == kCount) launch_tile<kCount>(a, sms, s);

@@ -177,7 +177,7 @@ def test_layered(cap, mode):
 # shared candidate lists, the per-thread binary and 4-wide walks.  Results
 # must not depend on the variant, the tile size, the spatial-bin resolution
 # or the tile fallback (candidate-list overflow -> per-record walk).
-TRAV = {"tile": 3, "warptile": 4, "ptile": 5, "binary": 1, "wide": 2}
+TRAV = {"tile": 3, "binary": 1, "wide": 2}
 
 
 @pytest.mark.parametrize("device", [False, True], ids=["host", "device"])
@@ -201,20 +201,13 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"bin_occupancy": 1},                           # finest bins
     {"bin_occupancy": 1 << 20},                     # 256 bins
     {"bin_tma": 0},                                 # binning with plain loads
-    {"bin_tma": 3},                                 # both binning passes over TMA
-    {"bin_rank": 1},                                # slots from the histogram pass
-    {"rec_ids": 0},                                 # 32-B records instead of ids
     {"tile_wide": 1},                               # tile walk over 4-wide nodes
-    {"trav": 4, "warp_chunks": 1},                  # warp tiles of one chunk
-    {"trav": 4, "warp_chunks": 64},                 # warp tiles overflowing their lists
-    {"trav": 5, "tile_balance": 1, "tile_area": 1 << 20},  # pipelined tiles, overflowing
-    {"trav": 5, "tile_balance": 64},                # pipelined tiles, small
     {"range_max": 0},                               # candidate lists from the walk only
     {"range_max": 1 << 30},                         # candidate lists from key ranges only
     {"geom": 1},                                    # bin geometry derived once by the sample kernel
     {"tile_depth": 1, "tile_balance": 1},           # depth-complexity cap: one-CTA-size tiles
     {"tile_depth": 0, "tile_balance": 1},           # no depth cap
-], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "tma2", "rank", "records", "widewalk", "wt1", "wt64", "pthuge", "ptsmall", "walkonly", "rangeonly", "geom", "depth1", "depth0"])
+], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "widewalk", "walkonly", "rangeonly", "geom", "depth1", "depth0"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ("c1", "soup:17", "layered"))
 def test_tile_knobs_bitwise(name, mode, knobs):
@@ -294,7 +287,7 @@ def test_tile_random_soup_vs_oracle(seed, n_tri, n_seg, mode):
     V, T, s, _ = _random_soup(seed, n_tri, n_seg)
     e = s + np.random.default_rng(seed + 100).uniform(-1.5, 1.5, size=s.shape).astype(np.float32)
     want = O.run_batch(V, T, s, e, mode=mode, max_stack=10**6)
-    for variant in ("tile", "warptile", "ptile", "binary"):
+    for variant in ("tile", "binary"):
         with _lib.option("trav", TRAV[variant]):
             got = rs.run_batch(rs.Mesh.from_arrays(V, T), rs.SegmentBatch.from_arrays(s, e),
                                rs.EngineConfig(mode=mode, tree="fast"))
@@ -656,7 +649,7 @@ def _adversarial(kind: str, seed: int):
     return V, T, s.astype(np.float32), e.astype(np.float32)
 
 
-@pytest.mark.parametrize("variant", ["auto", "tile", "warptile", "ptile", "binary", "reference"])
+@pytest.mark.parametrize("variant", ["auto", "tile", "binary", "reference"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("kind", ["lattice", "inplane", "degenerate", "scale"])
 def test_adversarial_vs_oracle(kind, mode, variant):
