@@ -154,6 +154,16 @@ RS_API int rs_baseline_compact(const float *d_verts, int64_t n_v, const int32_t 
                                int32_t *d_ray_index, float *d_distance, int32_t *d_triangle_id,
                                float *d_point, int64_t *n_hits, void *stream);
 
+/* oracle_intersect (oracle.py:30-158): the reference's independent
+ * verification oracle on device -- all pairs, plane intersection + three
+ * edge sign tests in f64 (no Moller-Trumbore, no box prescreen).  boolean /
+ * count -> d_flags (n_r rows); barycentric -> compacted rows, *n_hits.
+ * Synchronises. */
+RS_API int rs_oracle_intersect(const float *d_verts, int64_t n_v, const int32_t *d_tris, int64_t n_t,
+                               const float *d_starts, const float *d_ends, int64_t n_r, int mode,
+                               int32_t *d_flags, int32_t *d_ray_index, float *d_distance,
+                               int32_t *d_triangle_id, float *d_point, int64_t *n_hits, void *stream);
+
 /* compute_segment_boxes (engine.py:115-122): d_boxes (n,6) f32
  * [xmin,xmax,ymin,ymax,zmin,zmax] per segment.  Stream-ordered. */
 RS_API int rs_segment_boxes(const float *d_starts, const float *d_ends, int64_t n, float *d_boxes,

@@ -53,6 +53,7 @@ _SIGS = {
     "rs_baseline_compact": (i32, [p, i64, p, i64, p, p, i64, p, p, p, p, p, p]),
     "rs_unpermute_dense": (i32, [p, i64, p, p, p]),
     "rs_segment_boxes": (i32, [p, p, i64, p, p]),
+    "rs_oracle_intersect": (i32, [p, i64, p, i64, p, p, i64, i32, p, p, p, p, p, p, p]),
     "rs_unpermute_rows": (i32, [p, i64, p, p, p, p, i64, p, p, p, p, p]),
     "rs_generate_segments": (i32, [p, p, i64, C.c_double, C.c_double, C.c_double, C.c_double,
                                    C.c_double, C.c_uint64, i64, i64, p, p, p, p]),

@@ -1136,6 +1136,54 @@ int rs_baseline_compact(const float* d_verts, int64_t n_v, const int32_t* d_tris
     return RS_OK;
 }
 
+int rs_oracle_intersect(const float* d_verts, int64_t n_v, const int32_t* d_tris, int64_t n_t,
+                        const float* d_starts, const float* d_ends, int64_t n_r, int mode,
+                        int32_t* d_flags, int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
+                        int64_t* n_hits, void* stream) {
+    marks_reset();
+    if (n_hits) *n_hits = 0;
+    if (mode < 0 || mode > 2) return fail(RS_INVALID_ARG, "unknown mode %d", mode);
+    if (n_t < 0 || n_r < 0 || n_t > 2147483647ll || n_r > 2147483647ll) return fail(RS_INVALID_ARG, "bad sizes");
+    (void)n_v;
+    cudaStream_t s = S(stream);
+    if (mode != kBarycentric) {
+        if (n_r && !d_flags) return fail(RS_INVALID_ARG, "null output");
+        if (n_r) CK(cudaMemsetAsync(d_flags, 0, 4ull * n_r, s));
+        BaselineArgs a{d_verts, d_tris, (int)n_t, d_starts, d_ends, n_r, d_flags, d_flags,
+                       nullptr, nullptr, nullptr, nullptr, nullptr};
+        if (n_t > 0) launch_sign_oracle(a, mode, s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+        return RS_OK;
+    }
+    if (!(d_ray && d_dist && d_tri && d_pt) && n_r > 0) return fail(RS_INVALID_ARG, "null output");
+    if (n_r == 0 || n_t == 0) return RS_OK;
+    const size_t cs = bary_compact_scratch(n_r);
+    char* blk = nullptr;
+    const size_t total = align256(sizeof(RsStatus)) + align256(8ull * n_r) + align256(4ull * n_r) + align256(cs);
+    CK(dmalloc(reinterpret_cast<void**>(&blk), total, s));
+    Carver c{blk};
+    RsStatus* st = c.take<RsStatus>(1);
+    unsigned long long* best_t = c.take<unsigned long long>(n_r);
+    int* best_tri = c.take<int>(n_r);
+    unsigned long long* tiles = c.take<unsigned long long>(cs / 8);
+    CK(cudaMemsetAsync(st, 0, sizeof(RsStatus), s));
+    CK(cudaMemsetAsync(tiles, 0, cs, s));
+    BaselineArgs a{d_verts, d_tris, (int)n_t, d_starts, d_ends, n_r, nullptr, nullptr,
+                   nullptr, nullptr, nullptr, best_t, best_tri};
+    launch_sign_oracle(a, kBarycentric, s);
+    CompactArgs ca{n_r, best_t, best_tri, d_starts, d_ends, d_ray, d_dist, d_tri, d_pt,
+                   tiles, tiles + (cs / 8 - 1), &st->hits, 0, nullptr};
+    launch_bary_compact(ca, s);
+    CK(cudaGetLastError());
+    RsStatus h;
+    int rc = read_status(st, s, &h);
+    CK(dfree(blk, s));
+    if (rc) return rc;
+    if (n_hits) *n_hits = (int64_t)h.hits;
+    return RS_OK;
+}
+
 int rs_segment_boxes(const float* d_starts, const float* d_ends, int64_t n, float* d_boxes,
                      void* stream) {
     if (n < 0) return fail(RS_INVALID_ARG, "negative count");

@@ -268,5 +268,7 @@ struct BaselineArgs {
     int* best_tri;
 };
 void launch_baseline(const BaselineArgs& a, int mode, cudaStream_t s);
+// oracle_intersect's plane + sign-test all-pairs (barycentric: best_t/best_tri)
+void launch_sign_oracle(const BaselineArgs& a, int mode, cudaStream_t s);
 
 }  // namespace rs

@@ -649,6 +649,96 @@ __global__ void __launch_bounds__(kBaseThreads) k_baseline(BaselineArgs a) {
     }
 }
 
+// oracle_intersect (oracle.py:30-158): the reference's independent
+// verification oracle -- every (segment, triangle) pair, no box prescreen,
+// plane intersection then three edge sign tests, f64 -- a formulation
+// algebraically independent of Moller-Trumbore (SPEC.md "oracle uses a
+// formulation algebraically independent of Moller-Trumbore").  Its results
+// agree with the engine's except for grazing pairs; the reference compares
+// them at 1e-4 on the floats.
+__device__ __forceinline__ double dot3(double ax, double ay, double az, double bx, double by, double bz) {
+    return ax * bx + ay * by + az * bz;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBaseThreads) k_sign_oracle(BaselineArgs a) {
+    __shared__ float sv[kBaseTile][9];
+    const long long i = (long long)blockIdx.x * kBaseThreads + threadIdx.x;
+    Ray r;
+    const bool live = i < a.n_r;
+    if (live) load_ray(a.starts, a.ends, i, r);
+    Hit h{0, 0, -1, 0.0};
+    bool done = !live;
+    for (int j0 = 0; j0 < a.n_t; j0 += kBaseTile) {
+        if (__syncthreads_and(done)) break;
+        for (int k = threadIdx.x; k < kBaseTile; k += kBaseThreads) {
+            const int j = j0 + k;
+            if (j < a.n_t) {
+                const int ia = a.T[3ll * j], ib = a.T[3ll * j + 1], ic = a.T[3ll * j + 2];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    sv[k][c] = a.V[3ll * ia + c];
+                    sv[k][3 + c] = a.V[3ll * ib + c];
+                    sv[k][6 + c] = a.V[3ll * ic + c];
+                }
+            }
+        }
+        __syncthreads();
+        const int jn = a.n_t - j0 < kBaseTile ? a.n_t - j0 : kBaseTile;
+        for (int k = 0; k < jn && !done; ++k) {
+            const float* v = sv[k];
+            const double ax = v[0], ay = v[1], az = v[2], bx = v[3], by = v[4], bz = v[5];
+            const double cx = v[6], cy = v[7], cz = v[8];
+            const double e1x = bx - ax, e1y = by - ay, e1z = bz - az;
+            const double e2x = cx - ax, e2y = cy - ay, e2z = cz - az;
+            const double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
+            const double denom = dot3(r.dx, r.dy, r.dz, nx, ny, nz);
+            if (fabs(denom) < kDetEps) continue;
+            const double t = (dot3(nx, ny, nz, ax, ay, az) - dot3(r.sx, r.sy, r.sz, nx, ny, nz)) / denom;
+            if (!(t >= 0.0 && t <= 1.0)) continue;
+            const double px = r.sx + t * r.dx, py = r.sy + t * r.dy, pz = r.sz + t * r.dz;
+            bool in = true;
+            // edges (b - a, a), (c - b, b), (a - c, c): n . (e x (p - v)) >= 0
+            const double ex[3] = {e1x, cx - bx, ax - cx}, ey[3] = {e1y, cy - by, ay - cy},
+                         ez[3] = {e1z, cz - bz, az - cz};
+            const double vx[3] = {ax, bx, cx}, vy[3] = {ay, by, cy}, vz[3] = {az, bz, cz};
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double rx = px - vx[q], ry = py - vy[q], rz = pz - vz[q];
+                const double qx = ey[q] * rz - ez[q] * ry, qy = ez[q] * rx - ex[q] * rz, qz = ex[q] * ry - ey[q] * rx;
+                in = in && (qx * nx + qy * ny + qz * nz >= 0.0);
+            }
+            if (!in) continue;
+            h.det = 1;
+            h.n_hits += 1;
+            if (MODE == kBoolean) { done = true; break; }
+            if (h.best_tri < 0 || t < h.best_t) {  // ascending j: argmin keeps the lowest id
+                h.best_t = t;
+                h.best_tri = j0 + k;
+            }
+        }
+        __syncthreads();
+    }
+    if (!live) return;
+    if (MODE == kBoolean) {
+        a.detected[i] = h.det;
+    } else if (MODE == kCount) {
+        a.counts[i] = h.n_hits;
+    } else {
+        a.best_tri[i] = h.best_tri;
+        a.best_t[i] = h.best_tri >= 0 && h.best_t != 0.0 ? (unsigned long long)__double_as_longlong(h.best_t) : 0ull;
+    }
+}
+
+void launch_sign_oracle(const BaselineArgs& a, int mode, cudaStream_t s) {
+    if (a.n_r <= 0) return;
+    count_launches(1);
+    const unsigned grid = (unsigned)((a.n_r + kBaseThreads - 1) / kBaseThreads);
+    if (mode == kBoolean) k_sign_oracle<kBoolean><<<grid, kBaseThreads, 0, s>>>(a);
+    else if (mode == kCount) k_sign_oracle<kCount><<<grid, kBaseThreads, 0, s>>>(a);
+    else k_sign_oracle<kBarycentric><<<grid, kBaseThreads, 0, s>>>(a);
+}
+
 void launch_baseline(const BaselineArgs& a, int mode, cudaStream_t s) {
     if (a.n_r <= 0) return;
     count_launches(1);

@@ -797,3 +797,44 @@ def test_baseline_barycentric_compaction(name, sort_rays):
         mesh, batch = mesh_batch(fx, device)
         got = rs.run_baseline_allpairs(mesh, batch, rs.EngineConfig(mode="barycentric", sort_rays=sort_rays))
         assert_result_fields(result_dict(got), want, f"{name} baseline bary sort={sort_rays}")
+
+
+@pytest.mark.parametrize("n", TREE_SIZES)
+def test_build_bvh_public_api(n):
+    """raysurf.build_bvh(mesh, sorted_codes, sorted_ids) (lbvh.py:148) on device."""
+    fx = load(f"tree_{n}")
+    tree = rs.build_bvh(rs.Mesh.from_arrays(fx["vertices"], fx["triangles"]), fx["sorted_codes"],
+                        fx["sorted_ids"])
+    for f in TREE_FIELDS:
+        assert np.array_equal(getattr(tree, f), fx[f"tree_{f}"]), f
+
+
+def _reference_oracle():
+    import sys
+
+    src = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "refpkg" / "src"
+    if not (src / "raysurf").is_dir():
+        pytest.skip("oracle/_ref/refpkg missing (make -f oracle/Makefile)")
+    if str(src) not in sys.path:
+        sys.path.insert(0, str(src))
+    import raysurf
+
+    return raysurf
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ("c1", "s19", "s77", "soup:17", "soup:20"))
+def test_oracle_intersect_matches_reference_oracle(name, mode):
+    """oracle_intersect (sign tests on device) vs the reference's own numpy
+    oracle_intersect (oracle.py:88-158): discrete fields exact, floats at the
+    reference's 1e-4 (its own comparison tolerance, test_acceptance.py:52-85)."""
+    raysurf = _reference_oracle()
+    fx = load(f"soup_{name[5:]}" if name.startswith("soup:") else f"scene_{name}")
+    want = raysurf.oracle_intersect(raysurf.Mesh.from_arrays(fx["vertices"], fx["triangles"]),
+                                    raysurf.SegmentBatch.from_arrays(fx["starts"], fx["ends"]), mode)
+    wd = {f: np.asarray(getattr(want, f)) for f in ("crossing", "counts", "ray_index", "distance",
+                                                   "triangle_id", "point") if getattr(want, f) is not None}
+    for device in (False, True):
+        mesh, batch = mesh_batch(fx, device)
+        got = rs.oracle_intersect(mesh, batch, mode)
+        assert_result_fields(result_dict(got), wd, f"{name} {mode} oracle", float_tol=1e-4)
