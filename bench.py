@@ -110,7 +110,8 @@ def peaks():
             "fp64_tops": sms * 64 * mhz * 1e6 / 1e12, "kind": kind, "sms": sms, "mhz": mhz}
 
 
-def roofline(cfg: Cfg, rays_per_s_kernel: float, rays_per_s_step: float, kernel: str):
+def roofline(cfg: Cfg, rays_per_s_kernel: float, rays_per_s_step: float, kernel: str,
+             own: dict | None = None):
     """ceiling = min(HBM/B_ray, FP32/W32, FP64/W64); the
     binding resource is the label, `achieved`/`peak` are in its unit for the
     dominant kernel, and every resource's fraction is listed."""
@@ -147,7 +148,26 @@ def roofline(cfg: Cfg, rays_per_s_kernel: float, rays_per_s_step: float, kernel:
                   "source": "SURVEY.md 8(d), reference-tree visit/test counts"},
         "peaks": pk["kind"] + "; FP32/FP64 = SMs x lanes x max SM clock",
         "traffic_source": tinfo.get("source") if tinfo else None,
+        "own_tree": own_tree_roofline(cfg, pk, own["fast"], rays_per_s_kernel) if own else None,
+        "reference_tree_units": own_tree_roofline(cfg, pk, own["reference"], rays_per_s_kernel)
+        if own else None,
     }
+
+
+def own_tree_roofline(cfg: Cfg, pk: dict, own: dict, rays_per_s_kernel: float) -> dict:
+    """The same ceiling with this engine's own tree's work units (SURVEY
+    8(d): "also report own-tree V_int/N_mt"): internal-node visits and exact
+    tests per segment of the fast tree's per-segment walk (rs_query_stats on
+    a sample), W32 = 12 V_int, W64 = 55 N_mt.  (The tile kernel does not walk
+    per segment; these are the per-segment-walk units of the same tree.)"""
+    v, m = own["internal_visits"] / own["n"], own["exact_tests"] / own["n"]
+    w32, w64 = 12.0 * v, 55.0 * m
+    ceil = {"hbm": pk["hbm_gbs"] * 1e9 / cfg.b_ray, "fp32": pk["fp32_tops"] * 1e12 / max(w32, 1e-9),
+            "fp64": pk["fp64_tops"] * 1e12 / max(w64, 1e-9)}
+    bound = min(ceil, key=ceil.get)
+    return {"V_int": round(v, 3), "N_mt": round(m, 3), "W32": round(w32, 1), "W64": round(w64, 1),
+            "bound": bound, "ceiling_grays": round(ceil[bound] / 1e9, 2),
+            "frac": round(rays_per_s_kernel / ceil[bound], 4), "sample": own["n"]}
 
 
 class ClockSampler:
@@ -545,6 +565,23 @@ def main():
                        "pageable_*: the same call on plain numpy arrays",
                "segments": e2e_note}
 
+    # per-segment work units on a sample (outside the timed region): this
+    # engine's fast tree and, as a cross-check of SURVEY 8(d)'s figures, the
+    # reference tree with the reference's traversal semantics
+    own = None
+    try:
+        from paper_2209_02878_b200._backend import b200 as _b200
+
+        m = min(n, 1_000_000)
+        own = {}
+        for kind_, ref_sem in (("fast", False), ("reference", True)):
+            tree = _b200.DeviceTree(mesh_d, kind=kind_)
+            st = tree.stats(seg_d.starts[:m], seg_d.ends[:m], mode, ref_semantics=ref_sem)
+            tree.close()
+            own[kind_] = dict(st, n=m)
+    except Exception as exc:  # diagnostics only
+        print(f"tree stats unavailable: {exc}", file=sys.stderr)
+        own = None
     q_ms = float(np.mean(query_ms))
     h_ms = float(np.mean(hot_ms)) if hot_ms and min(hot_ms) > 0 else q_ms
     phase_keys = sorted({k for p in phases for k in p})
@@ -565,7 +602,7 @@ def main():
                                           for k in phase_keys},
                      "source": "traversal_kernel: CUDA events in the timed region; the rest: "
                                "5 instrumented steps after it"},
-        "roofline": roofline(cfg, n / (h_ms / 1e3), value * 1e6 / world, hot_kernel),
+        "roofline": roofline(cfg, n / (h_ms / 1e3), value * 1e6 / world, hot_kernel, own),
         "gpu_launches": int(launches),
         "clocks": clocks.summary(t_start, t_end + 0.02),
     }

@@ -956,7 +956,9 @@ static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int6
     if (rc) return rc;
     if (n_r < 0) return fail(RS_INVALID_ARG, "negative segment count");
     if (n_r > 2147483647ll) return fail(RS_INVALID_ARG, "segment count exceeds int32 indexing");
-    if (t->kind == kTreeFast && n_r > 0 && !g_binary_fast) {
+    // statistics (rs_query_stats) come from the per-segment binary walk, the
+    // unit SURVEY 8(d)'s V_int / N_mt count, on either tree kind
+    if (t->kind == kTreeFast && n_r > 0 && !g_binary_fast && !stats) {
         FastOut o;
         o.flags = mode == kCount ? cnt : det;
         o.det = det; o.tri = tri; o.dist = dist; o.pts = pts;
@@ -980,6 +982,7 @@ static int query_impl(const rs_tree* t, const float* d_s, const float* d_e, int6
     RsStatus* st = reinterpret_cast<RsStatus*>(blk);
     CK(cudaMemsetAsync(blk, 0, align256(sizeof(RsStatus)) + cs, s));
     QueryArgs a = make_args(t, d_s, d_e, n_r, max_coll, max_stack, st);
+    if (t->kind == kTreeFast) a.nodes4 = nullptr;  // binary kernels over the fast tree's records
     a.detected = det; a.counts = cnt; a.tri = tri; a.dist = dist; a.points = pts;
     a.c_ray = c_ray; a.c_dist = c_dist; a.c_tri = c_tri; a.c_point = c_pt;
     a.tile_status = reinterpret_cast<unsigned long long*>(blk + align256(sizeof(RsStatus)));
