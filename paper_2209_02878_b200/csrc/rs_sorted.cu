@@ -82,6 +82,23 @@ __device__ __forceinline__ void get_rec(const SortedArgs& a, unsigned idx, float
     r1 = a.rec[2ull * idx + 1];
 }
 
+// The record's last read (the tile kernel's processing pass): marked
+// evict-first in L2, so the dead records stop displacing the outputs
+// (flags / winning triangles / hit bits written at random by segment id).
+__device__ __forceinline__ void get_rec_last(const SortedArgs& a, unsigned idx, float4& r0, float4& r1) {
+#ifdef RS_NO_EVICT_HINT
+    get_rec(a, idx, r0, r1);
+#else
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const float4* p = a.rec + 2ull * idx;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r0.x), "=f"(r0.y), "=f"(r0.z), "=f"(r0.w) : "l"(p), "l"(pol));
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r1.x), "=f"(r1.y), "=f"(r1.z), "=f"(r1.w) : "l"(p + 1), "l"(pol));
+#endif
+}
+
 __device__ __forceinline__ void put_rec(const SortedArgs& a, unsigned pos, const float s[3], int id,
                                         const float e[3]) {
     st_rec(a.rec + 2ull * pos, s, id, e);
@@ -1447,7 +1464,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
             const unsigned idx = base + lane;
             const bool valid = idx < end;
             float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-            if (valid) get_rec(a, idx, r0, r1);
+            if (valid) get_rec_last(a, idx, r0, r1);
             int det = 0, nh = 0, btri = -1;
             double bt = 0.0;
             if (fallback) {
