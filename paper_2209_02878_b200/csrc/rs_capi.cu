@@ -743,6 +743,7 @@ struct FastOut {
     float *c_dist = nullptr, *c_pt = nullptr;
     long long ray_offset = 0;
     unsigned long long* row_base = nullptr;  // compact rows: running row count across chunks
+    bool mapped = false;  // compact rows go to host-mapped memory
 };
 
 struct FastScratch {
@@ -881,7 +882,8 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
             launch_leaf_inverse(t->leaves, (int)t->n, t->leaf_of, s);
         }
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
-                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base, t->leaves, t->leaf_of};
+                       f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base, t->leaves, t->leaf_of,
+                       o.mapped};
         if (o.c_ray) launch_bary_compact(ca, s);
         else launch_bary_dense(ca, o.det, o.tri, o.dist, o.pts, s);
     }
@@ -2135,6 +2137,7 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
             if (bary && zc) {
                 o.c_ray = zray; o.c_dist = zdist; o.c_tri = ztri; o.c_pt = zpt;
                 o.row_base = d_rows;
+                o.mapped = true;
             } else if (bary) {
                 o.c_ray = dray + lo; o.c_dist = ddist + lo; o.c_tri = dtri + lo; o.c_pt = dpt + 3 * lo;
             } else {

@@ -153,6 +153,9 @@ struct CompactArgs {
     // test, instead of being stored per segment by the traversal
     const RsLeaf* leaves;
     const int* leaf_of;
+    // rows land in host-mapped memory: form them in one kernel (a second
+    // pass would read ray/triangle back over PCIe)
+    bool fused;
 };
 // leaf_of[leaves[k].id] = k for the n leaves (the compaction's t recompute).
 void launch_leaf_inverse(const RsLeaf* leaves, int n, int* leaf_of, cudaStream_t s);

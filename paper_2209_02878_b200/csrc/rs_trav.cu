@@ -489,6 +489,11 @@ void launch_leaf_inverse(const RsLeaf* leaves, int n, int* leaf_of, cudaStream_t
 constexpr int kCompactItems = 16;
 constexpr int kCompactTile = kCompactThreads * kCompactItems;
 
+// ROWS: the compaction also forms each row's distance and point (t stored
+// by the traversal); without ROWS it writes only ray index and triangle,
+// and k_bary_rows recomputes t and the geometry one row per thread (at 110
+// registers the fused recompute left the compaction at 24% occupancy).
+template <bool ROWS>
 __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a) {
     // Striped tile: in round k, thread t owns segment base + k*256 + t, so
     // every load and every output row of a round is coalesced across the
@@ -549,6 +554,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
         if (tri[k] < 0) continue;
         const long long i = base + k * kCompactThreads + threadIdx.x;
         const unsigned long long pos = tb + s_round[k][w] + inwarp[k];
+        a.ray[pos] = (int)(i + a.ray_offset);
+        a.tri[pos] = tri[k];
+        if (!ROWS) continue;
         const float* s = a.starts + 3 * i;
         const float* e = a.ends + 3 * i;
         const double sx = s[0], sy = s[1], sz = s[2];
@@ -557,9 +565,30 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
         const double t = win_t(a, i, tri[k], sx, sy, sz, dx, dy, dz);
         float px, py, pz, d;
         hit_point(sx, sy, sz, dx, dy, dz, t, &px, &py, &pz, &d);
-        a.ray[pos] = (int)(i + a.ray_offset);
         a.dist[pos] = d;
-        a.tri[pos] = tri[k];
+        a.point[3 * pos] = px;
+        a.point[3 * pos + 1] = py;
+        a.point[3 * pos + 2] = pz;
+    }
+}
+
+// The rows of one compaction (k_bary_compact<false>): t recomputed from the
+// winning leaf, then distance and point, one row per thread.
+__global__ void __launch_bounds__(256) k_bary_rows(CompactArgs a) {
+    const unsigned long long base = a.row_base ? *a.row_base : 0ull;
+    const unsigned long long hits = *a.n_hits;
+    for (unsigned long long r = blockIdx.x * 256ull + threadIdx.x; r < hits; r += gridDim.x * 256ull) {
+        const unsigned long long pos = base + r;
+        const long long i = (long long)a.ray[pos] - a.ray_offset;
+        const float* s = a.starts + 3 * i;
+        const float* e = a.ends + 3 * i;
+        const double sx = s[0], sy = s[1], sz = s[2];
+        const double dx = __dsub_rn((double)e[0], sx), dy = __dsub_rn((double)e[1], sy),
+                     dz = __dsub_rn((double)e[2], sz);
+        const double t = win_t(a, i, a.tri[pos], sx, sy, sz, dx, dy, dz);
+        float px, py, pz, d;
+        hit_point(sx, sy, sz, dx, dy, dz, t, &px, &py, &pz, &d);
+        a.dist[pos] = d;
         a.point[3 * pos] = px;
         a.point[3 * pos + 1] = py;
         a.point[3 * pos + 2] = pz;
@@ -764,8 +793,15 @@ __global__ void k_advance_rows(unsigned long long* row_base, const unsigned long
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s) {
     if (a.n_r <= 0) return;
     count_launches(1);
-    k_bary_compact<<<(unsigned)((a.n_r + kCompactTile - 1) / kCompactTile), kCompactThreads, 0,
-                     s>>>(a);
+    const unsigned tiles = (unsigned)((a.n_r + kCompactTile - 1) / kCompactTile);
+    if (a.best_t || a.fused) {
+        k_bary_compact<true><<<tiles, kCompactThreads, 0, s>>>(a);
+    } else {
+        k_bary_compact<false><<<tiles, kCompactThreads, 0, s>>>(a);
+        const long long want = (a.n_r + 255) / 256, cap = (long long)device_sms() * 16;
+        count_launches(1);
+        k_bary_rows<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(a);
+    }
     if (a.row_base) {
         count_launches(1);
         k_advance_rows<<<1, 1, 0, s>>>(a.row_base, a.n_hits);

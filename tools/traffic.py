@@ -4,8 +4,8 @@
 
     python tools/traffic.py launches.csv <cfg> [--out profiles/traffic_<cfg>.json]
 
-A step starts at a `k_prep` launch (the build's first kernel); the last
-complete step of the list is used.  The hot kernel is the step's longest
+A step starts at a `k_prep` launch (the build's first kernel); the
+next-to-last step that ran a traversal kernel is used.  The hot kernel is the step's longest
 traversal kernel (k_trav_*); its DRAM bytes per launch are the roofline's
 `traffic`, the step's total DRAM bytes go beside it.  ncu's times are
 cold-cache and serialised: shares matter, not absolutes.
@@ -43,10 +43,16 @@ def short(name: str) -> str:
 
 
 def last_step(launches):
+    """The last step (k_prep .. next k_prep) that ran the traversal kernel
+    (bench.py's per-segment statistics builds after the timed steps are
+    skipped)."""
     starts = [i for i, x in enumerate(launches) if short(x["kernel"]) == "k_prep"]
-    if len(starts) >= 2:
-        return launches[starts[-2]:starts[-1]]
-    return launches[starts[-1]:] if starts else launches
+    bounds = list(zip(starts, starts[1:] + [len(launches)]))
+    steps = [launches[a:b] for a, b in bounds]
+    with_trav = [st for st in steps if any(short(x["kernel"]).startswith("k_trav") for x in st)]
+    if len(with_trav) >= 2:
+        return with_trav[-2]  # the last one may be cut short by the capture's end
+    return with_trav[-1] if with_trav else (steps[-1] if steps else launches)
 
 
 def main():
