@@ -167,3 +167,49 @@ def test_two_rank_sharded_gpu_matches_reference(name, kind):
     GPU here) on numpy or CUDA-tensor inputs, gather to rank 0 over gloo."""
     res = _spawn(_worker, lambda q: (name, q, kind, "rank0"))
     _check(res, load(name), "rank0")
+
+
+def _generated_worker(rank, world, port, q):
+    """BASELINE configs[4]'s sharding: each rank generates its own contiguous
+    shard of one batch on its GPU (rs_generate_segments, keyed by the global
+    row), runs it, and the flags are gathered to rank 0."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+
+        mesh = rs.generate_scene(20_000, 0, 0.5, seed=2022).mesh
+        dmesh = rs.Mesh.from_arrays(torch.from_numpy(mesh.vertices).cuda(),
+                                    torch.from_numpy(mesh.triangles).cuda())
+        n = 1_000_003
+        lo, hi = shard_range(n, rank, world)
+        segs, truth = rs.generate_segments_device(dmesh, hi - lo, 0.5, seed=7, first=lo)
+        res = rs.run_batch(dmesh, segs, rs.EngineConfig(mode="count"))
+        assert torch.equal(res.counts, truth.to(torch.int32))
+        local = res.counts.cpu()
+        sizes = [shard_range(n, r, world)[1] - shard_range(n, r, world)[0] for r in range(world)]
+        pad = torch.zeros(max(sizes), dtype=torch.int32)
+        pad[: local.shape[0]] = local
+        bufs = [torch.zeros_like(pad) for _ in range(world)] if rank == 0 else None
+        dist.gather(pad, gather_list=bufs, dst=0)
+        out = torch.cat([b[:k] for b, k in zip(bufs, sizes)]).numpy() if rank == 0 else None
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_generated_shards_gather_to_rank0():
+    """Two ranks (one GPU here) each generate and intersect their shard of a
+    1M-segment batch; rank 0's gathered counts equal one rank generating the
+    whole batch (shard invariance of the generator + sharded run_batch)."""
+    import torch
+
+    res = _spawn(_generated_worker, lambda q: (q,))
+    mesh = rs.generate_scene(20_000, 0, 0.5, seed=2022).mesh
+    dmesh = rs.Mesh.from_arrays(torch.from_numpy(mesh.vertices).cuda(), torch.from_numpy(mesh.triangles).cuda())
+    segs, truth = rs.generate_segments_device(dmesh, 1_000_003, 0.5, seed=7)
+    whole = rs.run_batch(dmesh, segs, rs.EngineConfig(mode="count")).counts.cpu().numpy()
+    assert np.array_equal(res[0], whole)
+    assert np.array_equal(whole, truth.cpu().numpy().astype(np.int32))
