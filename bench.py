@@ -420,16 +420,19 @@ def main():
     else:
         out = {"flags": torch.empty(n, dtype=torch.int32, device=dev)}
     lib = _lib.lib()
-    # timed region: only the dominant kernel's CUDA events (phase events cost
-    # ~40 us per step); the build/query split comes from a short instrumented
-    # pass after the timed region
+    # timed region: the dominant kernel's CUDA events on every
+    # `hot_every`-th step (timing level 2; the event nodes add ~10 us to a
+    # step, phase events ~40 us), level 0 on the others; the build/query
+    # split comes from a short instrumented pass after the timed region
     timing_level = int(os.environ.get("RS_BENCH_TIMING", "2"))
+    hot_every = max(1, int(os.environ.get("RS_BENCH_HOT_EVERY", "10")))
     lib.rs_set_timing(timing_level)
 
     def step():
         return rs.run_device(mesh_d, seg_d, config, kind, out=out)
 
-    for _ in range(args.warmup):
+    for w in range(args.warmup):  # both graphs (with and without the kernel events) captured
+        lib.rs_set_timing(timing_level if w % 2 == 0 else 0)
         res = step()
     # correctness gate on the benchmarked output: generated ground truth
     if not os.environ.get("RS_BENCH_NOCHECK"):  # timing experiments on deliberately wrong builds only
@@ -454,9 +457,11 @@ def main():
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            sampled = timing_level and i % hot_every == 0
+            lib.rs_set_timing(timing_level if sampled else 0)
             step()
-            if timing_level:
+            if sampled:
                 lib.rs_last_timings(C.byref(bms), C.byref(qms), C.byref(hms))
                 hot_ms.append(hms.value)
         ev1.record(stream)
@@ -600,8 +605,8 @@ def main():
                      "traversal_kernel": round(h_ms, 4),
                      "reference_phases": {k: round(1e3 * float(np.mean([p.get(k, 0.0) for p in phases])), 4)
                                           for k in phase_keys},
-                     "source": "traversal_kernel: CUDA events in the timed region; the rest: "
-                               "5 instrumented steps after it"},
+                     "source": f"traversal_kernel: CUDA events around it on every {hot_every}th step "
+                               "of the timed region; the rest: 5 instrumented steps after it"},
         "roofline": roofline(cfg, n / (h_ms / 1e3), value * 1e6 / world, hot_kernel, own),
         "gpu_launches": int(launches),
         "clocks": clocks.summary(t_start, t_end + 0.02),
