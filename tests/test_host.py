@@ -150,3 +150,26 @@ def test_unpermute_barycentric_rows():
     assert np.array_equal(r.distance.cpu().numpy(), dist[order])
     assert np.array_equal(r.triangle_id.cpu().numpy(), tri[order])
     assert np.array_equal(r.point.cpu().numpy(), pt[order])
+
+
+def test_bench_reference_arm_line():
+    """bench.py --impl reference (the driver's reference arm) runs the
+    reference package's own run_batch on the host cores and prints one JSON
+    line with the contract's keys (small --rays so it takes seconds)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(repo / "bench.py"), "--impl", "reference", "--rays", "20000",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                       cwd=str(repo))
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["same_config"] is True  # every step ran the whole (small) batch
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
