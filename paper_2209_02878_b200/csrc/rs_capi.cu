@@ -94,8 +94,9 @@ struct rs_tree {
     const unsigned long long* codes = nullptr;
     unsigned long long* code_samples = nullptr;
     int sample_stride = 0, n_samples = 0, key_mode = 0;
-    // leaf index by triangle id (barycentric compaction's t recompute);
-    // allocated by the first barycentric fast query, freed with the tree
+    // leaf index by triangle id (the barycentric compaction's t recompute;
+    // part of the tree block, rewritten by every barycentric fast query --
+    // concurrent queries on one tree write identical values)
     int* leaf_of = nullptr;
 };
 
@@ -312,7 +313,7 @@ size_t tree_bytes(int64_t n) {
     b += align256(sizeof(RsNode) * (size_t)(n > 1 ? n - 1 : 1));
     b += align256(sizeof(RsLeaf) * (size_t)n);
     b += 2 * align256(sizeof(float) * 6 * (size_t)n);
-    b += 10 * align256(sizeof(int) * (size_t)n);
+    b += 11 * align256(sizeof(int) * (size_t)n);
     b += 2 * align256(sizeof(int) * 2 * (size_t)n);
     b += align256(sizeof(RsNode4) * (size_t)(n > 1 ? n - 1 : 1));
     return b;
@@ -339,6 +340,7 @@ void carve_tree(rs_tree* t) {
     t->ta.height = c.take<int>(2 * n);
     t->ta.parent = c.take<int>(2 * n);
     t->nodes4 = c.take<RsNode4>(n > 1 ? n - 1 : 1);
+    t->leaf_of = c.take<int>(n);
 }
 
 std::mutex g_pool_mu;
@@ -644,10 +646,21 @@ bool is_pageable(const void* p) {
     return at.type == cudaMemoryTypeUnregistered;
 }
 
+// per thread and per device: a thread that drives several GPUs keeps each
+// device's streams, events and pinned buffers (g_pipe is the current one)
+thread_local std::map<int, Pipe> g_pipes;
+
 int pipe_init() {
     int dev;
     CK(cudaGetDevice(&dev));
     if (g_pipe.device == dev) return RS_OK;
+    if (g_pipe.device >= 0) g_pipes[g_pipe.device] = g_pipe;  // park the previous device's set
+    auto it = g_pipes.find(dev);
+    if (it != g_pipes.end()) {
+        g_pipe = it->second;
+        return RS_OK;
+    }
+    g_pipe = Pipe{};
     CK(cudaStreamCreateWithFlags(&g_pipe.copy, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&g_pipe.copy2, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
@@ -723,7 +736,6 @@ int rs_tree_download(const rs_tree* t, float* ib, int32_t* cl, int32_t* cr, int3
 int rs_free(rs_tree* t, void* stream) {
     if (!t) return RS_OK;
     if (t->scratch) dfree(t->scratch, S(stream));
-    if (t->leaf_of) dfree(t->leaf_of, S(stream));
     cudaError_t e = dfree(t->block, S(stream));
     delete t;
     if (e != cudaSuccess) return fail(RS_CUDA_ERROR, "cudaFreeAsync: %s", cudaGetErrorString(e));
@@ -877,10 +889,8 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
     launch_sorted_trav(sorted_args(t, d_s, d_e, n_r, o, f), mode, stats, s);
     if (f.hitbits) launch_expand_bits(o.flags, f.hitbits, n_r, s);
     if (mode == kBarycentric) {
-        if (!f.best_t) {  // the compaction recomputes t from the winning leaf
-            if (!t->leaf_of) CK(dmalloc(reinterpret_cast<void**>(&const_cast<rs_tree*>(t)->leaf_of), 4ull * t->n, s));
+        if (!f.best_t)  // the compaction recomputes t from the winning leaf
             launch_leaf_inverse(t->leaves, (int)t->n, t->leaf_of, s);
-        }
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
                        f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base, t->leaves, t->leaf_of,
                        o.mapped};
@@ -1227,19 +1237,26 @@ struct Fork {
     cudaStream_t hp = nullptr;   // the build, at the highest stream priority
     cudaEvent_t prep = nullptr, bin = nullptr, bin2 = nullptr, start = nullptr, built = nullptr;
 };
+// per thread and per device (streams and events belong to one device)
+static thread_local std::map<int, Fork> g_forks;
 static thread_local Fork g_fork;
 
 static int fork_init() {
-    if (g_fork.aux) return RS_OK;
-    CK(cudaStreamCreateWithFlags(&g_fork.aux, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&g_fork.prep, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&g_fork.bin, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&g_fork.bin2, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&g_fork.start, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&g_fork.built, cudaEventDisableTiming));
-    int lo = 0, hi = 0;
-    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CK(cudaStreamCreateWithPriority(&g_fork.hp, cudaStreamNonBlocking, hi));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    Fork& f = g_forks[dev];
+    if (!f.aux) {
+        CK(cudaStreamCreateWithFlags(&f.aux, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&f.prep, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&f.bin, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&f.bin2, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&f.start, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&f.built, cudaEventDisableTiming));
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&f.hp, cudaStreamNonBlocking, hi));
+    }
+    g_fork = f;  // the current device's set
     return RS_OK;
 }
 
