@@ -383,9 +383,18 @@ def main():
     from paper_2209_02878_b200.parallel import shard_range
 
     rank, world, local = dist_env()
+    # RS_BENCH_BACKEND=gloo: the multi-rank code path on a single GPU (ranks
+    # share device local % device_count; collectives on CPU tensors) -- a
+    # test of the N>1 logic, never a scaling measurement
+    backend = os.environ.get("RS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    cdev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     cfg = CONFIGS[args.config]
     scaling = args.scaling or cfg.scaling
     mode = cfg.mode
@@ -499,32 +508,40 @@ def main():
     if world > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     total_rays = n * world * args.steps
     value = total_rays / (max_ms / 1e3) / 1e6
 
-    # result gather to rank 0 over NCCL (outside the timed region)
+    # result gather to rank 0 over NCCL (outside the timed region); shards
+    # may differ by a row (strong scaling): padded to the longest
     gather = None
     if world > 1 and mode != "barycentric":
-        flat = out["flags"]
+        sizes = torch.tensor([n], dtype=torch.int64, device=cdev)
+        every = [torch.zeros_like(sizes) for _ in range(world)]
+        dist.all_gather(every, sizes)
+        m = int(max(int(x.item()) for x in every))
+        flat = torch.zeros(m, dtype=torch.int32, device=cdev)
+        flat[:n] = out["flags"].to(cdev)
         bufs = [torch.empty_like(flat) for _ in range(world)] if rank == 0 else None
-        g0 = torch.cuda.Event(enable_timing=True)
-        g1 = torch.cuda.Event(enable_timing=True)
         dist.gather(flat, gather_list=bufs, dst=0)
         dist.barrier()
-        g0.record(stream)
+        torch.cuda.synchronize()
         reps = 5
+        g0 = time.perf_counter()
+        ev_g0, ev_g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev_g0.record(stream)
         for _ in range(reps):
             dist.gather(flat, gather_list=bufs, dst=0)
-        g1.record(stream)
+        ev_g1.record(stream)
         torch.cuda.synchronize()
-        gt = torch.tensor([g0.elapsed_time(g1) / reps], dtype=torch.float64, device=dev)
+        g_ms = ev_g0.elapsed_time(ev_g1) / reps if backend == "nccl" else 1e3 * (time.perf_counter() - g0) / reps
+        gt = torch.tensor([g_ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(gt, op=dist.ReduceOp.MAX)
-        gather = {"ms": round(float(gt.item()), 4), "bytes_to_rank0": 4 * n * (world - 1),
-                  "how": "dist.gather (NCCL) of every rank's int32 flags to rank 0, timed after "
+        gather = {"ms": round(float(gt.item()), 4), "bytes_to_rank0": 4 * m * (world - 1),
+                  "how": f"dist.gather ({backend}) of every rank's int32 flags to rank 0, timed after "
                          "the timed region, max over ranks"}
 
     # e2e through the public API with host buffers (pinned, then pageable)
@@ -552,7 +569,7 @@ def main():
                 t0 = time.perf_counter()
                 r = rs.run_batch(mesh_x, seg_x, config)
                 ts.append(time.perf_counter() - t0)
-            tt = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
+            tt = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=cdev)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             return tt.item(), r
