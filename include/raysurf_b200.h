@@ -247,8 +247,10 @@ RS_API int rs_set_option(const char *name, long long value, long long *old_value
 RS_API const char *rs_hot_kernel(void);
 
 /* Diagnostics: the 8 device status words (bad, internal, hits, tile_counter,
- * visits, mts, cand_count, pad) of the calling thread's last graph-replayed
- * rs_run_batch_device. */
+ * visits, mts, cand_count, pad) of the calling thread's last
+ * rs_run_batch_device call when that call ran a captured graph; all zeros
+ * when it ran the direct launches (a graph is captured on an argument set's
+ * second call). */
 RS_API int rs_last_status(unsigned long long *out8);
 
 #ifdef __cplusplus

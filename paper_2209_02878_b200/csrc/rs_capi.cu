@@ -1287,6 +1287,23 @@ __global__ void k_merge_status(RsStatus* dst, const RsStatus* src) {
 // Fast-tree run_batch with the binning forked onto a second stream right
 // after k_prep: binning (two passes over the segments) overlaps keys, sort
 // and climb.  Leaves the status in f.st (device); the caller frees f.blk.
+// critical-path experiments (RS_DEBUG_DELAY_BUILD_US / _BIN_US): a
+// one-thread spin of that many microseconds at the end of the build /
+// binning stream
+__global__ void k_debug_spin(long long ns) {
+    long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 >= ns) break;
+    }
+}
+static long long debug_delay_ns(const char* name) {
+    const char* e = getenv(name);
+    return e && *e ? atoll(e) * 1000ll : 0;
+}
+
 static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t* d_tris,
                                int64_t n_t, const float* d_starts, const float* d_ends,
                                int64_t n_r, int mode, const FastOut& o, FastScratch& f,
@@ -1323,6 +1340,7 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
         }
         r = fast_bin(t, d_starts, d_ends, n1, mode, o1, f, aux);
         if (r) return r;
+        if (const long long ns = debug_delay_ns("RS_DEBUG_DELAY_BIN_US")) k_debug_spin<<<1, 1, 0, aux>>>(ns);
         CK(cudaEventRecord(g_fork.bin, aux));
         if (two) {
             r = fast_bin(t, d_starts + 3 * n1, d_ends + 3 * n1, n2, mode, o2, f2, aux);
@@ -1334,6 +1352,7 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
     rs_tree* t = nullptr;
     rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, bs, &t, fork, true);
     if (rc) return rc;
+    if (const long long ns = debug_delay_ns("RS_DEBUG_DELAY_BUILD_US")) k_debug_spin<<<1, 1, 0, bs>>>(ns);
     if (bs != s) {
         CK(cudaEventRecord(g_fork.built, bs));
         CK(cudaStreamWaitEvent(s, g_fork.built, 0));
@@ -1717,7 +1736,9 @@ static std::shared_ptr<GraphEntry> capture_graph(const float* d_verts, int64_t n
                         cudaSuccess;
     if (g) cudaGraphDestroy(g);
     if (!ok) {
-        cudaGetLastError();
+        const cudaError_t ce = cudaGetLastError();
+        if (getenv("RS_DEBUG_GRAPH"))
+            fprintf(stderr, "[rs] graph capture failed: rc %d, %s\n", erc, cudaGetErrorString(ce));
         return nullptr;
     }
     return e;
@@ -1729,6 +1750,7 @@ int rs_run_batch_device(const float* d_verts, int64_t n_v, const int32_t* d_tris
                         int32_t* d_ray, float* d_dist, int32_t* d_tri, float* d_pt,
                         int64_t* n_hits, int64_t* bad, void* stream) {
     marks_reset();
+    g_last_status = RsStatus{};  // zeros unless this call runs a graph
     int rc = check_query(mode, max_coll, max_stack);
     if (rc) return rc;
     if (bad) *bad = -1;

@@ -555,10 +555,11 @@ __global__ void __launch_bounds__(256) k_bin_scatter(SortedArgs a) {
 // engine (cp.async.bulk global->shared, completion on an mbarrier) one chunk
 // ahead of the compute, so the DRAM stream never waits for the key math.
 #ifndef RS_STREAM_THREADS
-#define RS_STREAM_THREADS 256
+#define RS_STREAM_THREADS 128  // x 9 CTAs per SM, 7 resident (A/B vs 256 x 4: C3 -7 us, C2 -1.5, C4 +3;
+                                // 7 CTAs or plain reductions without the duplicate check: no gain)
 #endif
 #ifndef RS_STREAM_CTAS
-#define RS_STREAM_CTAS 4
+#define RS_STREAM_CTAS 9
 #endif
 constexpr int kStreamThreads = RS_STREAM_THREADS;
 constexpr int kStreamSegs = 4 * kStreamThreads;  // four segments per thread per stage
@@ -1509,7 +1510,7 @@ struct SortedOpts {
     int tile_wide = 0;           // tile walk over the collapsed 4-wide nodes (A/B: no gain on C2)
     int fast_keys = 0;           // fast-tree key grid: 0 isotropic, 1 per-axis, 2 auto
     unsigned range_max = 4096;   // tile lists from a Morton key range of at most this many leaves (0: walk only)
-    int geom = 0;                // 1: bin geometry derived once by k_seg_sample (A/B: C3/C5 -1..2%, C2 +3%)
+    int geom = 1;                // 1: bin geometry derived once by k_seg_sample (A/B round 2: C2 -9 us, C3 -2.5 us)
     int fast_path = 0;           // 0 binned tiles, 1 collision buffer (rs_trav.cu)
     long long cand_cap = 0;      // collision buffer: initial capacity (0: 2 x segments + 4096)
 };

@@ -204,7 +204,7 @@ def test_traversal_variants_bitwise(name, mode, variant, device):
     {"tile_wide": 1},                               # tile walk over 4-wide nodes
     {"range_max": 0},                               # candidate lists from the walk only
     {"range_max": 1 << 30},                         # candidate lists from key ranges only
-    {"geom": 1},                                    # bin geometry derived once by the sample kernel
+    {"geom": 0},                                    # bin geometry derived by every binning CTA
     {"tile_depth": 1, "tile_balance": 1},           # depth-complexity cap: one-CTA-size tiles
     {"tile_depth": 0, "tile_balance": 1},           # no depth cap
 ], ids=["small", "huge", "many", "finebins", "coarsebins", "notma", "widewalk", "walkonly", "rangeonly", "geom", "depth1", "depth0"])
@@ -240,13 +240,25 @@ def test_collision_buffer_path(name, mode, cap, device):
     mesh, batch = mesh_batch(fx, device)
     want = expected(fx, "cap32" if name == "layered" else "batch", mode)
     with _lib.option("fast_path", 1), _lib.option("cand_cap", cap):
-        for rep in range(3 if device else 1):  # direct, graph capture, graph replay
+        # direct launches until an argument set repeats (the outputs are fresh
+        # tensors each call, so that depends on the caching allocator), then
+        # graph capture + launch, then replays
+        graph_runs = 0
+        for rep in range(8 if device else 1):
             got = rs.run_batch(mesh, batch, rs.EngineConfig(mode=mode, tree="fast"))
             assert_result_fields(result_dict(got), want, f"{name} {mode} buffer cap={cap} rep {rep}")
-        if cap and device:
-            st = (C.c_ulonglong * 8)()
-            _lib.lib().rs_last_status(st)
-            assert st[6] > cap and st[7] == 1, list(st)  # cand_count claimed past the end, dropped
+            if device:
+                st = (C.c_ulonglong * 8)()
+                _lib.lib().rs_last_status(st)
+                if st[6] == 0:
+                    continue  # no graph ran this call
+                graph_runs += 1
+                if cap:
+                    assert st[6] > cap and st[7] == 1, list(st)  # cand_count claimed past the end, dropped
+                if graph_runs == 2:
+                    break
+        if device:
+            assert graph_runs >= 1, "no call ran a captured graph"
         dt = b200.DeviceTree(rs.Mesh.from_arrays(fx["vertices"], fx["triangles"]), kind="fast")
         dense = dt.query_dense(fx["starts"], fx["ends"], mode, 32, 64, ref_semantics=False)
         key = {"boolean": "detected", "count": "counts", "barycentric": "detected"}[mode]
