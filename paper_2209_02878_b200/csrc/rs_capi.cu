@@ -1316,16 +1316,22 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
     FastOut o1 = o, o2 = o;
     FastScratch f2;
     cudaStream_t bs = s;  // the build's stream
+    CK(cudaEventRecord(g_fork.start, s));
     if (g_build_prio) {
         bs = g_fork.hp;
-        CK(cudaEventRecord(g_fork.start, s));
         CK(cudaStreamWaitEvent(bs, g_fork.start, 0));
     }
+    // the binning stream's presets (status, zeroed bins and outputs) need
+    // nothing from the build: they run beside k_prep, off the critical path
+    CK(cudaStreamWaitEvent(aux, g_fork.start, 0));
+    rc = fast_alloc(f, n1, mode, 2ll * n1 + 4096, aux);
+    if (rc) return rc;
+    rc = fast_presets(d_starts, d_ends, n1, mode, o1, f, aux);
+    if (rc) return rc;
     auto fork = [&](rs_tree* t) -> int {
         CK(cudaEventRecord(g_fork.prep, bs));
         CK(cudaStreamWaitEvent(aux, g_fork.prep, 0));
-        int r = fast_alloc(f, n1, mode, 2ll * n1 + 4096, aux);
-        if (r) return r;
+        int r = RS_OK;
         if (two) {
             r = fast_alloc(f2, n2, mode, 2ll * n2 + 4096, aux);
             if (r) return r;
@@ -1338,7 +1344,7 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
                 o2.row_base = rows;
             }
         }
-        r = fast_bin(t, d_starts, d_ends, n1, mode, o1, f, aux);
+        r = fast_bin(t, d_starts, d_ends, n1, mode, o1, f, aux, false);
         if (r) return r;
         if (const long long ns = debug_delay_ns("RS_DEBUG_DELAY_BIN_US")) k_debug_spin<<<1, 1, 0, aux>>>(ns);
         CK(cudaEventRecord(g_fork.bin, aux));
