@@ -577,13 +577,17 @@ def main():
         t_pin, r = e2e_time(mesh_p, seg_p, max(3, min(args.steps // 4, 25)))
         t_pg, _ = e2e_time(mesh_h, seg_pg, 3)
         h2d = 24 * m + 12 * mesh_h.num_vertices + 12 * mesh_h.num_triangles
-        d2h = 4 * m if mode != "barycentric" else 24 * r.num_crossing()
+        # boolean flags cross PCIe packed 32 per word (expanded to the int32
+        # result on the host threads); count returns int32 counts
+        d2h = (4 * ((m + 31) // 32) if mode == "boolean" else 4 * m) if mode != "barycentric" \
+            else 24 * r.num_crossing()
         e2e = {"value": round(m * world / t_pin / 1e6, 3), "unit": "Mrays/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": round(1e3 * t_pin, 3),
                "pageable_value": round(m * world / t_pg / 1e6, 3),
                "pageable_ms_per_step": round(1e3 * t_pg, 3),
-               "path": "run_batch(numpy, pinned) -> rs_run_batch_host: chunked H2D/query/D2H; "
+               "path": "run_batch(numpy, pinned) -> rs_run_batch_host: chunked H2D/query/D2H "
+                       "(boolean flags as bits, expanded to int32 on the host); "
                        "pageable_*: the same call on plain numpy arrays",
                "segments": e2e_note}
 

@@ -562,6 +562,8 @@ struct Pipe {
     int64_t hst_cap = 0;
     char* stg = nullptr;      // pinned staging for pageable inputs (2 chunk slots + mesh)
     size_t stg_cap = 0;
+    unsigned* hbits = nullptr;  // pinned landing area of the packed boolean flags
+    size_t hbits_cap = 0;       // words
 };
 thread_local Pipe g_pipe;
 
@@ -581,22 +583,36 @@ class CopyPool {
             std::memcpy(dst, src, bytes);
             return;
         }
-        std::lock_guard<std::mutex> one(call_mu_);  // one parallel copy at a time
+        char* d = static_cast<char*>(dst);
+        const char* sp = static_cast<const char*>(src);
+        parallel([=](int k, int parts) {
+            const size_t per = ((bytes + parts - 1) / parts + 63) & ~size_t(63);
+            const size_t lo = per * (size_t)k;
+            if (lo < bytes) std::memcpy(d + lo, sp + lo, std::min(per, bytes - lo));
+        });
+    }
+    // job(k, parts) for k = 0..parts-1, one part on the caller
+    void parallel(const std::function<void(int, int)>& job) {
+        if (workers_ == 0) {
+            job(0, 1);
+            return;
+        }
+        std::lock_guard<std::mutex> one(call_mu_);  // one parallel job at a time
         const int parts = workers_ + 1;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            dst_ = static_cast<char*>(dst);
-            src_ = static_cast<const char*>(src);
-            bytes_ = bytes;
+            job_ = &job;
             parts_ = parts;
             pending_ = workers_;
             ++gen_;
         }
         cv_.notify_all();
-        run_part(0);
+        job(0, parts);
         std::unique_lock<std::mutex> lk(mu_);
         done_cv_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
     }
+    int parts() const { return workers_ + 1; }
 
   private:
     CopyPool() {
@@ -607,20 +623,19 @@ class CopyPool {
         workers_ = e && *e ? atoi(e) : (int)(hw >= 16 ? 8 : (hw > 1 ? hw / 2 : 0));
         for (int w = 0; w < workers_; ++w) std::thread([this, w] { loop(w + 1); }).detach();
     }
-    void run_part(int k) {
-        const size_t per = ((bytes_ + parts_ - 1) / parts_ + 63) & ~size_t(63);
-        const size_t lo = per * (size_t)k;
-        if (lo < bytes_) std::memcpy(dst_ + lo, src_ + lo, std::min(per, bytes_ - lo));
-    }
     void loop(int k) {
         unsigned long long seen = 0;
         for (;;) {
+            const std::function<void(int, int)>* job;
+            int parts;
             {
                 std::unique_lock<std::mutex> lk(mu_);
                 cv_.wait(lk, [&] { return gen_ != seen; });
                 seen = gen_;
+                job = job_;
+                parts = parts_;
             }
-            run_part(k);
+            (*job)(k, parts);
             {
                 std::lock_guard<std::mutex> lk(mu_);
                 if (--pending_ == 0) done_cv_.notify_one();
@@ -630,12 +645,42 @@ class CopyPool {
     int workers_ = 0;
     std::mutex call_mu_, mu_;
     std::condition_variable cv_, done_cv_;
-    char* dst_ = nullptr;
-    const char* src_ = nullptr;
-    size_t bytes_ = 0;
+    const std::function<void(int, int)>* job_ = nullptr;
     int parts_ = 1, pending_ = 0;
     unsigned long long gen_ = 0;
 };
+
+// dst[i] = bit i of bits, i < n (the packed boolean flags, expanded on the
+// host threads)
+static void expand_bits_host(const unsigned* bits, int64_t n, int32_t* dst) {
+    const int64_t words = (n + 31) / 32;
+    auto run = [&](int64_t w0, int64_t w1) {
+        for (int64_t w = w0; w < w1; ++w) {
+            const unsigned b = bits[w];
+            int32_t* d = dst + 32 * w;
+            const int m = (int)std::min<int64_t>(32, n - 32 * w);
+            if (m == 32) {
+                for (int j = 0; j < 32; ++j) d[j] = (int32_t)((b >> j) & 1u);
+            } else {
+                for (int j = 0; j < m; ++j) d[j] = (int32_t)((b >> j) & 1u);
+            }
+        }
+    };
+    if (words < 4096) {
+        run(0, words);
+        return;
+    }
+    CopyPool::get().parallel([&](int k, int parts) {
+        const int64_t per = (words + parts - 1) / parts;
+        const int64_t w0 = per * k, w1 = std::min(words, w0 + per);
+        if (w0 < w1) run(w0, w1);
+    });
+}
+// RS_PACK_FLAGS=0: boolean flags come back as int32 (A/B)
+static const bool g_pack_flags = [] {
+    const char* e = getenv("RS_PACK_FLAGS");
+    return !(e && e[0] == '0');
+}();
 
 bool is_pageable(const void* p) {
     cudaPointerAttributes at{};
@@ -1994,7 +2039,7 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     for (int64_t lo = 0; lo < n_r; lo += chunk_rays) bounds.push_back(lo);
     if (auto_chunks && bounds.size() > 1) {
         const int64_t last = bounds.back(), rem = n_r - last;
-        const int64_t cut = ((rem * 3 / 4 + 127) / 128) * 128;
+        const int64_t cut = ((rem * 3 / 4 + 127) / 128) * 128;  // (7:1 and 15:1 measured slower)
         if (cut > 0 && cut < rem) bounds.push_back(last + cut);
     }
     bounds.push_back(n_r);
@@ -2025,7 +2070,11 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
     // one device block: mesh, 2x chunk inputs, outputs, status, tile status
     const size_t mesh_b = align256(12ull * n_v) + align256(12ull * n_t);
     const size_t in_b = 2 * 2 * align256(12ull * chunk_rays);
-    const size_t out_b = bary ? (zc ? 256 : 4 * align256(12ull * n_r)) : 2 * align256(4ull * chunk_rays);
+    // boolean flags return as bits (the PCIe D2H of 4-B flags ran beside the
+    // uploads and slowed them by ~10%); the host threads expand them
+    const bool pack = mode == kBoolean && g_pack_flags;
+    const size_t bits_b = pack ? align256(4ull * (chunk_rays / 32 + 1)) : 0;
+    const size_t out_b = bary ? (zc ? 256 : 4 * align256(12ull * n_r)) : 2 * align256(4ull * chunk_rays) + 2 * bits_b;
     const size_t tiles_b = align256(compact_scratch_bytes(chunk_rays)) * (size_t)nchunks;
     const size_t st_b = align256(sizeof(RsStatus) * (size_t)nchunks);
     // every exit (errors included) drains the pipeline's streams and
@@ -2072,6 +2121,28 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
         dflag[0] = c.take<int32_t>(chunk_rays);
         dflag[1] = c.take<int32_t>(chunk_rays);
     }
+    unsigned* dbits[2] = {nullptr, nullptr};
+    if (pack) {
+        dbits[0] = c.take<unsigned>(chunk_rays / 32 + 1);
+        dbits[1] = c.take<unsigned>(chunk_rays / 32 + 1);
+        const size_t words = (size_t)(n_r / 32) + (size_t)nchunks + 1;
+        if (g_pipe.hbits_cap < words) {
+            if (g_pipe.hbits) {
+                CK(cudaStreamSynchronize(g_pipe.copy2));  // a previous call's copies may still land
+                cudaFreeHost(g_pipe.hbits);
+            }
+            g_pipe.hbits = nullptr;
+            g_pipe.hbits_cap = 0;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&g_pipe.hbits), 4 * words, cudaHostAllocDefault));
+            g_pipe.hbits_cap = words;
+        }
+    }
+    // chunk boundaries are multiples of 128 rows: chunk k's bits start at word lo / 32
+    auto expand_chunk = [&](int64_t k) -> int {
+        CK(cudaEventSynchronize(g_pipe.ev_out[k & 1]));
+        expand_bits_host(g_pipe.hbits + chunk_lo(k) / 32, chunk_cnt(k), h_flags + chunk_lo(k));
+        return RS_OK;
+    };
     char* tiles = reinterpret_cast<char*>(c.take<char>(align256(compact_scratch_bytes(chunk_rays)) * nchunks));
     RsStatus* st = c.take<RsStatus>(nchunks);
     // Streams: s computes (build, then one query per chunk), h2d = g_pipe.copy
@@ -2212,8 +2283,13 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
             if (lq) return fail(RS_INVALID_ARG, "no kernel variant for this configuration");
             CK(cudaGetLastError());
         }
+        if (pack) launch_pack_flags(dflag[b], cnt, dbits[b], s);
         CK(cudaEventRecord(g_pipe.ev_q[b], s));
-        if (!bary) {
+        if (pack) {
+            CK(cudaStreamWaitEvent(d2h, g_pipe.ev_q[b], 0));
+            CK(cudaMemcpyAsync(g_pipe.hbits + lo / 32, dbits[b], 4ull * ((cnt + 31) / 32), cudaMemcpyDeviceToHost, d2h));
+            CK(cudaEventRecord(g_pipe.ev_out[b], d2h));
+        } else if (!bary) {
             CK(cudaStreamWaitEvent(d2h, g_pipe.ev_q[b], 0));
             CK(cudaMemcpyAsync(h_flags + lo, dflag[b], 4ull * cnt, cudaMemcpyDeviceToHost, d2h));
             CK(cudaEventRecord(g_pipe.ev_out[b], d2h));
@@ -2225,7 +2301,10 @@ static int run_batch_host_impl(const float* h_verts, int64_t n_v, const int32_t*
         }
         // the next chunk's rows into the other pinned slot while this one uploads
         if (stage_in && k + 1 < nchunks && (rc = stage_chunk(k + 1))) return rc;
+        // the previous chunk's flags, expanded while this chunk uploads
+        if (pack && k >= 1 && (rc = expand_chunk(k - 1))) return rc;
     }
+    if (pack && (rc = expand_chunk(nchunks - 1))) return rc;
     if (lagged && (rc = retire(nchunks - 1))) return rc;
     cp = d2h;
     // statuses of every chunk; barycentric row counts come back with them

@@ -206,6 +206,9 @@ struct SortedArgs {
 };
 // Writes flags[i] = bit i of hitbits for i < n (every row: no zero preset needed).
 void launch_expand_bits(int* flags, const unsigned* hitbits, long long n, cudaStream_t s);
+// bits[w] bit j = (flags[32 w + j] != 0), (n + 31) / 32 words (the host
+// pipeline returns boolean flags as bits: 32x fewer D2H bytes)
+void launch_pack_flags(const int* flags, long long n, unsigned* bits, cudaStream_t s);
 size_t sorted_bins();
 size_t bin_geom_bytes();
 bool sorted_wide();  // RS_SORTED_WIDE=1: 4-wide per-thread traversal (needs nodes4)

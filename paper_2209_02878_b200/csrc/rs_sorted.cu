@@ -1600,6 +1600,27 @@ __global__ void __launch_bounds__(256) k_expand_bits(int* __restrict__ flags, co
     }
 }
 
+// bits[w] bit j = (flags[32 w + j] != 0): one ballot per warp over 32
+// consecutive flags (128 coalesced bytes in, 4 out)
+__global__ void __launch_bounds__(256) k_pack_flags(const int* __restrict__ flags, long long n,
+                                                   unsigned* __restrict__ bits) {
+    const long long words = (n + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    for (long long w = (blockIdx.x * 256ll + threadIdx.x) >> 5; w < words; w += (gridDim.x * 256ll) >> 5) {
+        const long long i = 32 * w + lane;
+        const unsigned b = __ballot_sync(kFullMask, i < n && __ldg(flags + i) != 0);
+        if (lane == 0) bits[w] = b;
+    }
+}
+
+void launch_pack_flags(const int* flags, long long n, unsigned* bits, cudaStream_t s) {
+    if (n <= 0) return;
+    const long long want = ((n + 31) / 32 * 32 + 255) / 256;
+    const long long cap = (long long)sm_total() * 8;
+    count_launches(1);
+    k_pack_flags<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(flags, n, bits);
+}
+
 void launch_expand_bits(int* flags, const unsigned* hitbits, long long n, cudaStream_t s) {
     if (n <= 0) return;
     const long long want = (n / 4 + 255) / 256 + 1;

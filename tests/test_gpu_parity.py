@@ -410,6 +410,25 @@ def test_host_pipeline_chunking(mode, chunk):
     assert_result_fields(result_dict(got), expected(fx, "batch", mode), f"chunk {chunk}")
 
 
+@pytest.mark.parametrize("pageable", [False, True], ids=["pinned", "pageable"])
+def test_host_boolean_flags_packed(pageable):
+    """Boolean flags cross PCIe as bits (k_pack_flags, 32 flags per word)
+    and the host threads expand them into the int32 result, chunk by chunk
+    behind the uploads: a 3M-segment batch (4 chunks + split tail, a ragged
+    last word) against the generator's ground truth, from pinned and from
+    plain numpy inputs (the staged path)."""
+    sc = rs.generate_scene(29_284, 3_000_017, 0.5, seed=5)
+    s, e = sc.segments.starts, sc.segments.ends
+    if not pageable:
+        import torch
+
+        s = torch.from_numpy(s).pin_memory().numpy()
+        e = torch.from_numpy(e).pin_memory().numpy()
+    got = rs.run_batch(sc.mesh, rs.SegmentBatch.from_arrays(s, e), rs.EngineConfig(mode="boolean"))
+    assert got.crossing.dtype == np.int32
+    assert np.array_equal(got.crossing, sc.expected_crossings.astype(np.int32))
+
+
 @pytest.mark.parametrize("chunk", [0, 1000])
 def test_host_pipeline_pageable_outputs(chunk):
     """rs_run_batch_host with plain (pageable) numpy outputs: barycentric rows
