@@ -569,13 +569,13 @@ def main():
                 t0 = time.perf_counter()
                 r = rs.run_batch(mesh_x, seg_x, config)
                 ts.append(time.perf_counter() - t0)
-            tt = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=cdev)
+            tt = torch.tensor([float(np.median(ts))], dtype=torch.float64, device=cdev)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             return tt.item(), r
 
         t_pin, r = e2e_time(mesh_p, seg_p, max(3, min(args.steps // 4, 25)))
-        t_pg, _ = e2e_time(mesh_h, seg_pg, 3)
+        t_pg, _ = e2e_time(mesh_h, seg_pg, 7)
         h2d = 24 * m + 12 * mesh_h.num_vertices + 12 * mesh_h.num_triangles
         # boolean flags cross PCIe packed 32 per word (expanded to the int32
         # result on the host threads); count returns int32 counts
