@@ -158,8 +158,15 @@ __device__ __forceinline__ void root_info_compute(const RsHeader* hdr, const Sor
     // total bits: about a.bin_occupancy live segments per bin, so the bins'
     // open output lines stay L2-resident during the scatter
     const double live = (double)a.n_r * (st[3] / (float)(kSampleCtas * kSampleThreads));
+    // stacked surfaces (depth complexity, projected triangle-box area over
+    // the root box's, above 6): proportionally finer bins, since a tile's
+    // candidate list holds every layer under its records (C4, depth 12.8:
+    // 1.79 -> 1.54 ms; the single terrains C2/C5 sit at 3.2-3.4)
+    const float ra = e0 * e1 + e1 * e2 + e2 * e0;
+    const float depth = ra > 0.f ? __ldg(&hdr->parea) / ra : 0.f;
+    const double occ = depth > 6.f ? fmax(1.0, (double)a.bin_occupancy * 6.0 / depth) : (double)a.bin_occupancy;
     int nbits = 0;
-    while (nbits < kBinBits && (double)(1u << (nbits + 1)) * a.bin_occupancy <= live) ++nbits;
+    while (nbits < kBinBits && (double)(1u << (nbits + 1)) * occ <= live) ++nbits;
     nbits = nbits < 8 ? 8 : nbits;
     ri.nbits = nbits;
     float c0 = e0, c1 = e1, c2 = e2;
@@ -1286,7 +1293,9 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) k_trav_tile(Sort
         const float ra = r[0] * r[1] + r[1] * r[2] + r[2] * r[0];
         const float depth = ra > 0.f ? __ldg(&a.hdr->parea) / ra : 0.f;
         if (depth > 1.f) {
-            const float cap = (float)a.tile_depth / depth;
+            // cap = tile_depth / depth^1.5 (sweeps: C4, depth 12.8, best at
+            // 256-record tiles; C5, depth 3.4, at ~2048; C2's 512 uncapped)
+            const float cap = (float)a.tile_depth / (depth * sqrtf(depth));
             T = (float)T < cap ? T : (unsigned)cap;
         }
     }
@@ -1504,7 +1513,7 @@ struct SortedOpts {
     unsigned tile_density = 16;  // auto: tiles when segments >= this x triangles
     unsigned tile_balance = 8;   // at least this many tiles per CTA
     unsigned tile_area = 48;     // about this many triangles' worth of records per tile
-    unsigned tile_depth = 4900;  // and at most this / depth-complexity records (0: off)
+    unsigned tile_depth = 11000; // and at most this / depth-complexity^1.5 records (0: off)
     unsigned bin_occ = 16;       // target live segments per spatial bin
     int bin_tma = 1;             // binning passes stream through TMA bulk copies
     int tile_wide = 0;           // tile walk over the collapsed 4-wide nodes (A/B: no gain on C2)
