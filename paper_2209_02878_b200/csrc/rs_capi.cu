@@ -817,6 +817,7 @@ struct FastScratch {
     float4* rec = nullptr;
     void* geom = nullptr;
     unsigned* hitbits = nullptr;  // large boolean batches: hit bitmap (see SortedArgs::hitbits)
+    bool leaf_of_ready = false;   // barycentric: the tree's leaf_of inverse already built
 };
 
 // Boolean batches from this many segments on set hit bits instead of
@@ -934,7 +935,7 @@ static int fast_trav(const rs_tree* t, const float* d_s, const float* d_e, int64
     launch_sorted_trav(sorted_args(t, d_s, d_e, n_r, o, f), mode, stats, s);
     if (f.hitbits) launch_expand_bits(o.flags, f.hitbits, n_r, s);
     if (mode == kBarycentric) {
-        if (!f.best_t)  // the compaction recomputes t from the winning leaf
+        if (!f.best_t && !f.leaf_of_ready)  // the compaction recomputes t from the winning leaf
             launch_leaf_inverse(t->leaves, (int)t->n, t->leaf_of, s);
         CompactArgs ca{n_r, f.best_t, f.best_tri, d_s, d_e, o.c_ray, o.c_dist, o.c_tri, o.c_pt,
                        f.tiles, f.tile_ctr, &f.st->hits, o.ray_offset, o.row_base, t->leaves, t->leaf_of,
@@ -1404,6 +1405,11 @@ static int enqueue_fast_forked(const float* d_verts, int64_t n_v, const int32_t*
     rc = build_impl(d_verts, n_v, d_tris, n_t, kTreeFast, nullptr, nullptr, bs, &t, fork, true);
     if (rc) return rc;
     if (const long long ns = debug_delay_ns("RS_DEBUG_DELAY_BUILD_US")) k_debug_spin<<<1, 1, 0, bs>>>(ns);
+    if (mode == kBarycentric && !f.best_t) {  // off the traversal's stream: beside the binning
+        launch_leaf_inverse(t->leaves, (int)t->n, t->leaf_of, bs);
+        f.leaf_of_ready = true;
+        if (two) f2.leaf_of_ready = true;
+    }
     if (bs != s) {
         CK(cudaEventRecord(g_fork.built, bs));
         CK(cudaStreamWaitEvent(s, g_fork.built, 0));

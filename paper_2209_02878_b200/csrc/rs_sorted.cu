@@ -36,7 +36,10 @@ constexpr unsigned kFullMask = 0xffffffffu;
 // up to 512k spatial bins: the scatter's open output lines (one 128-B line
 // per bin) stay within half of L2 (1B-segment C5: 2M bins took the scatter
 // from 13 to 17 ms; C2-C4 use 2^18-2^19 bins anyway)
-constexpr int kBinBits = 19;
+#ifndef RS_BIN_BITS
+#define RS_BIN_BITS 19
+#endif
+constexpr int kBinBits = RS_BIN_BITS;
 constexpr int kSampleCtas = 32;              // k_seg_sample grid
 constexpr int kSampleThreads = 128;
 constexpr int kBins = 1 << kBinBits;
