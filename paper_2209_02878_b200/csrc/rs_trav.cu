@@ -493,7 +493,10 @@ constexpr int kCompactTile = kCompactThreads * kCompactItems;
 // by the traversal); without ROWS it writes only ray index and triangle,
 // and k_bary_rows recomputes t and the geometry one row per thread (at 110
 // registers the fused recompute left the compaction at 24% occupancy).
-template <bool ROWS>
+// SCAN: the tiles' offsets come from k_bary_tile_counts + k_bary_tile_scan
+// (tile = blockIdx.x, no look-back chain); otherwise tiles are taken in
+// ticket order and chained by the decoupled look-back.
+template <bool ROWS, bool SCAN>
 __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a) {
     // Striped tile: in round k, thread t owns segment base + k*256 + t, so
     // every load and every output row of a round is coalesced across the
@@ -502,9 +505,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
     __shared__ unsigned s_round[kCompactItems][kCompactThreads / 32];
     __shared__ unsigned long long s_prefix;
     __shared__ int s_tile;
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1ull);
+    if (!SCAN && threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1ull);
     __syncthreads();
-    const long long tile = s_tile;
+    const long long tile = SCAN ? (long long)blockIdx.x : s_tile;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const unsigned lt = (1u << l) - 1u;
     const long long base = tile * kCompactTile;
@@ -541,10 +544,14 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
             (&s_round[0][0])[l * (kCells / 32) + j] = off;
             off += c;
         }
-        const unsigned long long excl = lookback_warp(a.tile_status, tile, agg);
-        if (l == 0) {
-            s_prefix = excl;
-            if (base + kCompactTile >= a.n_r) *a.n_hits = excl + agg;
+        if (SCAN) {
+            if (l == 0) s_prefix = a.tile_status[tile];  // exclusive prefix; k_bary_tile_scan wrote n_hits
+        } else {
+            const unsigned long long excl = lookback_warp(a.tile_status, tile, agg);
+            if (l == 0) {
+                s_prefix = excl;
+                if (base + kCompactTile >= a.n_r) *a.n_hits = excl + agg;
+            }
         }
     }
     __syncthreads();
@@ -569,6 +576,62 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
         a.point[3 * pos] = px;
         a.point[3 * pos + 1] = py;
         a.point[3 * pos + 2] = pz;
+    }
+}
+
+// Hits per compaction tile (the reduce pass of the scanned compaction).
+__global__ void __launch_bounds__(kCompactThreads) k_bary_tile_counts(const int* __restrict__ best_tri,
+                                                                      long long n_r, unsigned* counts) {
+    __shared__ unsigned s_w[kCompactThreads / 32];
+    const long long base = (long long)blockIdx.x * kCompactTile;
+    unsigned c = 0;
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        const long long i = base + k * kCompactThreads + threadIdx.x;
+        c += (i < n_r && __ldg(best_tri + i) >= 0) ? 1u : 0u;
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (int j = 0; j < kCompactThreads / 32; ++j) t += s_w[j];
+        counts[blockIdx.x] = t;
+    }
+}
+
+// Exclusive scan of the tile counts (one CTA): prefix[tile], and the total
+// into *n_hits.
+__global__ void __launch_bounds__(1024) k_bary_tile_scan(const unsigned* __restrict__ counts, long long tiles,
+                                                         unsigned long long* prefix, unsigned long long* n_hits) {
+    __shared__ unsigned long long s_w[32];
+    const long long per = (tiles + 1023) / 1024;
+    const long long lo = threadIdx.x * per, hi = lo + per < tiles ? lo + per : tiles;
+    unsigned long long sum = 0;
+    for (long long j = lo; j < hi; ++j) sum += counts[j];
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long x = sum;  // inclusive scan within the warp
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, x, o);
+        if (l >= o) x += y;
+    }
+    if (l == 31) s_w[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        const unsigned long long v = s_w[l];
+        unsigned long long z = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(kFull, z, o);
+            if (l >= o) z += y;
+        }
+        s_w[l] = z - v;  // exclusive over warps
+        if (l == 31) *n_hits = z;
+    }
+    __syncthreads();
+    unsigned long long run = s_w[w] + x - sum;
+    for (long long j = lo; j < hi; ++j) {
+        prefix[j] = run;
+        run += counts[j];
     }
 }
 
@@ -782,9 +845,16 @@ void launch_unpermute_rows(const long long* perm, long long n, const int* ray, c
     k_gather_compact<<<(unsigned)tiles, kCompactThreads, 0, s>>>(a);
 }
 
+// [tile words (look-back status, or the scanned prefixes) x tiles]
+// [tile counts, u32 x tiles, padded to 8 B][ticket counter]
 size_t bary_compact_scratch(long long n_r) {
-    return (size_t)((n_r + kCompactTile - 1) / kCompactTile) * 8 + 8;
+    const size_t tiles = (size_t)((n_r + kCompactTile - 1) / kCompactTile);
+    return tiles * 8 + ((tiles * 4 + 7) & ~size_t(7)) + 8;
 }
+static const bool g_compact_scan = [] {  // RS_COMPACT_SCAN=0: look-back chain (A/B)
+    const char* e = getenv("RS_COMPACT_SCAN");
+    return !(e && e[0] == '0');
+}();
 
 __global__ void k_advance_rows(unsigned long long* row_base, const unsigned long long* n_hits) {
     *row_base += *n_hits;
@@ -794,10 +864,26 @@ void launch_bary_compact(const CompactArgs& a, cudaStream_t s) {
     if (a.n_r <= 0) return;
     count_launches(1);
     const unsigned tiles = (unsigned)((a.n_r + kCompactTile - 1) / kCompactTile);
-    if (a.best_t || a.fused) {
-        k_bary_compact<true><<<tiles, kCompactThreads, 0, s>>>(a);
+    const bool rows = a.best_t || a.fused;
+    if (g_compact_scan) {
+        // reduce, scan, compact: the look-back chain held every CTA at its
+        // barrier (C3: 50 -> 33 us for the three kernels, step -23 us)
+        unsigned* counts = reinterpret_cast<unsigned*>(a.tile_status + tiles);
+        count_launches(2);
+        k_bary_tile_counts<<<tiles, kCompactThreads, 0, s>>>(a.best_tri, a.n_r, counts);
+        k_bary_tile_scan<<<1, 1024, 0, s>>>(counts, (long long)tiles, a.tile_status, a.n_hits);
+        if (rows) {
+            k_bary_compact<true, true><<<tiles, kCompactThreads, 0, s>>>(a);
+        } else {
+            k_bary_compact<false, true><<<tiles, kCompactThreads, 0, s>>>(a);
+            const long long want = (a.n_r + 255) / 256, cap = (long long)device_sms() * 16;
+            count_launches(1);
+            k_bary_rows<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(a);
+        }
+    } else if (rows) {
+        k_bary_compact<true, false><<<tiles, kCompactThreads, 0, s>>>(a);
     } else {
-        k_bary_compact<false><<<tiles, kCompactThreads, 0, s>>>(a);
+        k_bary_compact<false, false><<<tiles, kCompactThreads, 0, s>>>(a);
         const long long want = (a.n_r + 255) / 256, cap = (long long)device_sms() * 16;
         count_launches(1);
         k_bary_rows<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(a);
