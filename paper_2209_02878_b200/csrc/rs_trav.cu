@@ -15,8 +15,8 @@
 //                 barycentric atomicMin on the t key.
 //   k_tiebreak    barycentric: among hits with t == min t, atomicMin of the
 //                 triangle id (_core.pyx:317-320 (t, tid) order).
-//   k_bary_compact ordered compaction of barycentric rows (decoupled
-//                 look-back), point/distance computed from the winning t.
+//   k_bary_compact ordered compaction of barycentric rows (per-tile counts,
+//                 one-CTA scan, placement), point/distance from the winning t.
 //
 // Candidates are staged per warp in shared memory and written 32 at a time
 // behind one atomicAdd, so the buffer is dense (no gaps).  Capacity: the
@@ -453,9 +453,9 @@ __global__ void __launch_bounds__(256) k_tiebreak(ExactArgs a) {
 
 // Ordered barycentric compaction over segments (engine.py:206-215): each CTA
 // owns a tile of kCompactItems x 256 segments, block-scans the hit flags,
-// chains tiles with a warp-parallel decoupled look-back, and writes its rows
-// at their final ascending positions with point/distance computed from the
-// winning t in reference op order (_core.pyx:330-348).
+// takes its tile's offset from the scanned per-tile counts, and writes its
+// rows at their final ascending positions with point/distance computed from
+// the winning t in reference op order (_core.pyx:330-348).
 constexpr int kCompactThreads = 256;
 
 // The winning hit's t: stored by the traversal (best_t), or recomputed from
@@ -493,10 +493,10 @@ constexpr int kCompactTile = kCompactThreads * kCompactItems;
 // by the traversal); without ROWS it writes only ray index and triangle,
 // and k_bary_rows recomputes t and the geometry one row per thread (at 110
 // registers the fused recompute left the compaction at 24% occupancy).
-// SCAN: the tiles' offsets come from k_bary_tile_counts + k_bary_tile_scan
-// (tile = blockIdx.x, no look-back chain); otherwise tiles are taken in
-// ticket order and chained by the decoupled look-back.
-template <bool ROWS, bool SCAN>
+// The tiles' offsets come from k_bary_tile_counts + k_bary_tile_scan (a
+// decoupled look-back chain across the tiles held every CTA at its barrier:
+// C3 50 -> 33 us for the three kernels).
+template <bool ROWS>
 __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a) {
     // Striped tile: in round k, thread t owns segment base + k*256 + t, so
     // every load and every output row of a round is coalesced across the
@@ -504,10 +504,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
     // lower threads in its round (ballots + a warp-sum scan per round).
     __shared__ unsigned s_round[kCompactItems][kCompactThreads / 32];
     __shared__ unsigned long long s_prefix;
-    __shared__ int s_tile;
-    if (!SCAN && threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1ull);
-    __syncthreads();
-    const long long tile = SCAN ? (long long)blockIdx.x : s_tile;
+    const long long tile = blockIdx.x;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const unsigned lt = (1u << l) - 1u;
     const long long base = tile * kCompactTile;
@@ -544,15 +541,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_bary_compact(CompactArgs a)
             (&s_round[0][0])[l * (kCells / 32) + j] = off;
             off += c;
         }
-        if (SCAN) {
-            if (l == 0) s_prefix = a.tile_status[tile];  // exclusive prefix; k_bary_tile_scan wrote n_hits
-        } else {
-            const unsigned long long excl = lookback_warp(a.tile_status, tile, agg);
-            if (l == 0) {
-                s_prefix = excl;
-                if (base + kCompactTile >= a.n_r) *a.n_hits = excl + agg;
-            }
-        }
+        (void)agg;
+        if (l == 0) s_prefix = a.tile_status[tile];  // exclusive prefix; k_bary_tile_scan wrote n_hits
     }
     __syncthreads();
     const unsigned long long tb = s_prefix + (a.row_base ? *a.row_base : 0ull);
@@ -851,10 +841,7 @@ size_t bary_compact_scratch(long long n_r) {
     const size_t tiles = (size_t)((n_r + kCompactTile - 1) / kCompactTile);
     return tiles * 8 + ((tiles * 4 + 7) & ~size_t(7)) + 8;
 }
-static const bool g_compact_scan = [] {  // RS_COMPACT_SCAN=0: look-back chain (A/B)
-    const char* e = getenv("RS_COMPACT_SCAN");
-    return !(e && e[0] == '0');
-}();
+
 
 __global__ void k_advance_rows(unsigned long long* row_base, const unsigned long long* n_hits) {
     *row_base += *n_hits;
@@ -862,28 +849,16 @@ __global__ void k_advance_rows(unsigned long long* row_base, const unsigned long
 
 void launch_bary_compact(const CompactArgs& a, cudaStream_t s) {
     if (a.n_r <= 0) return;
-    count_launches(1);
     const unsigned tiles = (unsigned)((a.n_r + kCompactTile - 1) / kCompactTile);
     const bool rows = a.best_t || a.fused;
-    if (g_compact_scan) {
-        // reduce, scan, compact: the look-back chain held every CTA at its
-        // barrier (C3: 50 -> 33 us for the three kernels, step -23 us)
-        unsigned* counts = reinterpret_cast<unsigned*>(a.tile_status + tiles);
-        count_launches(2);
-        k_bary_tile_counts<<<tiles, kCompactThreads, 0, s>>>(a.best_tri, a.n_r, counts);
-        k_bary_tile_scan<<<1, 1024, 0, s>>>(counts, (long long)tiles, a.tile_status, a.n_hits);
-        if (rows) {
-            k_bary_compact<true, true><<<tiles, kCompactThreads, 0, s>>>(a);
-        } else {
-            k_bary_compact<false, true><<<tiles, kCompactThreads, 0, s>>>(a);
-            const long long want = (a.n_r + 255) / 256, cap = (long long)device_sms() * 16;
-            count_launches(1);
-            k_bary_rows<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(a);
-        }
-    } else if (rows) {
-        k_bary_compact<true, false><<<tiles, kCompactThreads, 0, s>>>(a);
+    unsigned* counts = reinterpret_cast<unsigned*>(a.tile_status + tiles);
+    count_launches(3);
+    k_bary_tile_counts<<<tiles, kCompactThreads, 0, s>>>(a.best_tri, a.n_r, counts);
+    k_bary_tile_scan<<<1, 1024, 0, s>>>(counts, (long long)tiles, a.tile_status, a.n_hits);
+    if (rows) {
+        k_bary_compact<true><<<tiles, kCompactThreads, 0, s>>>(a);
     } else {
-        k_bary_compact<false, false><<<tiles, kCompactThreads, 0, s>>>(a);
+        k_bary_compact<false><<<tiles, kCompactThreads, 0, s>>>(a);
         const long long want = (a.n_r + 255) / 256, cap = (long long)device_sms() * 16;
         count_launches(1);
         k_bary_rows<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(a);
