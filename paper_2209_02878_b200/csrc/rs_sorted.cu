@@ -5,21 +5,24 @@
 // 128-B line (L1-wavefront bound).  So the query first reorders the segments
 // spatially with a two-pass counting sort, fused with root culling:
 //
-//   k_bin_count    per segment: f32 AABB (engine.py:115-122), test against the
-//                  root's children (a segment overlapping none of them has no
-//                  candidates: its result is the pre-zeroed default and it is
-//                  dropped here), 21-bit isotropic Morton key of the box centre
-//                  over the root box, warp-aggregated histogram atomics.
-//   k_tile_scan +  two-level exclusive scan of the 2M bins.
-//   k_bin_scan
-//   k_bin_scatter  same key; each live segment's record (start, id, end; 32 B)
-//                  goes to its bin.
-//   k_trav_sorted  one thread per record, in bin order: stack traversal of the
-//                  4-wide BVH (four 256-bit slot loads per visit, exact f32
-//                  box tests), f64 Moller-Trumbore at the leaves in reference
-//                  op order, boolean early exit, result written to the
-//                  segment's original row.  Lanes of a warp hold spatially
-//                  adjacent segments, so their node loads coalesce.
+//   k_seg_sample     box statistics of 4096 sampled segments; its last CTA
+//                    derives the bin geometry (bits per axis, key tables) once
+//                    for the call (root box, sample, depth complexity).
+//   k_bin_count_tma  per segment, streamed through shared memory by TMA bulk
+//                    copies: f32 AABB (engine.py:115-122), root-box cull (a
+//                    segment outside it has no candidates: its result is the
+//                    pre-zeroed default and it is dropped), Morton key of the
+//                    box centre (up to 2^19 bins), histogram reductions.
+//   k_bin_scan1      single-pass exclusive scan of the active bins.
+//   k_bin_scatter    same key; each live segment's record (start, id, end;
+//                    32 B) goes to its bin's next slot.
+//   k_trav_tile      tiles of consecutive records (a small region): the
+//                    tile's candidate list from a Morton key range or a walk
+//                    of the tree, filtered per warp and per lane, then the f64
+//                    Moller-Trumbore test at the candidates in reference op
+//                    order, results written to the segments' original rows.
+//   k_trav_sorted_bin / k_trav_sorted: per-record stack walks (sparse batches,
+//                    tiles whose lists overflow, statistics).
 //
 // Results do not depend on the order: boolean = any, count = sum, barycentric
 // = min over (t, triangle id) (_core.pyx:304-322).
