@@ -12,7 +12,8 @@
 //   k_climb     Apetrei single-pass climb (lbvh.py:198-233, _core.pyx:148-184):
 //               write child/range, release fence, acq_rel visit counter; the
 //               second arriver unions the children and also emits the packed
-//               64-B RsNode the traversal reads.
+//               64-B RsNode the traversal reads.  k_climb_lean: the same climb
+//               for query-only fast trees, writing only the RsNode records.
 #include <cuda/atomic>
 
 #include "rs_common.cuh"

@@ -1,6 +1,9 @@
-// rs_trav.cu -- the fast-tree hot path: 4-lane group traversal of the 4-wide
-// BVH that emits (segment, leaf) candidates into a collision buffer, then a
-// SIMD-dense exact-test pass over the buffer.
+// rs_trav.cu -- the collision-buffer path (option fast_path=1, north_star's
+// buffer manager; the default hot path is the tile traversal in
+// rs_sorted.cu): 4-lane group traversal of the 4-wide BVH that emits
+// (segment, leaf) candidates into a collision buffer, then a SIMD-dense
+// exact-test pass over the buffer.  Also the barycentric compaction and the
+// sort_rays un-permutation that every path uses.
 //
 //   k_trav_quad   one segment per 4-lane group, one child slot per lane: a
 //                 node visit is one 256-bit load per lane (the group reads one
